@@ -1,0 +1,73 @@
+// ds_blend.cuh — device dual-quaternion blending of a K<=4 skinning entry.
+//   blend_dual_quaternions  geometry.cpp:127-147 (raw Gaussian weights, sign fix
+//                           against slot 0, degenerate if |sum real| < 1e-8)
+//   make_blend_state        solver.cpp:31-49 (signed weights kept for Jacobians)
+#pragma once
+#include "ds_math.cuh"
+
+namespace ds {
+
+struct Blend {
+  Q4 rs, ds;
+  double sw[4];
+  int idx[4];
+  int count;
+  bool degenerate;
+};
+
+__device__ __forceinline__ int entry_count(int4 ki) {
+  return ki.x < 0 ? 0 : (ki.y < 0 ? 1 : (ki.z < 0 ? 2 : (ki.w < 0 ? 3 : 4)));
+}
+
+__device__ __forceinline__ Q4 ld_q(const double4* __restrict__ p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return q4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ Q4 ld_q_plain(const double4* p) {
+  const double4 v = *p;
+  return q4(v.x, v.y, v.z, v.w);
+}
+
+// node_dq holds 2 double4 per node: real (w,x,y,z), dual (w,x,y,z)
+__device__ __forceinline__ Blend blend_entry(int4 ki, float4 kw, const double4* __restrict__ node_dq) {
+  Blend b;
+  b.rs = q4(0, 0, 0, 0);
+  b.ds = q4(0, 0, 0, 0);
+  b.idx[0] = ki.x;
+  b.idx[1] = ki.y;
+  b.idx[2] = ki.z;
+  b.idx[3] = ki.w;
+  const double w4[4] = {(double)kw.x, (double)kw.y, (double)kw.z, (double)kw.w};
+  b.count = entry_count(ki);
+  b.degenerate = true;
+  if (b.count == 0) return b;
+  const Q4 pivot = ld_q(node_dq + 2 * b.idx[0]);
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    b.sw[m] = 0.0;
+    if (m < b.count) {
+      const Q4 r = ld_q(node_dq + 2 * b.idx[m]);
+      const Q4 d = ld_q(node_dq + 2 * b.idx[m] + 1);
+      const double sign = (qdot(pivot, r) < 0.0) ? -1.0 : 1.0;
+      const double w = sign * w4[m];
+      b.sw[m] = w;
+      b.rs = qadd(b.rs, qscl(w, r));
+      b.ds = qadd(b.ds, qscl(w, d));
+    }
+  }
+  b.degenerate = qnrm(b.rs) < kDegenerateBlend;
+  return b;
+}
+
+// Rigid transform of a non-degenerate blend: normalized() then to_se3()
+// (which normalizes again), as blend_dual_quaternions + to_se3 do.
+__device__ __forceinline__ Rig blend_rig(const Blend& b) {
+  DQ raw;
+  raw.r = b.rs;
+  raw.d = b.ds;
+  return dq_to_rig(dq_normalized(raw));
+}
+
+}  // namespace ds

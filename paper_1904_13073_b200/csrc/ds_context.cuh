@@ -1,0 +1,292 @@
+// ds_context.cuh — device-resident state of one sequence and the host-side
+// stage entry points (implemented across the k_*.cu translation units).
+//
+// HBM layout (per context, one sequence, one stream):
+//   surfels   SoA, double-buffered for stable compaction (fusion.cpp:264-284)
+//             ref_pr/live_pr float4 (x,y,z,radius), ref_nc/live_nc float4
+//             (nx,ny,nz,confidence), t int2 (t_init,t_observed), knn int4 +
+//             w float4 (K=4 skinning, -1 = empty slot)            104 B/surfel
+//   nodes     pos double4 (x,y,z,sigma), dq 2 x double4 (real, dual), nbr int[8],
+//             se3 cache double[12] (per GN iteration)
+//   frame     depth u16, vert/nrm double4 (x,y,z,radius)/(n,confidence), flags u8
+//   maps      model-map point/splat keys (fp64 depth bits) + index, index map
+//             (supersampled W*f x H*f) keys + index
+//   solver    per-pixel pair slot (surfel, 4x6 fp32 Jacobian rows, fp64 residual),
+//             per-surfel pair lists, term->block records sorted per frame,
+//             BSR 6x6 fp32 blocks, PCG vectors fp64
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/dynsurf_b200.h"
+#include "ds_math.cuh"
+
+namespace ds {
+
+struct Error {
+  ds_status code;
+  std::string msg;
+};
+[[noreturn]] void fail(ds_status code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define DS_CUDA(call) ::ds::cuda_check((call), #call)
+
+enum KernelKind {
+  KK_FRAME_MAPS = 0,
+  KK_FORWARD_WARP,
+  KK_COMPACT_INVERSE_WARP,
+  KK_MODEL_MAP_SPLAT,
+  KK_ASSOCIATE,
+  KK_INDEX_MAP,
+  KK_PAIR_TERMS,
+  KK_PAIR_LISTS,
+  KK_PATTERN,
+  KK_BLOCK_ASSEMBLY,
+  KK_PCG,
+  KK_NODE_UPDATE,
+  KK_ENERGY,
+  KK_REDUCE,
+  KK_RIGID,
+  KK_FUSE,
+  KK_SKIN_APPEND,
+  KK_REMOVE,
+  KK_GREEDY_NODES,
+  KK_NODE_EDGES,
+  KK_SKIN_KNN,
+  KK_SKIN_INCREMENTAL,
+  KK_SCAN,
+  KK_MISC,
+  KK_COUNT
+};
+extern const char* kKernelNames[KK_COUNT];
+
+struct ModelBuf {
+  float4* rp = nullptr;  // reference (x,y,z,radius)
+  float4* rn = nullptr;  // reference (nx,ny,nz,confidence)
+  float4* lp = nullptr;  // live
+  float4* ln = nullptr;
+  int2* t = nullptr;     // (t_init, t_observed), shared by both arrays
+  int4* ki = nullptr;    // skinning node indices (-1 empty)
+  float4* kw = nullptr;  // skinning weights
+};
+
+// Small device-side scalars read back once per sync point.
+struct DevScalars {
+  int valid_count, degenerate, any_stable, n_pairs;
+  int n_pairs_ok, fused, n_cand, n_accept;
+  int low_support, comp_rejected, removed, n_keep;
+  int n_nodes, n_new_nodes, err, finite;
+  int up_blocks, full_blocks, pcg_iters, mean_cnt;
+  int rigid_pairs, rigid_low, n_records, survivors;
+  double e_data, e_reg, ginf, htrace;
+  double pcg_rr, pcg_rr0, mean_abs_r, rigid_abs;
+  double rigid_pose[12];
+};
+
+enum DevErr { DERR_NODE_CAP = 1, DERR_HASH_CELL = 2, DERR_HASH_FULL = 4, DERR_BLOCK_CAP = 8 };
+
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+
+struct Ctx {
+  ds_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  int W = 0, H = 0, P = 0;
+  int S_cap = 0, N_cap = 0, R_cap = 0, UB_cap = 0, B_cap = 0, HT = 0;
+
+  // model
+  ModelBuf mb[2];
+  int cur = 0;
+  int n_surfels = 0;
+  // nodes
+  int n_nodes = 0;
+  double4* node_pos = nullptr;
+  double4* node_dq = nullptr;
+  double4* node_dq_cand = nullptr;
+  int* node_nbr = nullptr;
+  double* node_se3 = nullptr;
+  double* node_se3_cand = nullptr;
+  double4* node_live = nullptr;
+  // frame
+  uint16_t* depth = nullptr;
+  uint16_t* depth_f = nullptr;
+  double4* f_vert = nullptr;
+  double4* f_nrm = nullptr;
+  uint8_t* f_flag = nullptr;  // bit0 vertex_valid, bit1 valid
+  int frame_index = 0;
+  int valid_count = 0;
+  bool frame_ready = false;
+  // model maps
+  unsigned long long* mm_pkey = nullptr;
+  unsigned long long* mm_skey = nullptr;
+  int* mm_pidx = nullptr;
+  int* mm_sidx = nullptr;
+  int* mm_idx = nullptr;
+  double mm_pose[12];
+  bool mm_ready = false;
+  // supersampled index map
+  unsigned long long* im_key = nullptr;
+  int* im_idx = nullptr;
+  int im_factor = 0;
+  double im_pose[12];
+  bool im_ready = false;
+  // pairs / surfel lists
+  int* pair_s = nullptr;     // per pixel: surfel or -1
+  uint8_t* pair_ok = nullptr;
+  float* pair_rows = nullptr;  // per pixel 4 x 6
+  double* pair_r = nullptr;
+  int* s_cnt = nullptr;
+  int* s_off = nullptr;
+  int* s_cur = nullptr;
+  int* s_list = nullptr;
+  // term -> block records and BSR
+  int* rec_key = nullptr;
+  int* rec_val = nullptr;
+  int* rec_key2 = nullptr;
+  int* rec_val2 = nullptr;
+  int* rec_flag = nullptr;
+  int* up_key = nullptr;
+  int* up_start = nullptr;
+  int* up_pos = nullptr;
+  int* up_mpos = nullptr;
+  int* row_ptr = nullptr;
+  int* row_cnt = nullptr;
+  int* bsr_col = nullptr;
+  int* bsr_tag = nullptr;  // upper block id << 1 | mirrored
+  float* bsr_val = nullptr;
+  uint8_t* bsr_touch = nullptr;
+  int* diag_pos = nullptr;
+  int n_records = 0, n_up = 0, n_full = 0;
+  bool pattern_ready = false;
+  void* cub_tmp = nullptr;
+  size_t cub_tmp_bytes = 0;
+  // PCG
+  double* g = nullptr;
+  double* pcg_x = nullptr;
+  double* pcg_r = nullptr;
+  double* pcg_z = nullptr;
+  double* pcg_p0 = nullptr;
+  double* pcg_p1 = nullptr;
+  double* pcg_q = nullptr;
+  double* pcg_minv = nullptr;
+  double* pcg_part = nullptr;
+  int pcg_grid = 0;
+  // fusion
+  int* cand_flag = nullptr;
+  int* cand_scan = nullptr;
+  int* cand_pix = nullptr;
+  float4* cand_p = nullptr;
+  float4* cand_n = nullptr;
+  int4* cand_ki = nullptr;
+  float4* cand_kw = nullptr;
+  int* cand_ok = nullptr;
+  int* cand_ok_scan = nullptr;
+  int* keep = nullptr;
+  int* keep_scan = nullptr;
+  // greedy node hash
+  long long* ht_key = nullptr;
+  int* ht_cnt = nullptr;
+  int* ht_ids = nullptr;
+  // scratch
+  int* scan_tmp = nullptr;
+  int scan_tmp_n = 0;
+  double* red_part = nullptr;
+  int red_part_n = 0;
+  double* d_pose = nullptr;  // 12 doubles
+  DevScalars* dsc = nullptr;
+  DevScalars* hsc = nullptr;  // pinned mirror
+  uint16_t* h_depth_pinned = nullptr;
+
+  // host pipeline state (Pipeline, pipeline.hpp:52-59)
+  double pose[12];
+  bool initialized = false;
+  int t_last_reinit = 0;
+  std::deque<double> win_residual;
+  std::deque<int> win_appended;
+
+  // accounting
+  int64_t launches[KK_COUNT] = {0};
+  double prof_ms[KK_COUNT] = {0};
+  double prof_bytes[KK_COUNT] = {0};
+  int64_t total_launches = 0;
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::vector<void*> allocations;
+  // per-frame extras
+  int lm_attempts = 0, pcg_iterations = 0;
+
+  ModelBuf& M() { return mb[cur]; }
+  ModelBuf& Malt() { return mb[cur ^ 1]; }
+};
+
+// ---- launch accounting (every kernel of the library goes through these)
+void launch_begin(Ctx& c, int kind);
+void launch_end(Ctx& c, int kind, double bytes);
+void prof_flush(Ctx& c);
+#define DS_LAUNCH(ctx, kind, bytes, grid, block, smem, kernel, ...)        \
+  do {                                                                     \
+    ::ds::launch_begin((ctx), (kind));                                     \
+    kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);        \
+    ::ds::launch_end((ctx), (kind), (double)(bytes));                      \
+  } while (0)
+
+inline int cdiv(long long a, long long b) { return int((a + b - 1) / b); }
+void sync(Ctx& c);                   // stream sync + profile flush
+void fetch_scalars(Ctx& c);          // D2H of DevScalars (syncs)
+void clear_scalars(Ctx& c);
+
+// ---- utilities (k_scan.cu)
+// exclusive scan of n ints: out[0..n] (out[n] = total). in may alias out only if n+1 storage.
+void scan_exclusive(Ctx& c, const int* in, int* out, int n);
+void sort_pairs(Ctx& c, int* keys, int* vals, int* keys_alt, int* vals_alt, int n, int end_bit,
+                int** keys_out, int** vals_out);
+// fixed-order deterministic sum of `n` partials into dst (device)
+void reduce_partials(Ctx& c, const double* part, int n, double* dst, int mode);
+
+// ---- frame (k_frame.cu)
+void frame_maps(Ctx& c, const uint16_t* depth_dev, int frame_index);
+void init_surfels_from_frame(Ctx& c);  // initialize_from_frame (pipeline.cpp:42-72) surfels
+
+// ---- warp field (k_warp.cu, k_skin.cu)
+int forward_warp(Ctx& c, bool count_degenerate);
+void node_se3(Ctx& c, const double4* dq, double* se3);
+void node_live_positions(Ctx& c);
+void apply_increments(Ctx& c, const double* delta, double4* out);  // solver.cpp:277-286
+void init_warp_field(Ctx& c);
+void compute_node_edges(Ctx& c);
+int extend_warp_field(Ctx& c, const float4* positions, int n);  // returns appended
+void update_skinning_incremental(Ctx& c, int first_new);
+
+// ---- raster (k_raster.cu)
+void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool associate,
+                       const double* assoc_pose);
+void render_index_map(Ctx& c, const double* pose, int factor);
+
+// ---- solver (k_solver.cu, k_rigid.cu)
+void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver_report* out);
+void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_pre, int* n_pairs);
+void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double* rel_res);
+void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int t_now,
+                 int t_last, ds_rigid_result* out);
+
+// ---- fusion (k_fusion.cu)
+void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out);
+void fuse_depth(Ctx& c, const double* pose, int t_now, int* fused, int* n_cand);
+void screen_candidates(Ctx& c, int n_cand, int* low_support, int* comp_rejected, int* accepted);
+void removal_mask(Ctx& c, const double* pose, int t_now, int n);
+int clean_and_reset(Ctx& c, const double* pose, int* survivors);
+
+// capacity guards
+void ensure_surfel_capacity(Ctx& c, long long n);
+void ensure_node_capacity(Ctx& c, long long n);
+
+}  // namespace ds

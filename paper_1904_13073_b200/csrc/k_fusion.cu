@@ -1,0 +1,615 @@
+// k_fusion.cu — geometry update (K11-K16, K2) and reinitialisation cleaning.
+//   fuse_depth         fusion.cpp:9-75: per valid pixel, scan the f x f block of
+//                      the supersampled index map, best = (confidence desc, d2
+//                      asc, index asc) within the 1 mm / 0.85 gates, Eq. 5 update
+//                      (each surfel lives in exactly one block, so pixels are
+//                      independent writers), else an append candidate.
+//   candidates         row-major stable compaction (fusion.cpp:46-57)
+//   skin_appended      fusion.cpp:77-122 (brute-force live-frame K-NN over nodes,
+//                      Eq. 6 ratio test, delta_nn support)
+//   check_compressive  fusion.cpp:128-177 (1 mm re-weighted inverse-warp strain,
+//                      sigma_max <= 1 + epsilon)
+//   remove_surfels     fusion.cpp:179-218 (unstable rule, 3x3 duplicate rule on the
+//                      pre-append index map)
+//   compaction + inverse warp  fusion.cpp:264-294 fused in one pass: stable scatter
+//                      of the survivors into the alternate SoA buffer while the
+//                      reference pose is rebuilt from the live one.
+//   clean_and_reset    reinit.cpp:28-89
+#include "ds_blend.cuh"
+#include "ds_context.cuh"
+
+namespace ds {
+
+void init_warp_field(Ctx& c);
+
+namespace {
+
+constexpr int kEmptyIdx = 0x7f7f7f7f;
+
+struct FuseParams {
+  Rig pose;
+  int W, H, f;
+  int t_now;
+  double dd2, dn;
+};
+
+__global__ void __launch_bounds__(256) k_fuse(const int* __restrict__ im_idx, ModelBuf m,
+                                              const double4* __restrict__ fvert,
+                                              const double4* __restrict__ fnrm,
+                                              const uint8_t* __restrict__ fflag, FuseParams fp,
+                                              int* __restrict__ cand_flag, int* __restrict__ fused) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= fp.W * fp.H) return;
+  if (!(fflag[c] & 2)) {
+    cand_flag[c] = 0;
+    return;
+  }
+  const int x = c % fp.W, y = c / fp.W;
+  const double4 fv = fvert[c], fn = fnrm[c];
+  const V3 vd = rig_apply(fp.pose, v3(fv.x, fv.y, fv.z));
+  const V3 nd = rig_rotate(fp.pose, v3(fn.x, fn.y, fn.z));
+  int best = -1;
+  double bc = 0, bd2 = 0;
+  const int Wf = fp.W * fp.f;
+  for (int sy = fp.f * y; sy < fp.f * (y + 1); ++sy)
+    for (int sx = fp.f * x; sx < fp.f * (x + 1); ++sx) {
+      const int id = im_idx[(size_t)sy * Wf + sx];
+      if (id == kEmptyIdx) continue;
+      const float4 lp = m.lp[id], ln = m.ln[id];
+      const double d2 = sqn(sub(v3(lp.x, lp.y, lp.z), vd));
+      if (d2 >= fp.dd2) continue;
+      if (dot(nd, v3(ln.x, ln.y, ln.z)) < fp.dn) continue;
+      const double sc = ln.w;
+      const bool better = best < 0 || sc > bc || (sc == bc && (d2 < bd2 || (d2 == bd2 && id < best)));
+      if (better) {
+        best = id;
+        bc = sc;
+        bd2 = d2;
+      }
+    }
+  if (best < 0) {
+    cand_flag[c] = 1;
+    return;
+  }
+  cand_flag[c] = 0;
+  const float4 lp = m.lp[best], ln = m.ln[best];
+  const double c_old = ln.w, c_d = fn.w, c_new = c_old + c_d;
+  const V3 sp = v3(lp.x, lp.y, lp.z), sn = v3(ln.x, ln.y, ln.z);
+  const V3 np = dvd(add(scl(c_old, sp), scl(c_d, vd)), c_new);
+  const V3 nn = dvd(add(scl(c_old, sn), scl(c_d, nd)), c_new);
+  const V3 nu = dvd(nn, nrm(nn));
+  const double r = (c_old * (double)lp.w + c_d * fv.w) / c_new;
+  m.lp[best] = make_float4((float)np.x, (float)np.y, (float)np.z, (float)r);
+  m.ln[best] = make_float4((float)nu.x, (float)nu.y, (float)nu.z, (float)c_new);
+  m.t[best].y = fp.t_now;
+  atomicAdd(fused, 1);
+}
+
+__global__ void k_write_cands(const int* __restrict__ flag, const int* __restrict__ scan, int P,
+                              const double4* __restrict__ fvert, const double4* __restrict__ fnrm,
+                              Rig pose, int* __restrict__ cand_pix, float4* __restrict__ cp,
+                              float4* __restrict__ cn) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P || !flag[c]) return;
+  const int k = scan[c];
+  const double4 fv = fvert[c], fn = fnrm[c];
+  const V3 vd = rig_apply(pose, v3(fv.x, fv.y, fv.z));
+  const V3 nd = rig_rotate(pose, v3(fn.x, fn.y, fn.z));
+  cand_pix[k] = c;
+  cp[k] = make_float4((float)vd.x, (float)vd.y, (float)vd.z, (float)fv.w);
+  cn[k] = make_float4((float)nd.x, (float)nd.y, (float)nd.z, (float)fn.w);
+}
+
+// 3x3 symmetric eigenvalues by cyclic Jacobi; returns sqrt(max eig of S^T S)
+__device__ double sigma_max3(const double S[3][3]) {
+  double a[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double acc = 0;
+      for (int k = 0; k < 3; ++k) acc += S[k][i] * S[k][j];
+      a[i][j] = acc;
+    }
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    const double off = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
+    if (off < 1e-300) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (a[p][q] == 0.0) continue;
+        const double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < 3; ++k) {
+          const double akp = a[k][p], akq = a[k][q];
+          a[k][p] = cs * akp - sn * akq;
+          a[k][q] = sn * akp + cs * akq;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = cs * apk - sn * aqk;
+          a[q][k] = sn * apk + cs * aqk;
+        }
+      }
+  }
+  const double m = fmax(fmax(a[0][0], a[1][1]), fmax(a[2][2], 0.0));
+  return sqrt(m);
+}
+
+struct ScreenParams {
+  int N, K, compressive;
+  double eps, delta_nn;
+};
+
+// inverse warp with weights re-evaluated at x over the entry's node set
+__device__ bool inv_warp_reweighted(V3 x, const int* ids, int cnt, const double4* __restrict__ node_dq,
+                                    const double4* __restrict__ node_live, V3& out) {
+  Q4 rs = q4(0, 0, 0, 0), ds_ = q4(0, 0, 0, 0);
+  const Q4 pivot = ld_q(node_dq + 2 * ids[0]);
+  for (int m = 0; m < cnt; ++m) {
+    const double4 nl = node_live[ids[m]];
+    const double w = skin_weight(x, v3(nl.x, nl.y, nl.z), nl.w);
+    const Q4 r = ld_q(node_dq + 2 * ids[m]);
+    const Q4 d = ld_q(node_dq + 2 * ids[m] + 1);
+    const double sign = (qdot(pivot, r) < 0.0) ? -1.0 : 1.0;
+    const double ww = sign * w;
+    rs = qadd(rs, qscl(ww, r));
+    ds_ = qadd(ds_, qscl(ww, d));
+  }
+  if (qnrm(rs) < kDegenerateBlend) return false;
+  DQ raw;
+  raw.r = rs;
+  raw.d = ds_;
+  out = rig_apply(rig_inverse(dq_to_rig(dq_normalized(raw))), x);
+  return true;
+}
+
+// skin_appended + check_compressive for candidate k (fusion.cpp:77-177).
+// result: 0 = low support, 1 = compressive reject, 2 = accepted
+__device__ int screen_one(V3 x, const double4* __restrict__ node_pos,
+                          const double4* __restrict__ node_live, const double4* __restrict__ node_dq,
+                          const ScreenParams& sp, int ids[4], float ws[4], int& cnt) {
+  double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+  for (int j = 0; j < sp.N; ++j) {
+    const double4 nl = node_live[j];
+    const double d2 = sqn(sub(v3(nl.x, nl.y, nl.z), x));
+    if (!nb_less(d2, j, bd[3], bi[3])) continue;
+    double cd = d2;
+    int ci = j;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      if (nb_less(cd, ci, bd[s], bi[s])) {
+        const double td = bd[s];
+        const int ti = bi[s];
+        bd[s] = cd;
+        bi[s] = ci;
+        cd = td;
+        ci = ti;
+      }
+  }
+  const int k = min(sp.K, sp.N);
+  const int n0 = bi[0];
+  const double4 l0 = node_live[n0], p0 = node_pos[n0];
+  double w[4];
+  cnt = 0;
+  ids[cnt] = n0;
+  w[cnt] = skin_weight(x, v3(l0.x, l0.y, l0.z), l0.w);
+  ++cnt;
+  for (int m = 1; m < k; ++m) {
+    const int j = bi[m];
+    const double4 lj = node_live[j], pj = node_pos[j];
+    const double lpair = nrm(sub(v3(lj.x, lj.y, lj.z), v3(l0.x, l0.y, l0.z)));
+    const double rpair = nrm(sub(v3(pj.x, pj.y, pj.z), v3(p0.x, p0.y, p0.z)));
+    if (rpair <= 0) continue;
+    const double ratio = lpair / rpair;
+    if (ratio <= 1.0 - sp.eps || ratio >= 1.0 + sp.eps) continue;
+    ids[cnt] = j;
+    w[cnt] = skin_weight(x, v3(lj.x, lj.y, lj.z), lj.w);
+    ++cnt;
+  }
+  double wsum = 0;
+  for (int m = 0; m < cnt; ++m) wsum += w[m];
+  for (int m = 0; m < 4; ++m) ws[m] = m < cnt ? (float)w[m] : 0.f;
+  for (int m = cnt; m < 4; ++m) ids[m] = -1;
+  if (wsum < sp.delta_nn) return 0;
+  if (sp.compressive) {
+    V3 c0;
+    if (!inv_warp_reweighted(x, ids, cnt, node_dq, node_live, c0)) return 1;
+    double S[3][3];
+    for (int a = 0; a < 3; ++a) {
+      V3 pr = x;
+      if (a == 0) pr.x += 1e-3;
+      else if (a == 1) pr.y += 1e-3;
+      else pr.z += 1e-3;
+      V3 sh;
+      if (!inv_warp_reweighted(pr, ids, cnt, node_dq, node_live, sh)) return 1;
+      const V3 col = dvd(sub(sh, c0), 1e-3);
+      S[0][a] = col.x;
+      S[1][a] = col.y;
+      S[2][a] = col.z;
+    }
+    if (!(sigma_max3(S) <= 1.0 + sp.eps)) return 1;
+  }
+  return 2;
+}
+
+__global__ void k_screen(const float4* __restrict__ cp, const int* __restrict__ n_cand_dev,
+                         const double4* __restrict__ node_pos, const double4* __restrict__ node_live,
+                         const double4* __restrict__ node_dq, ScreenParams sp,
+                         int4* __restrict__ cki, float4* __restrict__ ckw, int* __restrict__ ok,
+                         int* __restrict__ res_out, int* __restrict__ low, int* __restrict__ comp) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = *n_cand_dev;
+  if (k >= n) {
+    return;
+  }
+  const float4 p = cp[k];
+  int ids[4];
+  float ws[4];
+  int cnt = 0;
+  int res = 0;
+  if (sp.N > 0) res = screen_one(v3(p.x, p.y, p.z), node_pos, node_live, node_dq, sp, ids, ws, cnt);
+  if (sp.N == 0) {
+    for (int m = 0; m < 4; ++m) {
+      ids[m] = -1;
+      ws[m] = 0.f;
+    }
+  }
+  ok[k] = res == 2 ? 1 : 0;
+  res_out[k] = res;
+  if (res == 0) atomicAdd(low, 1);
+  if (res == 1) atomicAdd(comp, 1);
+  cki[k] = make_int4(ids[0], ids[1], ids[2], ids[3]);
+  ckw[k] = make_float4(ws[0], ws[1], ws[2], ws[3]);
+}
+
+__global__ void k_append(const int* __restrict__ ok, const int* __restrict__ scan,
+                         const int* __restrict__ n_cand_dev, const float4* __restrict__ cp,
+                         const float4* __restrict__ cn, const int4* __restrict__ cki,
+                         const float4* __restrict__ ckw, int n_old, int cap, int t_now, ModelBuf m,
+                         int* __restrict__ err) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= *n_cand_dev || !ok[k]) return;
+  const int o = n_old + scan[k];
+  if (o >= cap) {
+    atomicOr(err, 16);
+    return;
+  }
+  m.rp[o] = cp[k];
+  m.lp[o] = cp[k];
+  m.rn[o] = cn[k];
+  m.ln[o] = cn[k];
+  m.t[o] = make_int2(t_now, t_now);
+  m.ki[o] = cki[k];
+  m.kw[o] = ckw[k];
+}
+
+struct RemoveParams {
+  Rig w2c;
+  double fx, fy, cx, cy;
+  int W, H, f, t_now, t_low;
+  double delta_stable, delta_distance, delta_normal;
+};
+
+__global__ void __launch_bounds__(256) k_remove(ModelBuf m, const int* __restrict__ n_dev, int n_old,
+                                                const int* __restrict__ im_idx, RemoveParams rp,
+                                                int* __restrict__ keep) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = n_old + *n_dev;
+  if (i >= n) {
+    if (i < n_old + rp.W * rp.H) keep[i] = 0;
+    return;
+  }
+  const float4 lp = m.lp[i], ln = m.ln[i];
+  const int2 t = m.t[i];
+  const double ci = ln.w;
+  int rm = 0;
+  if (rp.t_now - t.x > rp.t_low && ci < rp.delta_stable) {
+    rm = 1;
+  } else {
+    const V3 sp = v3(lp.x, lp.y, lp.z), sn = v3(ln.x, ln.y, ln.z);
+    const V3 pc = rig_apply(rp.w2c, sp);
+    if (pc.z > 0) {
+      const double u = rp.fx * pc.x / pc.z + rp.cx;
+      const double v = rp.fy * pc.y / pc.z + rp.cy;
+      const double fsx = floor(rp.f * (u + 0.5)), fsy = floor(rp.f * (v + 0.5));
+      const int Wf = rp.W * rp.f, Hf = rp.H * rp.f;
+      if (fabs(fsx) < 1e9 && fabs(fsy) < 1e9) {
+        const int sx = (int)fsx, sy = (int)fsy;
+        for (int dy = -1; dy <= 1 && !rm; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int nx = sx + dx, ny = sy + dy;
+            if (nx < 0 || nx >= Wf || ny < 0 || ny >= Hf) continue;
+            const int j = im_idx[(size_t)ny * Wf + nx];
+            if (j == kEmptyIdx || j == i) continue;
+            const float4 op = m.lp[j], on = m.ln[j];
+            const double oc = on.w;
+            if (oc <= rp.delta_stable) continue;
+            if (oc <= ci) continue;
+            if (nrm(sub(v3(op.x, op.y, op.z), sp)) >= rp.delta_distance) continue;
+            if (dot(v3(on.x, on.y, on.z), sn) < rp.delta_normal) continue;
+            rm = 1;
+            break;
+          }
+      }
+    }
+  }
+  keep[i] = rm ? 0 : 1;
+}
+
+// stable scatter of survivors into the alternate buffer + inverse warp (K2, K16)
+__global__ void __launch_bounds__(256) k_compact_inverse(ModelBuf src, ModelBuf dst, int limit,
+                                                         const int* __restrict__ keep,
+                                                         const int* __restrict__ scan,
+                                                         const double4* __restrict__ node_dq,
+                                                         int* __restrict__ degenerate) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= limit || !keep[i]) return;
+  const int o = scan[i];
+  const float4 lp = src.lp[i], ln = src.ln[i];
+  const int4 ki = src.ki[i];
+  const float4 kw = src.kw[i];
+  const Blend b = blend_entry(ki, kw, node_dq);
+  float4 rp = lp, rn = ln;
+  if (!b.degenerate) {
+    const Rig inv = rig_inverse(blend_rig(b));
+    const V3 p = rig_apply(inv, v3(lp.x, lp.y, lp.z));
+    const V3 q = rig_rotate(inv, v3(ln.x, ln.y, ln.z));
+    rp = make_float4((float)p.x, (float)p.y, (float)p.z, lp.w);
+    rn = make_float4((float)q.x, (float)q.y, (float)q.z, ln.w);
+  } else {
+    atomicAdd(degenerate, 1);
+  }
+  dst.lp[o] = lp;
+  dst.ln[o] = ln;
+  dst.rp[o] = rp;
+  dst.rn[o] = rn;
+  dst.t[o] = src.t[i];
+  dst.ki[o] = ki;
+  dst.kw[o] = kw;
+}
+
+// clean_and_reset keep rule (reinit.cpp:37-75)
+struct CleanParams {
+  Rig pose, w2c;
+  double fx, fy, cx, cy, gate, delta_normal;
+  int W, H;
+};
+__global__ void k_clean(ModelBuf m, int n, const double4* __restrict__ fvert,
+                        const double4* __restrict__ fnrm, const uint8_t* __restrict__ fflag,
+                        CleanParams cp, int* __restrict__ keep) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 lp = m.lp[i], ln = m.ln[i];
+  const V3 sp = v3(lp.x, lp.y, lp.z), sn = v3(ln.x, ln.y, ln.z);
+  const V3 pc = rig_apply(cp.w2c, sp);
+  bool kp = true;
+  if (pc.z > 0 && dot(rig_rotate(cp.w2c, sn), pc) < 0) {
+    const double u = cp.fx * pc.x / pc.z + cp.cx;
+    const double v = cp.fy * pc.y / pc.z + cp.cy;
+    if (fabs(u) < 1e9 && fabs(v) < 1e9) {
+      const int ui = (int)llround(u), vi = (int)llround(v);
+      if (ui >= 0 && ui < cp.W && vi >= 0 && vi < cp.H) {
+        bool corr = false, occl = false, anym = false;
+        for (int dy = -1; dy <= 2 && !corr; ++dy)
+          for (int dx = -1; dx <= 2; ++dx) {
+            const int x = ui + dx, y = vi + dy;
+            if (x < 0 || x >= cp.W || y < 0 || y >= cp.H) continue;
+            const size_t c = (size_t)y * cp.W + x;
+            const uint8_t fl = fflag[c];
+            if (!(fl & 1)) continue;
+            anym = true;
+            const double4 fv = fvert[c];
+            if (fv.z < pc.z - cp.gate) occl = true;
+            if (!(fl & 2)) continue;
+            const V3 vd = rig_apply(cp.pose, v3(fv.x, fv.y, fv.z));
+            if (nrm(sub(vd, sp)) >= cp.gate) continue;
+            const double4 fn = fnrm[c];
+            if (dot(rig_rotate(cp.pose, v3(fn.x, fn.y, fn.z)), sn) < cp.delta_normal) continue;
+            corr = true;
+            break;
+          }
+        kp = corr || occl || !anym;
+      }
+    }
+  }
+  keep[i] = kp ? 1 : 0;
+}
+__global__ void k_compact_reset(ModelBuf src, ModelBuf dst, int n, const int* __restrict__ keep,
+                                const int* __restrict__ scan) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !keep[i]) return;
+  const int o = scan[i];
+  const float4 lp = src.lp[i], ln = src.ln[i];
+  dst.lp[o] = lp;
+  dst.ln[o] = ln;
+  dst.rp[o] = lp;
+  dst.rn[o] = ln;
+  dst.t[o] = src.t[i];
+  dst.ki[o] = make_int4(-1, -1, -1, -1);
+  dst.kw[o] = make_float4(0, 0, 0, 0);
+}
+
+FuseParams fuse_params(Ctx& c, const double* pose, int t_now) {
+  FuseParams fp;
+  fp.pose = rig_load(pose);
+  fp.W = c.W;
+  fp.H = c.H;
+  fp.f = c.im_factor;
+  fp.t_now = t_now;
+  fp.dd2 = c.cfg.delta_distance * c.cfg.delta_distance;
+  fp.dn = c.cfg.delta_normal;
+  return fp;
+}
+
+ScreenParams screen_params(Ctx& c) {
+  ScreenParams sp;
+  sp.N = c.n_nodes;
+  sp.K = std::min(4, c.cfg.knn_k);
+  sp.compressive = c.cfg.compressive_check ? 1 : 0;
+  sp.eps = c.cfg.epsilon;
+  sp.delta_nn = c.cfg.delta_nn;
+  return sp;
+}
+
+}  // namespace
+
+// fuse_depth + candidate compaction; counts stay on the device (dsc)
+void fuse_depth_async(Ctx& c, const double* pose, int t_now) {
+  if (!c.im_ready) fail(DS_ERR_INVALID_ARGUMENT, "fuse_depth: no index map rendered");
+  DS_CUDA(cudaMemsetAsync(&c.dsc->fused, 0, sizeof(int), c.stream));
+  const int P = c.P;
+  // per pixel: frame maps 65 B, 16 index cells x 4 B, winner read+write 64 B, flag 4 B
+  DS_LAUNCH(c, KK_FUSE, 197.0 * P, cdiv(P, 256), 256, 0, k_fuse, c.im_idx, c.M(), c.f_vert, c.f_nrm,
+            c.f_flag, fuse_params(c, pose, t_now), c.cand_flag, &c.dsc->fused);
+  scan_exclusive(c, c.cand_flag, c.cand_scan, P);
+  DS_LAUNCH(c, KK_FUSE, 40.0 * P, cdiv(P, 256), 256, 0, k_write_cands, c.cand_flag, c.cand_scan, P,
+            c.f_vert, c.f_nrm, rig_load(pose), c.cand_pix, c.cand_p, c.cand_n);
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->n_cand, c.cand_scan + P, sizeof(int), cudaMemcpyDeviceToDevice,
+                          c.stream));
+}
+
+void fuse_depth(Ctx& c, const double* pose, int t_now, int* fused, int* n_cand) {
+  fuse_depth_async(c, pose, t_now);
+  fetch_scalars(c);
+  *fused = c.hsc->fused;
+  *n_cand = c.hsc->n_cand;
+}
+
+void screen_candidates_async(Ctx& c) {
+  DS_CUDA(cudaMemsetAsync(&c.dsc->low_support, 0, sizeof(int), c.stream));
+  DS_CUDA(cudaMemsetAsync(&c.dsc->comp_rejected, 0, sizeof(int), c.stream));
+  DS_CUDA(cudaMemsetAsync(c.cand_ok, 0, sizeof(int) * c.P, c.stream));
+  node_live_positions(c);
+  DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02, cdiv(c.P, 128), 128, 0, k_screen, c.cand_p,
+            &c.dsc->n_cand, c.node_pos, c.node_live, c.node_dq, screen_params(c), c.cand_ki,
+            c.cand_kw, c.cand_ok, c.cand_flag, &c.dsc->low_support, &c.dsc->comp_rejected);
+}
+
+void screen_candidates(Ctx& c, int n_cand, int* low_support, int* comp_rejected, int* accepted) {
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->n_cand, &n_cand, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  screen_candidates_async(c);
+  fetch_scalars(c);
+  *low_support = c.hsc->low_support;
+  *comp_rejected = c.hsc->comp_rejected;
+  *accepted = n_cand - c.hsc->low_support - c.hsc->comp_rejected;
+}
+
+void removal_mask(Ctx& c, const double* pose, int t_now, int n) {
+  RemoveParams rp;
+  rp.w2c = rig_inverse(rig_load(pose));
+  rp.fx = c.cfg.fx;
+  rp.fy = c.cfg.fy;
+  rp.cx = c.cfg.cx;
+  rp.cy = c.cfg.cy;
+  rp.W = c.W;
+  rp.H = c.H;
+  rp.f = c.im_factor;
+  rp.t_now = t_now;
+  rp.t_low = c.cfg.t_low_confid;
+  rp.delta_stable = c.cfg.delta_stable;
+  rp.delta_distance = c.cfg.delta_distance;
+  rp.delta_normal = c.cfg.delta_normal;
+  int zero = 0;
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->n_accept, &zero, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  DS_LAUNCH(c, KK_REMOVE, 76.0 * n, cdiv(n, 256), 256, 0, k_remove, c.M(), &c.dsc->n_accept, n,
+            c.im_idx, rp, c.keep);
+}
+
+// apply_fusion (fusion.cpp:220-307)
+void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out) {
+  ds_fusion_outcome oc{};
+  const int P = c.P;
+  render_index_map(c, pose, c.cfg.supersample_factor);
+  fuse_depth_async(c, pose, t_now);
+  screen_candidates_async(c);
+  // accepted candidates keep row-major order (fusion.cpp:235-257)
+  scan_exclusive(c, c.cand_ok, c.cand_ok_scan, P);
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->n_accept, c.cand_ok_scan + P, sizeof(int),
+                          cudaMemcpyDeviceToDevice, c.stream));
+  const int n_old = c.n_surfels;
+  DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
+  DS_LAUNCH(c, KK_FUSE, 64.0 * P * 0.02, cdiv(P, 256), 256, 0, k_append, c.cand_ok, c.cand_ok_scan,
+            &c.dsc->n_cand, c.cand_p, c.cand_n, c.cand_ki, c.cand_kw, n_old, c.S_cap, t_now, c.M(),
+            &c.dsc->err);
+  // removal over old + appended (upper bound n_old + P, exact count on device)
+  RemoveParams rp;
+  rp.w2c = rig_inverse(rig_load(pose));
+  rp.fx = c.cfg.fx;
+  rp.fy = c.cfg.fy;
+  rp.cx = c.cfg.cx;
+  rp.cy = c.cfg.cy;
+  rp.W = c.W;
+  rp.H = c.H;
+  rp.f = c.im_factor;
+  rp.t_now = t_now;
+  rp.t_low = c.cfg.t_low_confid;
+  rp.delta_stable = c.cfg.delta_stable;
+  rp.delta_distance = c.cfg.delta_distance;
+  rp.delta_normal = c.cfg.delta_normal;
+  const int limit = std::min(n_old + P, c.S_cap);
+  DS_LAUNCH(c, KK_REMOVE, 76.0 * limit, cdiv(limit, 256), 256, 0, k_remove, c.M(), &c.dsc->n_accept,
+            n_old, c.im_idx, rp, c.keep);
+  scan_exclusive(c, c.keep, c.keep_scan, limit);
+  DS_CUDA(cudaMemsetAsync(&c.dsc->degenerate, 0, sizeof(int), c.stream));
+  DS_LAUNCH(c, KK_COMPACT_INVERSE_WARP, 104.0 * 2 * limit, cdiv(limit, 256), 256, 0,
+            k_compact_inverse, c.M(), c.Malt(), limit, c.keep, c.keep_scan, c.node_dq,
+            &c.dsc->degenerate);
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->n_keep, c.keep_scan + limit, sizeof(int),
+                          cudaMemcpyDeviceToDevice, c.stream));
+  int surv_old = 0;
+  DS_CUDA(cudaMemcpyAsync(&surv_old, c.keep_scan + n_old, sizeof(int), cudaMemcpyDeviceToHost,
+                          c.stream));
+  fetch_scalars(c);
+  if (c.hsc->err & 16) fail(DS_ERR_CAPACITY, "surfel capacity exceeded while appending");
+  c.cur ^= 1;
+  const int n_acc = c.hsc->n_accept;
+  const int n_new = c.hsc->n_keep;
+  oc.fused = c.hsc->fused;
+  oc.appended = n_acc;
+  oc.low_support_rejected = c.hsc->low_support;
+  oc.compressive_rejected = c.hsc->comp_rejected;
+  oc.removed = n_old + n_acc - n_new;
+  oc.degenerate_warps = c.hsc->degenerate;
+  c.n_surfels = n_new;
+  // extend the warp field over the appended survivors (compacted order)
+  const int app_surv = n_new - surv_old;
+  const int first_new = c.n_nodes;
+  oc.new_nodes = extend_warp_field(c, c.M().rp + surv_old, app_surv);
+  if (oc.new_nodes > 0) update_skinning_incremental(c, first_new);
+  c.pattern_ready = false;
+  *out = oc;
+}
+
+int clean_and_reset(Ctx& c, const double* pose, int* survivors) {
+  const int n = c.n_surfels;
+  CleanParams cp;
+  cp.pose = rig_load(pose);
+  cp.w2c = rig_inverse(cp.pose);
+  cp.fx = c.cfg.fx;
+  cp.fy = c.cfg.fy;
+  cp.cx = c.cfg.cx;
+  cp.cy = c.cfg.cy;
+  cp.gate = c.cfg.delta_distance_reinit;
+  cp.delta_normal = c.cfg.delta_normal;
+  cp.W = c.W;
+  cp.H = c.H;
+  if (n > 0) {
+    DS_LAUNCH(c, KK_MISC, 40.0 * n, cdiv(n, 256), 256, 0, k_clean, c.M(), n, c.f_vert, c.f_nrm,
+              c.f_flag, cp, c.keep);
+  }
+  scan_exclusive(c, c.keep, c.keep_scan, n);
+  int kept = 0;
+  DS_CUDA(cudaMemcpyAsync(&kept, c.keep_scan + n, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  sync(c);
+  if (kept == 0) fail(DS_ERR_EMPTY_GEOMETRY, "clean_and_reset: no surfel survived");
+  DS_LAUNCH(c, KK_MISC, 72.0 * n, cdiv(n, 256), 256, 0, k_compact_reset, c.M(), c.Malt(), n, c.keep,
+            c.keep_scan);
+  c.cur ^= 1;
+  c.n_surfels = kept;
+  if (survivors) *survivors = kept;
+  init_warp_field(c);
+  c.pattern_ready = false;
+  return n - kept;
+}
+
+}  // namespace ds

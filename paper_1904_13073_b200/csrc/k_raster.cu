@@ -1,0 +1,215 @@
+// k_raster.cu — compute-side rasterisation (K3, K4, K10) replacing the paper's
+// OpenGL index maps.
+//   render_model_maps   raster.cpp:32-121: eligibility (stable, or recent in the
+//                       bootstrap window), back-face cull, point channel at the
+//                       lround pixel, opaque disk splats, point beats splat
+//   find_correspondences solver.cpp:244-271: gates |v_m - v_d| < 3 cm and
+//                       n_m . n_d > 0.7, pair per pixel in row-major order
+//   render_index_map    raster.cpp:8-30: supersampled point z-buffer
+// Exact z-buffer semantics (nearest fp64 depth wins, ties -> lower surfel index)
+// in two atomic passes: pass 1 atomicMin on the fp64 depth bits (positive
+// doubles order like unsigned ints), pass 2 atomicMin on the index among the
+// writers whose depth equals the stored minimum.
+#include "ds_context.cuh"
+
+namespace ds {
+namespace {
+
+constexpr int kEmptyIdx = 0x7f7f7f7f;
+
+struct CamParams {
+  Rig w2c;
+  double fx, fy, cx, cy, focal;
+  int W, H;
+};
+
+struct SplatParams {
+  CamParams cam;
+  int t_now, delta_recent, host_bootstrap;
+  double delta_stable;
+};
+
+__global__ void k_any_stable(const float4* __restrict__ ln, int n, double delta_stable,
+                             int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool st = i < n && (double)ln[i].w > delta_stable;
+  const unsigned b = __ballot_sync(0xffffffffu, st);
+  if ((threadIdx.x & 31) == 0 && b) atomicOr(flag, 1);
+}
+
+template <bool kPass2>
+__global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, SplatParams sp,
+                                                     const int* __restrict__ any_stable,
+                                                     unsigned long long* pkey,
+                                                     unsigned long long* skey, int* pidx,
+                                                     int* sidx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 lp = m.lp[i];
+  const float4 ln = m.ln[i];
+  const int2 t = m.t[i];
+  const bool stable = (double)ln.w > sp.delta_stable;
+  const bool recent = (sp.t_now - t.y) <= sp.delta_recent;
+  const bool bootstrap = sp.host_bootstrap || !(*any_stable);
+  if (!stable && !(bootstrap && recent)) return;
+  const CamParams& k = sp.cam;
+  const V3 pc = rig_apply(k.w2c, v3(lp.x, lp.y, lp.z));
+  if (pc.z <= 0) return;
+  const V3 nc = rig_rotate(k.w2c, v3(ln.x, ln.y, ln.z));
+  if (dot(nc, pc) >= 0) return;
+  const double u = k.fx * pc.x / pc.z + k.cx;
+  const double v = k.fy * pc.y / pc.z + k.cy;
+  const unsigned long long zb = (unsigned long long)__double_as_longlong(pc.z);
+  const bool sane = fabs(u) < 1e9 && fabs(v) < 1e9;
+  const int ccx = sane ? (int)llround(u) : -1, ccy = sane ? (int)llround(v) : -1;
+  const bool cin = ccx >= 0 && ccx < k.W && ccy >= 0 && ccy < k.H;
+  if (cin) {
+    const size_t c = (size_t)ccy * k.W + ccx;
+    if (!kPass2) atomicMin(pkey + c, zb);
+    else if (pkey[c] == zb) atomicMin(pidx + c, i);
+  }
+  const double rpx = (double)lp.w * k.focal / pc.z;
+  const double r2 = rpx * rpx;
+  if (sane && rpx < 1e6) {
+    const int y0 = max((int)ceil(v - rpx), 0), y1 = min((int)floor(v + rpx), k.H - 1);
+    const int x0 = max((int)ceil(u - rpx), 0), x1 = min((int)floor(u + rpx), k.W - 1);
+    for (int y = y0; y <= y1; ++y)
+      for (int x = x0; x <= x1; ++x) {
+        const double dx = x - u, dy = y - v;
+        if (dx * dx + dy * dy <= r2) {
+          const size_t c = (size_t)y * k.W + x;
+          if (!kPass2) atomicMin(skey + c, zb);
+          else if (skey[c] == zb) atomicMin(sidx + c, i);
+        }
+      }
+  }
+  if (cin) {  // sub-pixel splats keep their own pixel (raster.cpp:101)
+    const size_t c = (size_t)ccy * k.W + ccx;
+    if (!kPass2) atomicMin(skey + c, zb);
+    else if (skey[c] == zb) atomicMin(sidx + c, i);
+  }
+}
+
+struct AssocParams {
+  Rig pose;
+  int P;
+  int associate;
+};
+
+__global__ void k_resolve_associate(const int* __restrict__ pidx, const int* __restrict__ sidx,
+                                    ModelBuf m, const double4* __restrict__ fvert,
+                                    const double4* __restrict__ fnrm,
+                                    const uint8_t* __restrict__ fflag, AssocParams ap,
+                                    int* __restrict__ mm_idx, int* __restrict__ pair_s,
+                                    int* __restrict__ n_pairs) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ap.P) return;
+  int win = pidx[c];
+  if (win == kEmptyIdx) win = sidx[c];
+  if (win == kEmptyIdx) win = -1;
+  mm_idx[c] = win;
+  if (!ap.associate) return;
+  int ps = -1;
+  if (win >= 0 && (fflag[c] & 2)) {
+    const double4 fv = fvert[c], fn = fnrm[c];
+    const V3 vd = rig_apply(ap.pose, v3(fv.x, fv.y, fv.z));
+    const V3 nd = rig_rotate(ap.pose, v3(fn.x, fn.y, fn.z));
+    const float4 lp = m.lp[win], ln = m.ln[win];
+    const V3 vm = v3(lp.x, lp.y, lp.z);
+    if (nrm(sub(vm, vd)) < 0.03 && dot(v3(ln.x, ln.y, ln.z), nd) > 0.7) ps = win;
+  }
+  pair_s[c] = ps;
+  const unsigned b = __ballot_sync(0xffffffffu, ps >= 0);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(n_pairs, __popc(b));
+}
+
+template <bool kPass2>
+__global__ void __launch_bounds__(256) k_index_splat(ModelBuf m, int n, CamParams k, int factor,
+                                                     unsigned long long* key, int* idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 lp = m.lp[i];
+  const V3 pc = rig_apply(k.w2c, v3(lp.x, lp.y, lp.z));
+  if (pc.z <= 0) return;
+  const double u = k.fx * pc.x / pc.z + k.cx;
+  const double v = k.fy * pc.y / pc.z + k.cy;
+  const double fu = floor(factor * (u + 0.5)), fv = floor(factor * (v + 0.5));
+  const int Wf = k.W * factor, Hf = k.H * factor;
+  if (!(fu >= 0 && fu < Wf && fv >= 0 && fv < Hf)) return;
+  const size_t c = (size_t)fv * Wf + (size_t)fu;
+  const unsigned long long zb = (unsigned long long)__double_as_longlong(pc.z);
+  if (!kPass2) atomicMin(key + c, zb);
+  else if (key[c] == zb) atomicMin(idx + c, i);
+}
+
+CamParams cam_params(Ctx& c, const double* pose) {
+  CamParams k;
+  k.w2c = rig_inverse(rig_load(pose));
+  k.fx = c.cfg.fx;
+  k.fy = c.cfg.fy;
+  k.cx = c.cfg.cx;
+  k.cy = c.cfg.cy;
+  k.focal = 0.5 * (c.cfg.fx + c.cfg.fy);
+  k.W = c.W;
+  k.H = c.H;
+  return k;
+}
+
+}  // namespace
+
+void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool associate,
+                       const double* assoc_pose) {
+  const int n = c.n_surfels;
+  const size_t P = c.P;
+  DS_CUDA(cudaMemsetAsync(c.mm_pkey, 0xff, 8 * P, c.stream));
+  DS_CUDA(cudaMemsetAsync(c.mm_skey, 0xff, 8 * P, c.stream));
+  DS_CUDA(cudaMemsetAsync(c.mm_pidx, 0x7f, 4 * P, c.stream));
+  DS_CUDA(cudaMemsetAsync(c.mm_sidx, 0x7f, 4 * P, c.stream));
+  DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable, 0, sizeof(int), c.stream));
+  DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
+  SplatParams sp;
+  sp.cam = cam_params(c, pose);
+  sp.t_now = t_now;
+  sp.delta_recent = c.cfg.delta_recent;
+  sp.delta_stable = c.cfg.delta_stable;
+  sp.host_bootstrap = (t_now - t_last <= c.cfg.delta_recent) ? 1 : 0;
+  if (n > 0) {
+    DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 16.0 * n, cdiv(n, 256), 256, 0, k_any_stable, c.M().ln, n,
+              c.cfg.delta_stable, &c.dsc->any_stable);
+    DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 40.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(), n,
+              sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx);
+    DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 40.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
+              sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx);
+  }
+  AssocParams ap;
+  ap.pose = rig_load(associate ? assoc_pose : pose);
+  ap.P = c.P;
+  ap.associate = associate ? 1 : 0;
+  // per pixel: 2 x 4 B winner ids, frame maps 65 B, winner live 32 B, 2 x 4 B out
+  DS_LAUNCH(c, KK_ASSOCIATE, (associate ? 113.0 : 12.0) * c.P, cdiv(c.P, 256), 256, 0,
+            k_resolve_associate, c.mm_pidx, c.mm_sidx, c.M(), c.f_vert, c.f_nrm, c.f_flag, ap,
+            c.mm_idx, c.pair_s, &c.dsc->n_pairs);
+  std::copy(pose, pose + 12, c.mm_pose);
+  c.mm_ready = true;
+}
+
+void render_index_map(Ctx& c, const double* pose, int factor) {
+  const int n = c.n_surfels;
+  const size_t cells = (size_t)c.P * factor * factor;
+  if (factor != c.cfg.supersample_factor && factor > c.cfg.supersample_factor)
+    fail(DS_ERR_CAPACITY, "index map factor larger than the configured supersample_factor");
+  DS_CUDA(cudaMemsetAsync(c.im_key, 0xff, 8 * cells, c.stream));
+  DS_CUDA(cudaMemsetAsync(c.im_idx, 0x7f, 4 * cells, c.stream));
+  const CamParams k = cam_params(c, pose);
+  if (n > 0) {
+    DS_LAUNCH(c, KK_INDEX_MAP, 16.0 * n, cdiv(n, 256), 256, 0, k_index_splat<false>, c.M(), n, k,
+              factor, c.im_key, c.im_idx);
+    DS_LAUNCH(c, KK_INDEX_MAP, 16.0 * n, cdiv(n, 256), 256, 0, k_index_splat<true>, c.M(), n, k,
+              factor, c.im_key, c.im_idx);
+  }
+  c.im_factor = factor;
+  std::copy(pose, pose + 12, c.im_pose);
+  c.im_ready = true;
+}
+
+}  // namespace ds

@@ -1,0 +1,256 @@
+// k_rigid.cu — projective point-to-plane rigid pre-alignment (K23).
+//   rigid_align  solver.cpp:171-242: stride pyramid 4 -> 2 -> 1 with {3, 3, 4}
+//   iterations, association at the lround pixel of the pose-transformed vertex
+//   against model maps rendered under the initial pose, J = [v x n, n], 6x6
+//   LDLT, se3_increment. Every iteration is a sample kernel (fp64 block
+//   reduction of the 21 + 6 + 2 normal-equation terms) followed by a one-block
+//   finalize that sums the partials in a fixed order and solves on the device,
+//   so the whole pyramid runs without a host round trip.
+#include "ds_context.cuh"
+
+namespace ds {
+namespace {
+
+constexpr int kTerms = 29;  // 21 upper H, 6 g, count, sum |r|
+constexpr int kThreads = 256;
+
+struct RigidParams {
+  Rig render_inv;
+  double fx, fy, cx, cy;
+  int W, H, stride, sw, sh;
+};
+
+__global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const double* __restrict__ cur_pose,
+                                                          const int* __restrict__ mm_idx, ModelBuf m,
+                                                          const double4* __restrict__ fvert,
+                                                          const double4* __restrict__ fnrm,
+                                                          const uint8_t* __restrict__ fflag,
+                                                          double* __restrict__ part) {
+  __shared__ double sh[kThreads / 32][kTerms];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  double v[kTerms];
+#pragma unroll
+  for (int k = 0; k < kTerms; ++k) v[k] = 0.0;
+  if (t < rp.sw * rp.sh) {
+    const int x = (t % rp.sw) * rp.stride, y = (t / rp.sw) * rp.stride;
+    const size_t c = (size_t)y * rp.W + x;
+    if (fflag[c] & 2) {
+      const Rig cur = rig_load(cur_pose);
+      const double4 fv = fvert[c];
+      const V3 vw = rig_apply(cur, v3(fv.x, fv.y, fv.z));
+      const V3 pr = rig_apply(rp.render_inv, vw);
+      if (pr.z > 0) {
+        const double u = rp.fx * pr.x / pr.z + rp.cx;
+        const double vv = rp.fy * pr.y / pr.z + rp.cy;
+        if (fabs(u) < 1e9 && fabs(vv) < 1e9) {
+          const int ui = (int)llround(u), vi = (int)llround(vv);
+          if (ui >= 0 && ui < rp.W && vi >= 0 && vi < rp.H) {
+            const int win = mm_idx[(size_t)vi * rp.W + ui];
+            if (win >= 0) {
+              const float4 lp = m.lp[win], ln = m.ln[win];
+              const V3 vm = v3(lp.x, lp.y, lp.z), nm = v3(ln.x, ln.y, ln.z);
+              const double4 fn = fnrm[c];
+              if (nrm(sub(vw, vm)) < 0.03 &&
+                  dot(rig_rotate(cur, v3(fn.x, fn.y, fn.z)), nm) > 0.7) {
+                const double r = dot(nm, sub(vw, vm));
+                const V3 cr = cross(vw, nm);
+                const double J[6] = {cr.x, cr.y, cr.z, nm.x, nm.y, nm.z};
+                int k = 0;
+#pragma unroll
+                for (int a = 0; a < 6; ++a)
+#pragma unroll
+                  for (int b = a; b < 6; ++b) v[k++] = J[a] * J[b];
+#pragma unroll
+                for (int a = 0; a < 6; ++a) v[21 + a] = J[a] * r;
+                v[27] = 1.0;
+                v[28] = fabs(r);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < kTerms; ++k) {
+    double s = v[k];
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) sh[wid][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < kTerms) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += sh[w][threadIdx.x];
+    part[(size_t)blockIdx.x * kTerms + threadIdx.x] = s;
+  }
+}
+
+// Eigen::LDLT semantics (solver.cpp:225): diagonal pivoting, zero pivots kept,
+// pseudo-inverse of D with tolerance DBL_MIN.
+__device__ void ldlt_solve6(double A[6][6], const double* b, double* x) {
+  int perm[6];
+  double temp[6];
+  bool zero_all = false;
+  for (int k = 0; k < 6; ++k) {
+    int big = k;
+    double bv = fabs(A[k][k]);
+    for (int i = k + 1; i < 6; ++i)
+      if (fabs(A[i][i]) > bv) {
+        bv = fabs(A[i][i]);
+        big = i;
+      }
+    perm[k] = big;
+    if (big != k) {
+      for (int c = 0; c < k; ++c) {
+        const double t = A[k][c];
+        A[k][c] = A[big][c];
+        A[big][c] = t;
+      }
+      for (int r = big + 1; r < 6; ++r) {
+        const double t = A[r][k];
+        A[r][k] = A[r][big];
+        A[r][big] = t;
+      }
+      const double t = A[k][k];
+      A[k][k] = A[big][big];
+      A[big][big] = t;
+      for (int i = k + 1; i < big; ++i) {
+        const double tmp = A[i][k];
+        A[i][k] = A[big][i];
+        A[big][i] = tmp;
+      }
+    }
+    if (k > 0) {
+      for (int c = 0; c < k; ++c) temp[c] = A[c][c] * A[k][c];
+      double s = 0;
+      for (int c = 0; c < k; ++c) s += A[k][c] * temp[c];
+      A[k][k] -= s;
+      for (int r = k + 1; r < 6; ++r) {
+        double acc = 0;
+        for (int c = 0; c < k; ++c) acc += A[r][c] * temp[c];
+        A[r][k] -= acc;
+      }
+    }
+    const double akk = A[k][k];
+    const bool valid = fabs(akk) > 0.0;
+    if (k == 0 && !valid) {
+      zero_all = true;
+      break;
+    }
+    if (valid)
+      for (int r = k + 1; r < 6; ++r) A[r][k] /= akk;
+  }
+  for (int i = 0; i < 6; ++i) x[i] = zero_all ? 0.0 : b[i];
+  if (zero_all) return;
+  for (int k = 0; k < 6; ++k) {
+    const double t = x[k];
+    x[k] = x[perm[k]];
+    x[perm[k]] = t;
+  }
+  for (int r = 0; r < 6; ++r) {
+    double s = x[r];
+    for (int c = 0; c < r; ++c) s -= A[r][c] * x[c];
+    x[r] = s;
+  }
+  for (int i = 0; i < 6; ++i) x[i] = fabs(A[i][i]) > 2.2250738585072014e-308 ? x[i] / A[i][i] : 0.0;
+  for (int r = 5; r >= 0; --r) {
+    double s = x[r];
+    for (int c = r + 1; c < 6; ++c) s -= A[c][r] * x[c];
+    x[r] = s;
+  }
+  for (int k = 5; k >= 0; --k) {
+    const double t = x[k];
+    x[k] = x[perm[k]];
+    x[perm[k]] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rigid_finalize(const double* __restrict__ part,
+                                                         int nblocks, int level,
+                                                         double* __restrict__ cur_pose,
+                                                         DevScalars* sc) {
+  __shared__ double tot[kTerms];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int term = wid; term < kTerms; term += 8) {  // fixed order per term
+    double s = 0.0;
+    for (int b = lane; b < nblocks; b += 32) s += part[(size_t)b * kTerms + term];
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) tot[term] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int pairs = (int)tot[27];
+  if (level == 0) {
+    sc->rigid_pairs = pairs;
+    sc->rigid_abs = tot[28];
+  }
+  if (pairs < 6) return;
+  double A[6][6];
+  int k = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) {
+      A[a][b] = tot[k];
+      A[b][a] = tot[k];
+      ++k;
+    }
+  double ng[6], xi[6];
+  for (int a = 0; a < 6; ++a) ng[a] = -tot[21 + a];
+  ldlt_solve6(A, ng, xi);
+  for (int a = 0; a < 6; ++a)
+    if (!isfinite(xi[a])) return;
+  const Rig cur = rig_load(cur_pose);
+  rig_store(se3_increment(v3(xi[0], xi[1], xi[2]), v3(xi[3], xi[4], xi[5]), cur), cur_pose);
+}
+
+}  // namespace
+
+void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int t_now, int t_last,
+                 ds_rigid_result* out) {
+  render_model_maps(c, render_pose, t_now, t_last, false, nullptr);
+  DS_CUDA(cudaMemcpyAsync(c.d_pose, init_pose, 12 * sizeof(double), cudaMemcpyHostToDevice,
+                          c.stream));
+  DS_CUDA(cudaMemsetAsync(&c.dsc->rigid_pairs, 0, sizeof(int), c.stream));
+  DS_CUDA(cudaMemsetAsync(&c.dsc->rigid_abs, 0, sizeof(double), c.stream));
+  RigidParams rp;
+  rp.render_inv = rig_inverse(rig_load(init_pose));
+  rp.fx = c.cfg.fx;
+  rp.fy = c.cfg.fy;
+  rp.cx = c.cfg.cx;
+  rp.cy = c.cfg.cy;
+  rp.W = c.W;
+  rp.H = c.H;
+  static const int kIters[3] = {4, 3, 3};
+  for (int level = 2; level >= 0; --level) {
+    rp.stride = 1 << level;
+    rp.sw = cdiv(c.W, rp.stride);
+    rp.sh = cdiv(c.H, rp.stride);
+    const int samples = rp.sw * rp.sh;
+    const int nb = cdiv(samples, kThreads);
+    for (int it = 0; it < kIters[level]; ++it) {
+      DS_LAUNCH(c, KK_RIGID, 100.0 * samples, nb, kThreads, 0, k_rigid_terms, rp, c.d_pose,
+                c.mm_idx, c.M(), c.f_vert, c.f_nrm, c.f_flag, c.red_part);
+      DS_LAUNCH(c, KK_RIGID, 8.0 * kTerms * nb, 1, 256, 0, k_rigid_finalize, c.red_part, nb,
+                level, c.d_pose, c.dsc);
+    }
+  }
+  double pose[12];
+  DS_CUDA(cudaMemcpyAsync(pose, c.d_pose, sizeof pose, cudaMemcpyDeviceToHost, c.stream));
+  fetch_scalars(c);  // syncs
+  const int pairs = c.hsc->rigid_pairs;
+  const double abs_r = c.hsc->rigid_abs;
+  ds_rigid_result r{};
+  r.correspondences = pairs;
+  if (pairs < 100) {  // kRigidMinCorrespondences (solver.hpp:19)
+    std::copy(init_pose, init_pose + 12, r.pose);
+    r.low_confidence = 1;
+    r.mean_residual = pairs > 0 ? abs_r / pairs : 0.0;
+  } else {
+    std::copy(pose, pose + 12, r.pose);
+    r.low_confidence = 0;
+    r.mean_residual = abs_r / pairs;
+  }
+  *out = r;
+}
+
+}  // namespace ds

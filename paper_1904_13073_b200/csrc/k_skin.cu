@@ -1,0 +1,504 @@
+// k_skin.cu — node graph construction and skinning (K17-K21).
+//   greedy sigma-sampling   warp_field.cpp:88-97 (init) / :151-157 (extension):
+//       exact ordered greedy (lexicographic-first maximal independent set) in
+//       one persistent CTA: candidates are tested 1024 at a time against a
+//       sigma-cell hash of accepted nodes (27 cells, strict d2 < sigma^2,
+//       spatial_grid.hpp:46-60); the uncovered ones of a chunk are resolved in
+//       index order, one accepted node per block-wide round.
+//   node edges (k=8)        warp_field.cpp:42-56, warp per node, (d2, idx) order
+//   skinning KNN (K=4)      warp_field.cpp:60-79 (VoxelGrid::knn is exact, so a
+//       brute-force (d2, idx) scan over shared-memory node tiles is identical)
+//   extension seeds         warp_field.cpp:159-178
+//   incremental skinning    warp_field.cpp:186-236
+#include "ds_blend.cuh"
+#include "ds_context.cuh"
+
+namespace ds {
+namespace {
+
+constexpr long long kEmptyKey = -1;
+
+struct HashView {
+  long long* key;
+  int* cnt;
+  int* ids;
+  int mask;
+  double inv_cell;
+};
+
+__device__ __forceinline__ long long pack_cell(int x, int y, int z) {
+  const long long b = 1LL << 20;
+  return ((x + b) << 42) | ((y + b) << 21) | (z + b);
+}
+__device__ __forceinline__ unsigned hash_cell(long long k) {
+  unsigned long long h = (unsigned long long)k * 0x9E3779B97F4A7C15ULL;
+  return (unsigned)(h >> 32);
+}
+__device__ __forceinline__ void cell_of(const HashView& h, V3 p, int& x, int& y, int& z) {
+  x = (int)floor(p.x * h.inv_cell);
+  y = (int)floor(p.y * h.inv_cell);
+  z = (int)floor(p.z * h.inv_cell);
+}
+__device__ __forceinline__ double4 ldcg_d4(const double4* p) {
+  const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ int ht_find(const HashView& h, long long k) {
+  unsigned s = hash_cell(k) & h.mask;
+  for (int probe = 0; probe <= h.mask; ++probe) {
+    const long long v = __ldcg(h.key + s);
+    if (v == k) return (int)s;
+    if (v == kEmptyKey) return -1;
+    s = (s + 1) & h.mask;
+  }
+  return -1;
+}
+// single-writer insert (only one thread of the greedy CTA mutates the table)
+__device__ void ht_insert_single(const HashView& h, long long k, int id, int* err) {
+  unsigned s = hash_cell(k) & h.mask;
+  for (int probe = 0; probe <= h.mask; ++probe) {
+    const long long v = __ldcg(h.key + s);
+    if (v == k || v == kEmptyKey) {
+      if (v == kEmptyKey) {
+        h.key[s] = k;
+        h.cnt[s] = 0;
+      }
+      const int c = __ldcg(h.cnt + s);
+      if (c >= 8) {
+        atomicOr(err, DERR_HASH_CELL);
+        return;
+      }
+      h.ids[8 * s + c] = id;
+      h.cnt[s] = c + 1;
+      return;
+    }
+    s = (s + 1) & h.mask;
+  }
+  atomicOr(err, DERR_HASH_FULL);
+}
+__device__ bool ht_any_within(const HashView& h, const double4* node_pos, V3 p, double r2) {
+  int cx, cy, cz;
+  cell_of(h, p, cx, cy, cz);
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int s = ht_find(h, pack_cell(cx + dx, cy + dy, cz + dz));
+        if (s < 0) continue;
+        const int c = __ldcg(h.cnt + s);
+        for (int q = 0; q < c; ++q) {
+          const int id = __ldcg(h.ids + 8 * s + q);
+          const double4 np = ldcg_d4(node_pos + id);
+          if (sqn(sub(v3(np.x, np.y, np.z), p)) < r2) return true;
+        }
+      }
+  return false;
+}
+
+__global__ void k_ht_prefill(HashView h, const double4* __restrict__ node_pos, int n, int* err) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double4 np = node_pos[j];
+  int cx, cy, cz;
+  cell_of(h, v3(np.x, np.y, np.z), cx, cy, cz);
+  const long long k = pack_cell(cx, cy, cz);
+  unsigned s = hash_cell(k) & h.mask;
+  for (int probe = 0; probe <= h.mask; ++probe) {
+    const long long prev = (long long)atomicCAS((unsigned long long*)(h.key + s),
+                                                (unsigned long long)kEmptyKey, (unsigned long long)k);
+    if (prev == kEmptyKey || prev == k) {
+      const int c = atomicAdd(h.cnt + s, 1);
+      if (c < 8) h.ids[8 * s + c] = j;
+      else atomicOr(err, DERR_HASH_CELL);
+      return;
+    }
+    s = (s + 1) & h.mask;
+  }
+  atomicOr(err, DERR_HASH_FULL);
+}
+
+constexpr int kGreedyThreads = 1024;
+
+__global__ void __launch_bounds__(kGreedyThreads) k_greedy_nodes(
+    const float4* __restrict__ cand, int M, double sigma, HashView h, double4* node_pos,
+    int* n_nodes, int N_cap, int* err) {
+  __shared__ int s_first;
+  __shared__ int s_count;
+  __shared__ double s_new[3];
+  const int tid = threadIdx.x;
+  if (tid == 0) s_count = *n_nodes;
+  __syncthreads();
+  const double r2 = sigma * sigma;
+  for (int base = 0; base < M; base += kGreedyThreads) {
+    const int i = base + tid;
+    V3 p = v3(0, 0, 0);
+    bool covered = true;
+    if (i < M) {
+      const float4 cp = cand[i];
+      p = v3(cp.x, cp.y, cp.z);
+      covered = ht_any_within(h, node_pos, p, r2);
+    }
+    for (;;) {
+      if (tid == 0) s_first = 0x7fffffff;
+      __syncthreads();
+      if (!covered) atomicMin(&s_first, tid);
+      __syncthreads();
+      const int f = s_first;
+      if (f == 0x7fffffff) break;
+      if (tid == f) {
+        const int id = s_count;
+        if (id < N_cap) {
+          node_pos[id] = make_double4(p.x, p.y, p.z, sigma);
+          int cx, cy, cz;
+          cell_of(h, p, cx, cy, cz);
+          ht_insert_single(h, pack_cell(cx, cy, cz), id, err);
+        } else {
+          atomicOr(err, DERR_NODE_CAP);
+        }
+        s_count = id + 1;
+        s_new[0] = p.x;
+        s_new[1] = p.y;
+        s_new[2] = p.z;
+        covered = true;
+      }
+      __syncthreads();
+      if (!covered && sqn(sub(v3(s_new[0], s_new[1], s_new[2]), p)) < r2) covered = true;
+    }
+  }
+  if (tid == 0) *n_nodes = min(s_count, N_cap);
+}
+
+__global__ void k_identity_dq(double4* dq, int from, int to) {
+  const int j = from + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= to) return;
+  dq[2 * j] = make_double4(1, 0, 0, 0);
+  dq[2 * j + 1] = make_double4(0, 0, 0, 0);
+}
+
+// Warp per node: k nearest other nodes by (d2, index).
+__global__ void k_node_edges(const double4* __restrict__ pos, int n, int k, int* __restrict__ nbr) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const int j = warp;
+  const double4 pj = pos[j];
+  double bd[8];
+  int bi[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    bd[t] = INFINITY;
+    bi[t] = 0x7fffffff;
+  }
+  for (int i = lane; i < n; i += 32) {
+    if (i == j) continue;
+    const double4 pi = pos[i];
+    const double d2 = sqn(sub(v3(pi.x, pi.y, pi.z), v3(pj.x, pj.y, pj.z)));
+    if (!nb_less(d2, i, bd[7], bi[7])) continue;
+    // insert keeping ascending (d2, idx) order
+    double cd = d2;
+    int ci = i;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (nb_less(cd, ci, bd[t], bi[t])) {
+        const double td = bd[t];
+        const int ti = bi[t];
+        bd[t] = cd;
+        bi[t] = ci;
+        cd = td;
+        ci = ti;
+      }
+    }
+  }
+  for (int r = 0; r < 8; ++r) {
+    double md = bd[0];
+    int mi = bi[0];
+    for (int off = 16; off > 0; off >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, md, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, mi, off);
+      if (nb_less(od, oi, md, mi)) {
+        md = od;
+        mi = oi;
+      }
+    }
+    if (lane == 0) nbr[8 * j + r] = (r < k && mi != 0x7fffffff) ? mi : -1;
+    if (bi[0] == mi && mi != 0x7fffffff) {  // winner pops its head
+#pragma unroll
+      for (int t = 0; t < 7; ++t) {
+        bd[t] = bd[t + 1];
+        bi[t] = bi[t + 1];
+      }
+      bd[7] = INFINITY;
+      bi[7] = 0x7fffffff;
+    }
+  }
+}
+
+constexpr int kTile = 256;
+
+// Thread per surfel: exact K nearest nodes by (d2, idx), Gaussian weights.
+__global__ void __launch_bounds__(kTile) k_skin_knn(ModelBuf m, int n, const double4* __restrict__ pos,
+                                                    int N, int K) {
+  __shared__ double4 tile[kTile];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  V3 p = v3(0, 0, 0);
+  if (i < n) {
+    const float4 rp = m.rp[i];
+    p = v3(rp.x, rp.y, rp.z);
+  }
+  double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+  for (int base = 0; base < N; base += kTile) {
+    __syncthreads();
+    if (base + threadIdx.x < N) tile[threadIdx.x] = pos[base + threadIdx.x];
+    __syncthreads();
+    const int lim = min(kTile, N - base);
+    if (i < n) {
+      for (int t = 0; t < lim; ++t) {
+        const double4 q = tile[t];
+        const double d2 = sqn(sub(v3(q.x, q.y, q.z), p));
+        const int id = base + t;
+        if (!nb_less(d2, id, bd[3], bi[3])) continue;
+        double cd = d2;
+        int ci = id;
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+          if (nb_less(cd, ci, bd[s], bi[s])) {
+            const double td = bd[s];
+            const int ti = bi[s];
+            bd[s] = cd;
+            bi[s] = ci;
+            cd = td;
+            ci = ti;
+          }
+      }
+    }
+  }
+  if (i >= n) return;
+  int ids[4];
+  float w[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const bool ok = s < K && bi[s] != 0x7fffffff;
+    ids[s] = ok ? bi[s] : -1;
+    if (ok) {
+      const double4 q = pos[bi[s]];
+      w[s] = (float)skin_weight(p, v3(q.x, q.y, q.z), q.w);
+    } else {
+      w[s] = 0.f;
+    }
+  }
+  m.ki[i] = make_int4(ids[0], ids[1], ids[2], ids[3]);
+  m.kw[i] = make_float4(w[0], w[1], w[2], w[3]);
+}
+
+// Seeds of appended nodes from their K nearest pre-existing nodes.
+__global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, int N, int K) {
+  const int jn = N0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (jn >= N) return;
+  DQ out = dq_identity();
+  if (N0 > 0) {
+    const double4 pn = pos[jn];
+    const V3 p = v3(pn.x, pn.y, pn.z);
+    double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+    int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+    for (int i = 0; i < N0; ++i) {
+      const double4 q = pos[i];
+      const double d2 = sqn(sub(v3(q.x, q.y, q.z), p));
+      if (!nb_less(d2, i, bd[3], bi[3])) continue;
+      double cd = d2;
+      int ci = i;
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        if (nb_less(cd, ci, bd[s], bi[s])) {
+          const double td = bd[s];
+          const int ti = bi[s];
+          bd[s] = cd;
+          bi[s] = ci;
+          cd = td;
+          ci = ti;
+        }
+    }
+    Q4 rs = q4(0, 0, 0, 0), ds_ = q4(0, 0, 0, 0);
+    const int cnt = min(K, N0);
+    const Q4 pivot = ld_q_plain(dq + 2 * bi[0]);
+    for (int s = 0; s < cnt; ++s) {
+      const double4 q = pos[bi[s]];
+      const double w = skin_weight(p, v3(q.x, q.y, q.z), q.w);
+      const Q4 r = ld_q_plain(dq + 2 * bi[s]);
+      const Q4 d = ld_q_plain(dq + 2 * bi[s] + 1);
+      const double sign = (qdot(pivot, r) < 0.0) ? -1.0 : 1.0;
+      rs = qadd(rs, qscl(sign * w, r));
+      ds_ = qadd(ds_, qscl(sign * w, d));
+    }
+    if (!(qnrm(rs) < kDegenerateBlend)) {
+      DQ raw;
+      raw.r = rs;
+      raw.d = ds_;
+      out = dq_normalized(raw);
+    }
+  }
+  dq[2 * jn] = make_double4(out.r.w, out.r.x, out.r.y, out.r.z);
+  dq[2 * jn + 1] = make_double4(out.d.w, out.d.x, out.d.y, out.d.z);
+}
+
+// update_skinning_incremental (warp_field.cpp:186-236), thread per surfel.
+__global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict__ pos, int first,
+                                   int N, int K) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 rp = m.rp[i];
+  const V3 p = v3(rp.x, rp.y, rp.z);
+  const int4 ki = m.ki[i];
+  const float4 kw = m.kw[i];
+  int count = entry_count(ki);
+  double sd[4];
+  int si[4];
+  double sw[4];
+  const int ids[4] = {ki.x, ki.y, ki.z, ki.w};
+  const double ws[4] = {kw.x, kw.y, kw.z, kw.w};
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s < count) {
+      const double4 q = pos[ids[s]];
+      sd[s] = sqn(sub(v3(q.x, q.y, q.z), p));
+      si[s] = ids[s];
+      sw[s] = ws[s];
+    } else {
+      sd[s] = INFINITY;
+      si[s] = 0x7fffffff;
+      sw[s] = 0;
+    }
+  }
+  // insertion sort of the first `count` slots
+  for (int a = 1; a < count; ++a)
+    for (int b = a; b > 0 && nb_less(sd[b], si[b], sd[b - 1], si[b - 1]); --b) {
+      const double td = sd[b];
+      sd[b] = sd[b - 1];
+      sd[b - 1] = td;
+      const int ti = si[b];
+      si[b] = si[b - 1];
+      si[b - 1] = ti;
+      const double tw = sw[b];
+      sw[b] = sw[b - 1];
+      sw[b - 1] = tw;
+    }
+  bool changed = false;
+  for (int j = first; j < N; ++j) {
+    const double4 q = pos[j];
+    const double d2 = sqn(sub(v3(q.x, q.y, q.z), p));
+    int slot;
+    if (count < K) {
+      slot = count++;
+    } else if (nb_less(d2, j, sd[count - 1], si[count - 1])) {
+      slot = count - 1;
+    } else {
+      continue;
+    }
+    sd[slot] = d2;
+    si[slot] = j;
+    sw[slot] = skin_weight(p, v3(q.x, q.y, q.z), q.w);
+    for (int b = slot; b > 0 && nb_less(sd[b], si[b], sd[b - 1], si[b - 1]); --b) {
+      const double td = sd[b];
+      sd[b] = sd[b - 1];
+      sd[b - 1] = td;
+      const int ti = si[b];
+      si[b] = si[b - 1];
+      si[b - 1] = ti;
+      const double tw = sw[b];
+      sw[b] = sw[b - 1];
+      sw[b - 1] = tw;
+    }
+    changed = true;
+  }
+  if (!changed) return;
+  int o[4];
+  float w[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    o[s] = s < count ? si[s] : -1;
+    w[s] = s < count ? (float)sw[s] : 0.f;
+  }
+  m.ki[i] = make_int4(o[0], o[1], o[2], o[3]);
+  m.kw[i] = make_float4(w[0], w[1], w[2], w[3]);
+}
+
+HashView hash_view(Ctx& c) {
+  HashView h;
+  h.key = c.ht_key;
+  h.cnt = c.ht_cnt;
+  h.ids = c.ht_ids;
+  h.mask = c.HT - 1;
+  h.inv_cell = 1.0 / c.cfg.node_sigma;
+  return h;
+}
+
+void clear_hash(Ctx& c) {
+  DS_CUDA(cudaMemsetAsync(c.ht_key, 0xff, sizeof(long long) * c.HT, c.stream));
+  DS_CUDA(cudaMemsetAsync(c.ht_cnt, 0, sizeof(int) * c.HT, c.stream));
+}
+
+// runs the greedy CTA over `cand` starting at node count n0; returns new count
+int greedy(Ctx& c, const float4* cand, int M, int n0) {
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->n_nodes, &n0, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
+  DS_LAUNCH(c, KK_GREEDY_NODES, 16.0 * M, 1, kGreedyThreads, 0, k_greedy_nodes, cand, M,
+            c.cfg.node_sigma, hash_view(c), c.node_pos, &c.dsc->n_nodes, c.N_cap, &c.dsc->err);
+  int res[2];
+  DS_CUDA(cudaMemcpyAsync(&res[0], &c.dsc->n_nodes, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  DS_CUDA(cudaMemcpyAsync(&res[1], &c.dsc->err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  sync(c);
+  if (res[1] & DERR_NODE_CAP) fail(DS_ERR_CAPACITY, "node capacity exceeded");
+  if (res[1] & (DERR_HASH_CELL | DERR_HASH_FULL))
+    fail(DS_ERR_CAPACITY, "node hash overflow (nodes closer than node_sigma?)");
+  return res[0];
+}
+
+}  // namespace
+
+void compute_node_edges(Ctx& c) {
+  const int n = c.n_nodes;
+  if (n == 0) return;
+  const int k = std::min(8, std::max(0, c.cfg.node_neighbor_k));
+  DS_LAUNCH(c, KK_NODE_EDGES, 32.0 * n + 32.0 * n, cdiv((long long)n * 32, 256), 256, 0,
+            k_node_edges, c.node_pos, n, k, c.node_nbr);
+}
+
+void init_warp_field(Ctx& c) {
+  if (c.n_surfels == 0) fail(DS_ERR_EMPTY_GEOMETRY, "init_warp_field: no reference surfels");
+  clear_hash(c);
+  const int n = greedy(c, c.M().rp, c.n_surfels, 0);
+  c.n_nodes = n;
+  DS_LAUNCH(c, KK_MISC, 64.0 * n, cdiv(n, 128), 128, 0, k_identity_dq, c.node_dq, 0, n);
+  compute_node_edges(c);
+  DS_LAUNCH(c, KK_SKIN_KNN, 48.0 * c.n_surfels, cdiv(c.n_surfels, kTile), kTile, 0, k_skin_knn,
+            c.M(), c.n_surfels, c.node_pos, n, std::min(4, c.cfg.knn_k));
+}
+
+int extend_warp_field(Ctx& c, const float4* positions, int n) {
+  if (n == 0) return 0;
+  const int n0 = c.n_nodes;
+  clear_hash(c);
+  if (n0 > 0) {
+    DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
+    DS_LAUNCH(c, KK_GREEDY_NODES, 32.0 * n0, cdiv(n0, 256), 256, 0, k_ht_prefill, hash_view(c),
+              c.node_pos, n0, &c.dsc->err);
+  }
+  const int total = greedy(c, positions, n, n0);
+  const int added = total - n0;
+  c.n_nodes = total;
+  if (added > 0) {
+    DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, cdiv(added, 64), 64, 0, k_seed_dq, c.node_pos,
+              c.node_dq, n0, total, std::min(4, c.cfg.knn_k));
+    compute_node_edges(c);
+  }
+  return added;
+}
+
+void update_skinning_incremental(Ctx& c, int first_new) {
+  if (first_new >= c.n_nodes || c.n_surfels == 0) return;
+  DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 48.0 * c.n_surfels, cdiv(c.n_surfels, 256), 256, 0,
+            k_skin_incremental, c.M(), c.n_surfels, c.node_pos, first_new, c.n_nodes,
+            std::min(4, c.cfg.knn_k));
+}
+
+}  // namespace ds

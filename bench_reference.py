@@ -1,0 +1,43 @@
+"""`bench.py --impl reference`: the reference algorithm timed on the host cores.
+
+The reference C++ sources cannot be compiled here (Eigen 3, libpng, GTest and
+vendored json/CLI11 are absent), so this arm times the CPU
+oracle — the fp64 line-by-line restatement in oracle/ — on the same workload,
+config and metric as bench.py's B200 arm. Each step is a bounded sample (see
+bench.cpu_sample): real per-stage timings plus the dense 6N x 6N LDLT cost
+extrapolated from a measured factorisation rate.
+"""
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+
+def run_reference(args):
+    import bench
+
+    spec = bench.CFG2 if args.config == "cfg2" else bench.CFG1
+    cfg = bench.make_cfg(spec)
+    values = []
+    samples = []
+    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
+        cs = bench.cpu_sample(spec, cfg)
+        gn = 10.0
+        t_lin = cs["t_lin"] if cs["t_lin"] is not None else 0.0
+        t_frame = (t_lin + cs["t_ldlt"]) * gn
+        values.append(1.0 / t_frame)
+        samples.append(cs)
+    v = float(np.median(values))
+    cs = samples[-1]
+    return {
+        "impl": "reference", "metric": "frames/s", "value": round(v, 6), "unit": "frames/s",
+        "n_gpus": 0, "steps": len(values), "warmup": 0, "higher_is_better": True,
+        "config": {"workload": f"{args.config}: {spec['scene']} {spec['width']}x{spec['height']}"},
+        "cpu_baseline": {"value": round(v, 6), "unit": "frames/s", "cores": 1, "kind": "port",
+                         "sample": f"oracle stages + dense LDLT dim {cs['dim']} extrapolated "
+                                   f"({cs['ldlt_rate_gflops']:.2f} GFLOP/s) x 10 GN iters"},
+        "e2e": {"value": round(v, 6), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }

@@ -79,9 +79,9 @@ typedef struct ds_config {
   int32_t width, height;
   /* ---- device-only ---- */
   int32_t pcg_max_iters; /* block-Jacobi PCG iterations per LM attempt */
-  int32_t max_surfels;   /* capacity; 0 = 4 x width x height */
+  int32_t max_surfels;   /* capacity; 0 = 8 x width x height */
   double pcg_tol;        /* relative residual; 0 = run pcg_max_iters */
-  int32_t max_nodes;     /* capacity; 0 = 16384 */
+  int32_t max_nodes;     /* capacity; 0 = 8192 */
   int32_t profile;       /* 1 = time every kernel launch with CUDA events */
 } ds_config;
 
@@ -232,11 +232,14 @@ ds_status ds_clean_and_reset(ds_context* ctx, const double* pose, int32_t* remov
 /* ---- measurement ---- */
 int32_t ds_num_kernel_kinds(void);
 const char* ds_kernel_name(int32_t kind);
-/* per kernel kind since the last reset: launches, summed CUDA-event ms (profile=1),
- * algorithmic bytes moved */
+/* per kernel kind since the last reset: launches, summed CUDA-event ms and
+ * algorithmic bytes of the PROFILED launches (profiling on); with profiling
+ * never on, `launches` counts all launches */
 ds_status ds_kernel_stats(ds_context* ctx, int32_t kind, int64_t* launches, double* total_ms,
                           double* algorithmic_bytes);
 ds_status ds_reset_kernel_stats(ds_context* ctx);
+/* turn per-launch CUDA-event timing on/off (cfg.profile at create) */
+ds_status ds_set_profiling(ds_context* ctx, int32_t enable);
 ds_status ds_total_launches(const ds_context* ctx, int64_t* launches);
 
 /* ---- synthetic depth streams (synth.hpp:16-73; host only) ---- */

@@ -120,6 +120,7 @@ SIGNATURES = {
     "ds_kernel_name": [I32],
     "ds_kernel_stats": [P, I32, C.POINTER(C.c_int64), PD, PD],
     "ds_reset_kernel_stats": [P],
+    "ds_set_profiling": [P, I32],
     "ds_total_launches": [P, C.POINTER(C.c_int64)],
     "ds_synth_scenario": [C.c_char_p],
     "ds_synth_scenario_name": [I32],

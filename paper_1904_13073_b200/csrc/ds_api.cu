@@ -24,7 +24,7 @@ const char* kKernelNames[KK_COUNT] = {
 
 size_t sort_temp_bytes(int n);
 int pcg_max_grid(int num_sms);
-void build_pattern(Ctx& c);
+void build_pattern(Ctx& c, int t_now, int t_last);
 void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last);
 void fuse_depth_async(Ctx& c, const double* pose, int t_now);
 
@@ -58,10 +58,14 @@ void launch_end(Ctx& c, int kind, double bytes) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     throw Error{DS_ERR_CUDA, std::string("kernel ") + kKernelNames[kind] + ": " + cudaGetErrorString(e)};
-  if (c.cfg.profile && !c.prof_pending.empty()) DS_CUDA(cudaEventRecord(c.prof_pending.back().b, c.stream));
   c.launches[kind] += 1;
   c.total_launches += 1;
-  c.prof_bytes[kind] += bytes;
+  if (c.cfg.profile && !c.prof_pending.empty()) {
+    // launches/bytes of the profiled launches only, so bytes / ms is a rate
+    DS_CUDA(cudaEventRecord(c.prof_pending.back().b, c.stream));
+    c.prof_launches[kind] += 1;
+    c.prof_bytes[kind] += bytes;
+  }
 }
 void prof_flush(Ctx& c) {
   for (auto& r : c.prof_pending) {
@@ -137,7 +141,7 @@ void allocate(Ctx& c) {
   c.W = k.width;
   c.H = k.height;
   c.P = c.W * c.H;
-  c.S_cap = k.max_surfels > 0 ? k.max_surfels : std::max(4 * c.P, 4096);
+  c.S_cap = k.max_surfels > 0 ? k.max_surfels : std::max(8 * c.P, 4096);
   c.N_cap = k.max_nodes > 0 ? k.max_nodes : 8192;
   c.R_cap = c.S_cap * 10 + c.N_cap * 24;
   c.UB_cap = std::min(c.R_cap, std::max(48 * c.N_cap, 65536));
@@ -199,6 +203,14 @@ void allocate(Ctx& c) {
   c.bsr_val = dalloc<float>(c, (size_t)c.B_cap * 36);
   c.bsr_touch = dalloc<uint8_t>(c, c.B_cap);
   c.diag_pos = dalloc<int>(c, N);
+  c.CH_cap = c.R_cap / 64 + c.UB_cap + 1;
+  c.chunk_first = dalloc<int>(c, c.UB_cap + 1);
+  c.chunk_ub = dalloc<int>(c, c.CH_cap);
+  c.part_h = dalloc<float>(c, (size_t)c.CH_cap * 36);
+  c.part_g = dalloc<double>(c, (size_t)c.CH_cap * 6);
+  c.part_t = dalloc<int>(c, c.CH_cap);
+  c.rows_l = dalloc<float>(c, P * 24);
+  c.r_l = dalloc<double>(c, P);
   c.cub_tmp_bytes = sort_temp_bytes(c.R_cap);
   c.cub_tmp = dalloc<char>(c, c.cub_tmp_bytes);
   c.g = dalloc<double>(c, 6 * N);
@@ -222,6 +234,7 @@ void allocate(Ctx& c) {
   c.cand_ok_scan = dalloc<int>(c, P + 1);
   c.keep = dalloc<int>(c, S + P + 1);
   c.keep_scan = dalloc<int>(c, S + P + 1);
+  c.ext_pos = dalloc<float4>(c, P);
   c.ht_key = dalloc<long long>(c, c.HT);
   c.ht_cnt = dalloc<int>(c, c.HT);
   c.ht_ids = dalloc<int>(c, 8 * (size_t)c.HT);
@@ -231,6 +244,8 @@ void allocate(Ctx& c) {
   c.red_part_n = cdiv(c.P, 256) * 29 + cdiv(8 * (long long)N, 256) + cdiv(c.P, 256) + 64;
   c.red_part = dalloc<double>(c, c.red_part_n);
   c.d_pose = dalloc<double>(c, 12);
+  c.tickets = dalloc<unsigned>(c, 16);
+  DS_CUDA(cudaMemsetAsync(c.tickets, 0, 16 * sizeof(unsigned), c.stream));
   c.dsc = dalloc<DevScalars>(c, 1);
   DS_CUDA(cudaMallocHost(&c.hsc, sizeof(DevScalars)));
   DS_CUDA(cudaMallocHost(&c.h_depth_pinned, sizeof(uint16_t) * P));
@@ -956,7 +971,7 @@ ds_status ds_build_normal_equations(ds_context* ctx, const double* pose, int32_t
   Ctx& c = ctx->c;
   bind(c);
   REQUIRE(c.frame_ready, "no frame maps");
-  ds::build_pattern(c);
+  ds::build_pattern(c, t_now, t_last);
   ds::gn_linearize(c, pose, t_now, t_last, e_pre, n_pairs);
   if (n_blocks) *n_blocks = c.n_full;
   API_END
@@ -1179,7 +1194,8 @@ ds_status ds_kernel_stats(ds_context* ctx, int32_t kind, int64_t* launches, doub
   Ctx& c = ctx->c;
   bind(c);
   ds::sync(c);
-  if (launches) *launches = c.launches[kind];
+  if (launches) *launches = c.cfg.profile || c.prof_launches[kind] ? c.prof_launches[kind]
+                                                                  : c.launches[kind];
   if (total_ms) *total_ms = c.prof_ms[kind];
   if (bytes) *bytes = c.prof_bytes[kind];
   API_END
@@ -1192,10 +1208,20 @@ ds_status ds_reset_kernel_stats(ds_context* ctx) {
   ds::sync(c);
   for (int k = 0; k < ds::KK_COUNT; ++k) {
     c.launches[k] = 0;
+    c.prof_launches[k] = 0;
     c.prof_ms[k] = 0;
     c.prof_bytes[k] = 0;
   }
   c.total_launches = 0;
+  API_END
+}
+ds_status ds_set_profiling(ds_context* ctx, int32_t enable) {
+  API_BEGIN
+  REQUIRE(ctx, "null context");
+  Ctx& c = ctx->c;
+  bind(c);
+  ds::sync(c);
+  c.cfg.profile = enable ? 1 : 0;
   API_END
 }
 ds_status ds_total_launches(const ds_context* ctx, int64_t* launches) {

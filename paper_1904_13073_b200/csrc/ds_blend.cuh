@@ -61,6 +61,33 @@ __device__ __forceinline__ Blend blend_entry(int4 ki, float4 kw, const double4* 
   return b;
 }
 
+// Same rigid transform as blend_rig() up to rounding, with one rsqrt instead of
+// the ~24 fp64 divisions of normalized() -> to_se3() -> normalize(): used where
+// the result is a continuous quantity (warped positions/normals, residuals).
+__device__ __forceinline__ Rig blend_rig_fast(const Blend& b) {
+  const double ia = rsqrt(qdot(b.rs, b.rs));
+  const Q4 nr = qscl(ia, b.rs);
+  const double k = qdot(b.rs, b.ds) * (ia * ia * ia);
+  const Q4 nd = qsub(qscl(ia, b.ds), qscl(k, b.rs));
+  const double tx = 2.0 * nr.x, ty = 2.0 * nr.y, tz = 2.0 * nr.z;
+  const double twx = tx * nr.w, twy = ty * nr.w, twz = tz * nr.w;
+  const double txx = tx * nr.x, txy = ty * nr.x, txz = tz * nr.x;
+  const double tyy = ty * nr.y, tyz = tz * nr.y, tzz = tz * nr.z;
+  Rig T;
+  T.R.m[0] = 1.0 - (tyy + tzz);
+  T.R.m[1] = txy - twz;
+  T.R.m[2] = txz + twy;
+  T.R.m[3] = txy + twz;
+  T.R.m[4] = 1.0 - (txx + tzz);
+  T.R.m[5] = tyz - twx;
+  T.R.m[6] = txz - twy;
+  T.R.m[7] = tyz + twx;
+  T.R.m[8] = 1.0 - (txx + tyy);
+  const Q4 tq = qmul(nd, qconj(nr));
+  T.t = v3(2.0 * tq.x, 2.0 * tq.y, 2.0 * tq.z);
+  return T;
+}
+
 // Rigid transform of a non-degenerate blend: normalized() then to_se3()
 // (which normalizes again), as blend_dual_quaternions + to_se3 do.
 __device__ __forceinline__ Rig blend_rig(const Blend& b) {

@@ -165,7 +165,15 @@ struct Ctx {
   float* bsr_val = nullptr;
   uint8_t* bsr_touch = nullptr;
   int* diag_pos = nullptr;
-  int n_records = 0, n_up = 0, n_full = 0;
+  int* chunk_first = nullptr;  // per upper block: first assembly chunk (n_up + 1)
+  int* chunk_ub = nullptr;     // per chunk: upper block
+  float* part_h = nullptr;     // per chunk: 6x6 partial
+  double* part_g = nullptr;    // per chunk: g partial
+  int* part_t = nullptr;       // per chunk: touched
+  float* rows_l = nullptr;     // pair rows in per-surfel list order
+  double* r_l = nullptr;       // pair residuals in list order
+  int n_records = 0, n_up = 0, n_full = 0, n_chunks = 0, CH_cap = 0;
+  double n_pairs_ok_est = 0;
   bool pattern_ready = false;
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
@@ -192,6 +200,7 @@ struct Ctx {
   int* cand_ok_scan = nullptr;
   int* keep = nullptr;
   int* keep_scan = nullptr;
+  float4* ext_pos = nullptr;  // uncovered extension candidates (ordered)
   // greedy node hash
   long long* ht_key = nullptr;
   int* ht_cnt = nullptr;
@@ -202,6 +211,7 @@ struct Ctx {
   double* red_part = nullptr;
   int red_part_n = 0;
   double* d_pose = nullptr;  // 12 doubles
+  unsigned* tickets = nullptr;  // last-block tickets of fused grid reductions
   DevScalars* dsc = nullptr;
   DevScalars* hsc = nullptr;  // pinned mirror
   uint16_t* h_depth_pinned = nullptr;
@@ -217,6 +227,7 @@ struct Ctx {
   int64_t launches[KK_COUNT] = {0};
   double prof_ms[KK_COUNT] = {0};
   double prof_bytes[KK_COUNT] = {0};
+  int64_t prof_launches[KK_COUNT] = {0};
   int64_t total_launches = 0;
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> event_pool;

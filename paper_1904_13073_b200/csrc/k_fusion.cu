@@ -164,28 +164,28 @@ __device__ bool inv_warp_reweighted(V3 x, const int* ids, int cnt, const double4
 
 // skin_appended + check_compressive for candidate k (fusion.cpp:77-177).
 // result: 0 = low support, 1 = compressive reject, 2 = accepted
-__device__ int screen_one(V3 x, const double4* __restrict__ node_pos,
+__device__ __forceinline__ void knn4_insert(double d2, int j, double bd[4], int bi[4]) {
+  if (!nb_less(d2, j, bd[3], bi[3])) return;
+  double cd = d2;
+  int ci = j;
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+    if (nb_less(cd, ci, bd[s], bi[s])) {
+      const double td = bd[s];
+      const int ti = bi[s];
+      bd[s] = cd;
+      bi[s] = ci;
+      cd = td;
+      ci = ti;
+    }
+}
+
+// Eq. 6 ratio test, weights, delta_nn, compressive check on a K-NN list.
+__device__ int screen_one(V3 x, const double bd[4], const int bi[4],
+                          const double4* __restrict__ node_pos,
                           const double4* __restrict__ node_live, const double4* __restrict__ node_dq,
                           const ScreenParams& sp, int ids[4], float ws[4], int& cnt) {
-  double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-  int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-  for (int j = 0; j < sp.N; ++j) {
-    const double4 nl = node_live[j];
-    const double d2 = sqn(sub(v3(nl.x, nl.y, nl.z), x));
-    if (!nb_less(d2, j, bd[3], bi[3])) continue;
-    double cd = d2;
-    int ci = j;
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-      if (nb_less(cd, ci, bd[s], bi[s])) {
-        const double td = bd[s];
-        const int ti = bi[s];
-        bd[s] = cd;
-        bi[s] = ci;
-        cd = td;
-        ci = ti;
-      }
-  }
+  (void)bd;
   const int k = min(sp.K, sp.N);
   const int n0 = bi[0];
   const double4 l0 = node_live[n0], p0 = node_pos[n0];
@@ -237,17 +237,42 @@ __global__ void k_screen(const float4* __restrict__ cp, const int* __restrict__ 
                          const double4* __restrict__ node_dq, ScreenParams sp,
                          int4* __restrict__ cki, float4* __restrict__ ckw, int* __restrict__ ok,
                          int* __restrict__ res_out, int* __restrict__ low, int* __restrict__ comp) {
+  __shared__ double4 tile[128];
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = *n_cand_dev;
-  if (k >= n) {
-    return;
+  if (blockIdx.x * blockDim.x >= n) return;  // whole block idle
+  const bool active = k < n;
+  V3 x = v3(0, 0, 0);
+  if (active) {
+    const float4 p = cp[k];
+    x = v3(p.x, p.y, p.z);
   }
-  const float4 p = cp[k];
+  // brute-force live-frame K-NN over shared-memory tiles of node live positions
+  double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+  float thr = INFINITY;
+  for (int base = 0; base < sp.N; base += 128) {
+    __syncthreads();
+    if (base + threadIdx.x < sp.N) tile[threadIdx.x] = node_live[base + threadIdx.x];
+    __syncthreads();
+    const int lim = min(128, sp.N - base);
+    if (active)
+      for (int t = 0; t < lim; ++t) {
+        const double4 nl = tile[t];
+        // fp32 pre-test on the exactly-subtracted differences: d2f <= d2 (1 + 4e-7),
+        // so every node that can enter the exact (d2, idx) top-K passes it
+        const float dx = (float)(nl.x - x.x), dy = (float)(nl.y - x.y), dz = (float)(nl.z - x.z);
+        if ((dx * dx + dy * dy) + dz * dz > thr) continue;
+        knn4_insert(sqn(sub(v3(nl.x, nl.y, nl.z), x)), base + t, bd, bi);
+        if (bd[3] < INFINITY) thr = (float)(bd[3] * (1.0 + 1e-5)) + 1e-37f;
+      }
+  }
+  if (!active) return;
   int ids[4];
   float ws[4];
   int cnt = 0;
   int res = 0;
-  if (sp.N > 0) res = screen_one(v3(p.x, p.y, p.z), node_pos, node_live, node_dq, sp, ids, ws, cnt);
+  if (sp.N > 0) res = screen_one(x, bd, bi, node_pos, node_live, node_dq, sp, ids, ws, cnt);
   if (sp.N == 0) {
     for (int m = 0; m < 4; ++m) {
       ids[m] = -1;
@@ -351,7 +376,7 @@ __global__ void __launch_bounds__(256) k_compact_inverse(ModelBuf src, ModelBuf 
   const Blend b = blend_entry(ki, kw, node_dq);
   float4 rp = lp, rn = ln;
   if (!b.degenerate) {
-    const Rig inv = rig_inverse(blend_rig(b));
+    const Rig inv = rig_inverse(blend_rig_fast(b));
     const V3 p = rig_apply(inv, v3(lp.x, lp.y, lp.z));
     const V3 q = rig_rotate(inv, v3(ln.x, ln.y, ln.z));
     rp = make_float4((float)p.x, (float)p.y, (float)p.z, lp.w);

@@ -168,6 +168,22 @@ __global__ void __launch_bounds__(kGreedyThreads) k_greedy_nodes(
   if (tid == 0) *n_nodes = min(s_count, N_cap);
 }
 
+// Exact pre-filter for extension: a candidate within sigma of a pre-existing
+// node is skipped by the ordered greedy whatever happens before it, so only the
+// uncovered ones (kept in order) need the sequential pass.
+__global__ void k_uncovered(const float4* __restrict__ cand, int M, double sigma, HashView h,
+                            const double4* __restrict__ node_pos, int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const float4 cp = cand[i];
+  flag[i] = ht_any_within(h, node_pos, v3(cp.x, cp.y, cp.z), sigma * sigma) ? 0 : 1;
+}
+__global__ void k_gather_uncovered(const float4* __restrict__ cand, const int* __restrict__ flag,
+                                   const int* __restrict__ scan, int M, float4* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M && flag[i]) out[scan[i]] = cand[i];
+}
+
 __global__ void k_identity_dq(double4* dq, int from, int to) {
   const int j = from + blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= to) return;
@@ -247,6 +263,7 @@ __global__ void __launch_bounds__(kTile) k_skin_knn(ModelBuf m, int n, const dou
   }
   double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
   int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+  float thr = INFINITY;
   for (int base = 0; base < N; base += kTile) {
     __syncthreads();
     if (base + threadIdx.x < N) tile[threadIdx.x] = pos[base + threadIdx.x];
@@ -255,6 +272,9 @@ __global__ void __launch_bounds__(kTile) k_skin_knn(ModelBuf m, int n, const dou
     if (i < n) {
       for (int t = 0; t < lim; ++t) {
         const double4 q = tile[t];
+        // fp32 pre-test (see k_screen): never rejects a node of the exact top-K
+        const float fx = (float)(q.x - p.x), fy = (float)(q.y - p.y), fz = (float)(q.z - p.z);
+        if ((fx * fx + fy * fy) + fz * fz > thr) continue;
         const double d2 = sqn(sub(v3(q.x, q.y, q.z), p));
         const int id = base + t;
         if (!nb_less(d2, id, bd[3], bi[3])) continue;
@@ -270,6 +290,7 @@ __global__ void __launch_bounds__(kTile) k_skin_knn(ModelBuf m, int n, const dou
             cd = td;
             ci = ti;
           }
+        if (bd[3] < INFINITY) thr = (float)(bd[3] * (1.0 + 1e-5)) + 1e-37f;
       }
     }
   }
@@ -478,12 +499,23 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
   if (n == 0) return 0;
   const int n0 = c.n_nodes;
   clear_hash(c);
+  const float4* cand = positions;
+  int m = n;
   if (n0 > 0) {
     DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
     DS_LAUNCH(c, KK_GREEDY_NODES, 32.0 * n0, cdiv(n0, 256), 256, 0, k_ht_prefill, hash_view(c),
               c.node_pos, n0, &c.dsc->err);
+    DS_LAUNCH(c, KK_GREEDY_NODES, 20.0 * n, cdiv(n, 256), 256, 0, k_uncovered, positions, n,
+              c.cfg.node_sigma, hash_view(c), c.node_pos, c.keep);
+    scan_exclusive(c, c.keep, c.keep_scan, n);
+    DS_LAUNCH(c, KK_GREEDY_NODES, 24.0 * n, cdiv(n, 256), 256, 0, k_gather_uncovered, positions,
+              c.keep, c.keep_scan, n, c.ext_pos);
+    DS_CUDA(cudaMemcpyAsync(&m, c.keep_scan + n, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    sync(c);
+    cand = c.ext_pos;
+    if (m == 0) return 0;
   }
-  const int total = greedy(c, positions, n, n0);
+  const int total = greedy(c, cand, m, n0);
   const int added = total - n0;
   c.n_nodes = total;
   if (added > 0) {

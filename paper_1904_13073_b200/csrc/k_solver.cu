@@ -26,6 +26,7 @@
 
 #include "ds_blend.cuh"
 #include "ds_context.cuh"
+#include "ds_reduce.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -68,7 +69,9 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
                                                     float* __restrict__ rows,
                                                     double* __restrict__ pair_r,
                                                     int* __restrict__ s_cnt,
-                                                    double* __restrict__ part) {
+                                                    double* __restrict__ part,
+                                                    unsigned* __restrict__ ticket,
+                                                    double* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   double e = 0.0;
   int s = c < pp.P ? pair_s[c] : -1;
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
       const double4 fv = fvert[c], fn = fnrm[c];
       const V3 vd = rig_apply(pp.pose, v3(fv.x, fv.y, fv.z));
       const V3 nd = rig_rotate(pp.pose, v3(fn.x, fn.y, fn.z));
-      const V3 y = rig_apply(blend_rig(b), p);
+      const V3 y = rig_apply(blend_rig_fast(b), p);
       const double r = dot(nd, sub(y, vd));
       e = r * r;
       // ---- u = (dy/db)^T n_d  (solver.cpp:58-92)
@@ -147,15 +150,7 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
       atomicAdd(s_cnt + s, 1);
     }
   }
-  // block reduction of the data energy (fixed order)
-  __shared__ double sh[256];
-  sh[threadIdx.x] = e;
-  __syncthreads();
-  for (int k = 128; k > 0; k >>= 1) {
-    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+  grid_sum<256>(e, part, ticket, out);  // data energy, fixed order
 }
 
 // E_data at arbitrary node transforms over the fixed pair set (solver.cpp:132-143);
@@ -166,7 +161,9 @@ __global__ void __launch_bounds__(256) k_pair_energy(const int* __restrict__ pai
                                                      const double4* __restrict__ fnrm,
                                                      PairParams pp, int mode,
                                                      double* __restrict__ part,
-                                                     int* __restrict__ count) {
+                                                     int* __restrict__ count,
+                                                     unsigned* __restrict__ ticket,
+                                                     double* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   double e = 0.0;
   int ok = 0;
@@ -178,31 +175,26 @@ __global__ void __launch_bounds__(256) k_pair_energy(const int* __restrict__ pai
       const double4 fv = fvert[c], fn = fnrm[c];
       const V3 vd = rig_apply(pp.pose, v3(fv.x, fv.y, fv.z));
       const V3 nd = rig_rotate(pp.pose, v3(fn.x, fn.y, fn.z));
-      const V3 y = rig_apply(blend_rig(b), v3(rp.x, rp.y, rp.z));
+      const V3 y = rig_apply(blend_rig_fast(b), v3(rp.x, rp.y, rp.z));
       const double r = dot(nd, sub(y, vd));
       e = mode == 0 ? r * r : fabs(r);
       ok = 1;
     }
   }
-  __shared__ double sh[256];
-  sh[threadIdx.x] = e;
-  __syncthreads();
-  for (int k = 128; k > 0; k >>= 1) {
-    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
   if (count) {
     const unsigned bal = __ballot_sync(0xffffffffu, ok);
     if ((threadIdx.x & 31) == 0 && bal) atomicAdd(count, __popc(bal));
   }
+  grid_sum<256>(e, part, ticket, out);
 }
 
 // E_reg over directed edges j -> i (solver.cpp:145-155)
 __global__ void __launch_bounds__(256) k_reg_energy(const double4* __restrict__ pos,
                                                     const int* __restrict__ nbr,
                                                     const double* __restrict__ se3, int N,
-                                                    double* __restrict__ part) {
+                                                    double* __restrict__ part,
+                                                    unsigned* __restrict__ ticket,
+                                                    double* __restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
   if (e < 8 * N) {
@@ -215,14 +207,15 @@ __global__ void __launch_bounds__(256) k_reg_energy(const double4* __restrict__ 
       v = sqn(sub(rig_apply(Tj, p), rig_apply(Ti, p)));
     }
   }
-  __shared__ double sh[256];
-  sh[threadIdx.x] = v;
-  __syncthreads();
-  for (int k = 128; k > 0; k >>= 1) {
-    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+  grid_sum<256>(v, part, ticket, out);
+}
+
+__global__ void k_any_stable_flag(const float4* __restrict__ ln, int n, double delta_stable,
+                                  int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool st = i < n && (double)ln[i].w > delta_stable;
+  const unsigned b = __ballot_sync(0xffffffffu, st);
+  if ((threadIdx.x & 31) == 0 && b) atomicOr(flag, 1);
 }
 
 // ---------------------------------------------------------------- pair lists
@@ -236,13 +229,19 @@ __global__ void k_scatter_pairs(const int* __restrict__ pair_s, const uint8_t* _
   const int k = atomicAdd(s_cur + s, 1);
   s_list[s_off[s] + k] = c;
 }
+// Sort each surfel's pair list into pixel order (deterministic summation order)
+// and gather the pairs' Jacobian rows / residuals into list order, so the block
+// assembly reads one contiguous run per surfel.
 __global__ void k_sort_lists(const int* __restrict__ s_cnt, const int* __restrict__ s_off, int n,
-                             int* __restrict__ s_list) {
+                             int* __restrict__ s_list, const float* __restrict__ rows,
+                             const double* __restrict__ pair_r, float* __restrict__ rows_l,
+                             double* __restrict__ r_l) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int cnt = s_cnt[s];
-  if (cnt < 2) return;
-  int* l = s_list + s_off[s];
+  if (cnt == 0) return;
+  const int off = s_off[s];
+  int* l = s_list + off;
   for (int a = 1; a < cnt; ++a) {
     const int v = l[a];
     int b = a;
@@ -252,16 +251,43 @@ __global__ void k_sort_lists(const int* __restrict__ s_cnt, const int* __restric
     }
     l[b] = v;
   }
+  for (int q = 0; q < cnt; ++q) {
+    const int pix = l[q];
+    const float4* src = reinterpret_cast<const float4*>(rows + (size_t)pix * 24);
+    float4* dst = reinterpret_cast<float4*>(rows_l + (size_t)(off + q) * 24);
+#pragma unroll
+    for (int t = 0; t < 6; ++t) dst[t] = src[t];
+    r_l[off + q] = pair_r[pix];
+  }
 }
 
 // ------------------------------------------------------------ block pattern
 __constant__ int kSlotPairs[10][2] = {{0, 0}, {0, 1}, {0, 2}, {0, 3}, {1, 1},
                                       {1, 2}, {1, 3}, {2, 2}, {2, 3}, {3, 3}};
 
-__global__ void k_gen_records(const int4* __restrict__ ki, int n, int N, int* __restrict__ key,
-                              int* __restrict__ val) {
+// A surfel can only own correspondence pairs if render_model_maps draws it
+// (raster.cpp:42-49, 65-68); eligibility is fixed during one frame's solve.
+__global__ void k_elig_flags(const float4* __restrict__ ln, const int2* __restrict__ tt, int n,
+                             double delta_stable, int t_now, int delta_recent, int host_boot,
+                             const int* __restrict__ any_stable, int* __restrict__ flag) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
+  const bool stable = (double)ln[s].w > delta_stable;
+  const bool recent = (t_now - tt[s].y) <= delta_recent;
+  const bool boot = host_boot || !(*any_stable);
+  flag[s] = (stable || (boot && recent)) ? 1 : 0;
+}
+__global__ void k_elig_list(const int* __restrict__ flag, const int* __restrict__ scan, int n,
+                            int* __restrict__ list) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n && flag[s]) list[scan[s]] = s;
+}
+
+__global__ void k_gen_records(const int4* __restrict__ ki, const int* __restrict__ elig, int n,
+                              int N, int* __restrict__ key, int* __restrict__ val) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int s = elig[q];
   const int4 e = ki[s];
   const int cnt = entry_count(e);
   const int id[4] = {e.x, e.y, e.z, e.w};
@@ -279,8 +305,8 @@ __global__ void k_gen_records(const int4* __restrict__ ki, int n, int N, int* __
         v = (s << 4) | (m2 << 2) | m1;
       }
     }
-    key[(size_t)s * 10 + t] = k;
-    val[(size_t)s * 10 + t] = v;
+    key[(size_t)q * 10 + t] = k;
+    val[(size_t)q * 10 + t] = v;
   }
 }
 __global__ void k_gen_reg_records(const int* __restrict__ nbr, int N, int* __restrict__ key,
@@ -387,25 +413,36 @@ __global__ void k_row_sort(const int* __restrict__ row_ptr, int N, int* __restri
 }
 
 // ------------------------------------------------------------ block assembly
-constexpr int kAsmWarps = 4;
+// The sorted records of one upper block are cut into fixed chunks of <= 64;
+// an 8-lane group reduces each chunk (lane l takes records l, l+8, ...), then
+// one thread per block sums its chunk partials in chunk order. Fixed work
+// decomposition + fixed reduction order => bit-deterministic; chunking balances
+// the diagonal blocks (hundreds of records) against off-diagonal ones.
+constexpr int kChunk = 64;
+constexpr int kChunkLanes = 8;
 
 struct AsmArgs {
   const int* up_key;
   const int* up_start;
   const int* up_pos;
   const int* up_mpos;
+  const int* chunk_ub;
+  const int* chunk_first;
   const int* rec_val;
   const int* s_cnt;
   const int* s_off;
-  const int* s_list;
-  const float* rows;
-  const double* pair_r;
+  const float* rows_l;
+  const double* r_l;
   const double4* node_pos;
   const int* nbr;
   const double* se3;
   double lambda;
   int N;
   int n_up;
+  int n_chunks;
+  float* part_h;
+  double* part_g;
+  int* part_t;
   float* bsr_val;
   uint8_t* bsr_touch;
   double* g;
@@ -437,97 +474,136 @@ __device__ __forceinline__ void reg_jac(const double4* __restrict__ pos, const i
     }
 }
 
-__global__ void __launch_bounds__(32 * kAsmWarps) k_assemble(AsmArgs A) {
-  __shared__ double red[kAsmWarps][32][43];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ub = blockIdx.x * kAsmWarps + wid;
-  if (ub >= A.n_up) return;
-  const int key = A.up_key[ub];
-  const int row = key / A.N, colb = key % A.N;
-  const bool diag = row == colb;
-  double h[36], gg[6];
+__global__ void __launch_bounds__(256) k_assemble_chunks(AsmArgs A) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = gid / kChunkLanes, l = gid % kChunkLanes;
+  const bool valid = chunk < A.n_chunks;  // uniform within a lane group
+  float h[36];
+  double gg[6];
 #pragma unroll
-  for (int t = 0; t < 36; ++t) h[t] = 0.0;
+  for (int t = 0; t < 36; ++t) h[t] = 0.f;
 #pragma unroll
   for (int t = 0; t < 6; ++t) gg[t] = 0.0;
   int touched = 0;
-  const int r0 = A.up_start[ub], r1 = A.up_start[ub + 1];
-  for (int k = r0 + lane; k < r1; k += 32) {
-    const int v = A.rec_val[k];
-    if (v < 0) {
-      const int e = (v & 0x7fffffff) >> 2, type = v & 3;
-      double Jj[3][6], Ji[3][6], rv[3];
-      reg_jac(A.node_pos, A.nbr, A.se3, e, Jj, Ji, rv);
-      touched = 1;
-      const double(*L)[6] = (type == 0 || type == 2) ? Jj : Ji;
-      const double(*R)[6] = (type == 0 || type == 3) ? Jj : Ji;
+  if (valid) {
+    const int ub = A.chunk_ub[chunk];
+    const int key = A.up_key[ub];
+    const bool diag = (key / A.N) == (key % A.N);
+    const int first = A.chunk_first[ub];
+    const int r0 = A.up_start[ub] + (chunk - first) * kChunk;
+    const int r1 = min(r0 + kChunk, A.up_start[ub + 1]);
+    for (int k = r0 + l; k < r1; k += kChunkLanes) {
+      const int v = A.rec_val[k];
+      if (v < 0) {
+        const int e = (v & 0x7fffffff) >> 2, type = v & 3;
+        double Jj[3][6], Ji[3][6], rv[3];
+        reg_jac(A.node_pos, A.nbr, A.se3, e, Jj, Ji, rv);
+        touched = 1;
+        const bool lj = (type == 0 || type == 2), rj = (type == 0 || type == 3);
 #pragma unroll
-      for (int x = 0; x < 6; ++x) {
+        for (int x = 0; x < 6; ++x) {
 #pragma unroll
-        for (int y = 0; y < 6; ++y)
-          h[x * 6 + y] += A.lambda * ((L[0][x] * R[0][y] + L[1][x] * R[1][y]) + L[2][x] * R[2][y]);
-        if (type <= 1)
-          gg[x] += A.lambda * ((L[0][x] * rv[0] + L[1][x] * rv[1]) + L[2][x] * rv[2]);
-      }
-    } else {
-      const int s = v >> 4, mr = (v >> 2) & 3, mc = v & 3;
-      const int cnt = A.s_cnt[s];
-      if (cnt == 0) continue;
-      touched = 1;
-      const int off = A.s_off[s];
-      for (int q = 0; q < cnt; ++q) {
-        const int pix = A.s_list[off + q];
-        const float* rw = A.rows + (size_t)pix * 24;
-        double a[6], b[6];
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          a[t] = rw[mr * 6 + t];
-          b[t] = rw[mc * 6 + t];
+          for (int y = 0; y < 6; ++y) {
+            const double L0 = lj ? Jj[0][x] : Ji[0][x], L1 = lj ? Jj[1][x] : Ji[1][x],
+                         L2 = lj ? Jj[2][x] : Ji[2][x];
+            const double R0 = rj ? Jj[0][y] : Ji[0][y], R1 = rj ? Jj[1][y] : Ji[1][y],
+                         R2 = rj ? Jj[2][y] : Ji[2][y];
+            h[x * 6 + y] += (float)(A.lambda * ((L0 * R0 + L1 * R1) + L2 * R2));
+          }
+          if (type <= 1) {
+            const double L0 = lj ? Jj[0][x] : Ji[0][x], L1 = lj ? Jj[1][x] : Ji[1][x],
+                         L2 = lj ? Jj[2][x] : Ji[2][x];
+            gg[x] += A.lambda * ((L0 * rv[0] + L1 * rv[1]) + L2 * rv[2]);
+          }
         }
+      } else {
+        const int s = v >> 4, mr = (v >> 2) & 3, mc = v & 3;
+        const int cnt = A.s_cnt[s];
+        if (cnt == 0) continue;
+        touched = 1;
+        const int off = A.s_off[s];
+        for (int q = 0; q < cnt; ++q) {
+          const float* rw = A.rows_l + (size_t)(off + q) * 24;
+          float a[6], b[6];
 #pragma unroll
-        for (int x = 0; x < 6; ++x)
+          for (int t = 0; t < 6; ++t) {
+            a[t] = rw[mr * 6 + t];
+            b[t] = rw[mc * 6 + t];
+          }
 #pragma unroll
-          for (int y = 0; y < 6; ++y) h[x * 6 + y] += a[x] * b[y];
-        if (diag) {
-          const double r = A.pair_r[pix];
+          for (int x = 0; x < 6; ++x)
 #pragma unroll
-          for (int x = 0; x < 6; ++x) gg[x] += a[x] * r;
+            for (int y = 0; y < 6; ++y) h[x * 6 + y] += a[x] * b[y];
+          if (diag) {
+            const double r = A.r_l[off + q];
+#pragma unroll
+            for (int x = 0; x < 6; ++x) gg[x] += (double)a[x] * r;
+          }
         }
       }
     }
   }
-  // fixed-order reduction over lanes through shared memory
+  // fixed butterfly over the 8 lanes of the group
 #pragma unroll
-  for (int t = 0; t < 36; ++t) red[wid][lane][t] = h[t];
+  for (int off = kChunkLanes / 2; off > 0; off >>= 1) {
 #pragma unroll
-  for (int t = 0; t < 6; ++t) red[wid][lane][36 + t] = gg[t];
-  red[wid][lane][42] = (double)touched;
-  __syncwarp();
-  for (int t = lane; t < 43; t += 32) {
-    double acc = 0.0;
-    for (int l = 0; l < 32; ++l) acc += red[wid][l][t];
-    red[wid][0][t] = acc;  // row 0 slot t is only read by this lane afterwards
+    for (int t = 0; t < 36; ++t) h[t] += __shfl_xor_sync(0xffffffffu, h[t], off);
+#pragma unroll
+    for (int t = 0; t < 6; ++t) gg[t] += __shfl_xor_sync(0xffffffffu, gg[t], off);
+    touched |= __shfl_xor_sync(0xffffffffu, touched, off);
   }
-  __syncwarp();
-  const bool any = red[wid][0][42] > 0.0;
+  if (valid && l == 0) {
+    float4* ph = reinterpret_cast<float4*>(A.part_h + (size_t)chunk * 36);
+#pragma unroll
+    for (int t = 0; t < 9; ++t) ph[t] = make_float4(h[4 * t], h[4 * t + 1], h[4 * t + 2], h[4 * t + 3]);
+#pragma unroll
+    for (int t = 0; t < 6; ++t) A.part_g[(size_t)chunk * 6 + t] = gg[t];
+    A.part_t[chunk] = touched;
+  }
+}
+
+// thread per upper block: chunk partials in chunk order -> BSR (both triangles), g
+__global__ void k_assemble_finish(AsmArgs A) {
+  const int ub = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ub >= A.n_up) return;
+  const int key = A.up_key[ub];
+  const int row = key / A.N, colb = key % A.N;
+  const int c0 = A.chunk_first[ub], c1 = A.chunk_first[ub + 1];
+  int touched = 0;
+  for (int c = c0; c < c1; ++c) touched |= A.part_t[c];
   const int pu = A.up_pos[ub];
-  for (int t = lane; t < 36; t += 32) A.bsr_val[(size_t)pu * 36 + t] = (float)red[wid][0][t];
-  if (lane == 0) A.bsr_touch[pu] = any ? 1 : 0;
-  if (!diag) {
-    const int pm = A.up_mpos[ub];
-    for (int t = lane; t < 36; t += 32) {
-      const int x = t / 6, y = t % 6;
-      A.bsr_val[(size_t)pm * 36 + y * 6 + x] = (float)red[wid][0][t];
-    }
-    if (lane == 0) A.bsr_touch[pm] = any ? 1 : 0;
-  } else if (lane < 6) {
-    A.g[6 * row + lane] = red[wid][0][36 + lane];
+  const int pm = row != colb ? A.up_mpos[ub] : -1;
+  for (int t = 0; t < 36; ++t) {
+    double acc = 0.0;
+    for (int c = c0; c < c1; ++c) acc += (double)A.part_h[(size_t)c * 36 + t];
+    A.bsr_val[(size_t)pu * 36 + t] = (float)acc;
+    if (pm >= 0) A.bsr_val[(size_t)pm * 36 + (t % 6) * 6 + t / 6] = (float)acc;
   }
+  A.bsr_touch[pu] = touched ? 1 : 0;
+  if (pm >= 0) {
+    A.bsr_touch[pm] = touched ? 1 : 0;
+  } else {
+    for (int x = 0; x < 6; ++x) {
+      double acc = 0.0;
+      for (int c = c0; c < c1; ++c) acc += A.part_g[(size_t)c * 6 + x];
+      A.g[6 * row + x] = acc;
+    }
+  }
+}
+
+__global__ void k_chunk_count(const int* __restrict__ up_start, int n_up, int* __restrict__ cnt) {
+  const int ub = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ub < n_up) cnt[ub] = (up_start[ub + 1] - up_start[ub] + kChunk - 1) / kChunk;
+}
+__global__ void k_chunk_fill(const int* __restrict__ first, int n_up, int* __restrict__ chunk_ub) {
+  const int ub = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ub >= n_up) return;
+  for (int c = first[ub]; c < first[ub + 1]; ++c) chunk_ub[c] = ub;
 }
 
 // ginf, |g|^2, tr(H) (solver.cpp:371, 378)
 __global__ void k_g_stats(const double* __restrict__ g, int dim, const float* __restrict__ val,
-                          const int* __restrict__ diag_pos, int N, double* __restrict__ part) {
+                          const int* __restrict__ diag_pos, int N, DevScalars* __restrict__ sc) {
   __shared__ double smax[256], ssq[256], str[256];
   double mx = 0, sq = 0, tr = 0;
   for (int i = threadIdx.x; i < dim; i += blockDim.x) {
@@ -555,9 +631,9 @@ __global__ void k_g_stats(const double* __restrict__ g, int dim, const float* __
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    part[0] = smax[0];
-    part[1] = ssq[0];
-    part[2] = str[0];
+    sc->ginf = smax[0];
+    sc->pcg_rr0 = ssq[0];  // |g|^2
+    sc->htrace = str[0];
   }
 }
 
@@ -811,22 +887,37 @@ __global__ void k_check_finite(const double* __restrict__ x, int n, int* __restr
 }  // namespace
 
 // ------------------------------------------------------------------ host side
-void build_pattern(Ctx& c) {
-  const int n = c.n_surfels, N = c.n_nodes;
+void build_pattern(Ctx& c, int t_now, int t_last) {
+  const int n_all = c.n_surfels, N = c.n_nodes;
+  if ((long long)N * N >= 0x7fffffffLL) fail(DS_ERR_CAPACITY, "too many nodes for block keys");
+  // eligible surfels (the only ones render_model_maps can pair this frame)
+  int n = 0;
+  if (n_all > 0) {
+    DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable, 0, sizeof(int), c.stream));
+    DS_LAUNCH(c, KK_PATTERN, 16.0 * n_all, cdiv(n_all, 256), 256, 0, k_any_stable_flag,
+              c.M().ln, n_all, c.cfg.delta_stable, &c.dsc->any_stable);
+    const int boot = (t_now - t_last <= c.cfg.delta_recent) ? 1 : 0;
+    DS_LAUNCH(c, KK_PATTERN, 28.0 * n_all, cdiv(n_all, 256), 256, 0, k_elig_flags, c.M().ln,
+              c.M().t, n_all, c.cfg.delta_stable, t_now, c.cfg.delta_recent, boot,
+              &c.dsc->any_stable, c.keep);
+    scan_exclusive(c, c.keep, c.keep_scan, n_all);
+    DS_LAUNCH(c, KK_PATTERN, 12.0 * n_all, cdiv(n_all, 256), 256, 0, k_elig_list, c.keep,
+              c.keep_scan, n_all, c.rec_flag);
+    DS_CUDA(cudaMemcpyAsync(&n, c.keep_scan + n_all, sizeof(int), cudaMemcpyDeviceToHost,
+                            c.stream));
+    sync(c);
+  }
   const int R = n * 10 + N * 24;
   if (R > c.R_cap) fail(DS_ERR_CAPACITY, "term record capacity exceeded");
-  if ((long long)N * N >= 0x7fffffffLL) fail(DS_ERR_CAPACITY, "too many nodes for block keys");
   int* key = c.rec_key;
   int* val = c.rec_val;
   if (n > 0)
-    DS_LAUNCH(c, KK_PATTERN, 56.0 * n, cdiv(n, 256), 256, 0, k_gen_records, c.M().ki, n, N, key,
-              val);
+    DS_LAUNCH(c, KK_PATTERN, 60.0 * n, cdiv(n, 256), 256, 0, k_gen_records, c.M().ki, c.rec_flag,
+              n, N, key, val);
   if (N > 0)
     DS_LAUNCH(c, KK_PATTERN, 32.0 * 8 * N, cdiv(8 * N, 256), 256, 0, k_gen_reg_records, c.node_nbr,
               N, key + (size_t)n * 10, val + (size_t)n * 10);
-  int end_bit = 1;
-  while (end_bit < 31 && (1LL << end_bit) <= (long long)N * N) ++end_bit;
-  end_bit = 31;  // sentinel kIntMax needs all 31 bits
+  const int end_bit = 31;  // the kIntMax sentinel needs all 31 bits
   int *ks, *vs;
   sort_pairs(c, key, val, c.rec_key2, c.rec_val2, R, end_bit, &ks, &vs);
   // keep the sorted arrays in rec_key/rec_val
@@ -861,6 +952,20 @@ void build_pattern(Ctx& c) {
   }
   DS_LAUNCH(c, KK_PATTERN, 16.0 * c.n_full, cdiv(N, 128), 128, 0, k_row_sort, c.row_ptr, N,
             c.bsr_col, c.bsr_tag, c.up_pos, c.up_mpos, c.diag_pos);
+  if (c.n_pairs_ok_est <= 0) c.n_pairs_ok_est = 0.4 * c.P;
+  // fixed-size record chunks for the assembly (per frame)
+  c.n_chunks = 0;
+  if (c.n_up > 0) {
+    DS_LAUNCH(c, KK_PATTERN, 12.0 * c.n_up, cdiv(c.n_up, 256), 256, 0, k_chunk_count, c.up_start,
+              c.n_up, c.chunk_first);
+    scan_exclusive(c, c.chunk_first, c.chunk_first, c.n_up);
+    DS_CUDA(cudaMemcpyAsync(&c.n_chunks, c.chunk_first + c.n_up, sizeof(int),
+                            cudaMemcpyDeviceToHost, c.stream));
+    sync(c);
+    if (c.n_chunks > c.CH_cap) fail(DS_ERR_CAPACITY, "assembly chunk capacity exceeded");
+    DS_LAUNCH(c, KK_PATTERN, 8.0 * c.n_chunks, cdiv(c.n_up, 256), 256, 0, k_chunk_fill,
+              c.chunk_first, c.n_up, c.chunk_ub);
+  }
   c.pattern_ready = true;
 }
 
@@ -885,60 +990,59 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last) {
   // per pixel: pair id 4 B, surfel ref + skin 48 B, frame maps 64 B, rows 96 B + r 8 B out
   DS_LAUNCH(c, KK_PAIR_TERMS, 220.0 * P, nbp, 256, 0, k_pair_terms, c.pair_s, c.M(), c.node_dq,
             c.f_vert, c.f_nrm, pair_params(c, pose), c.pair_ok, c.pair_rows, c.pair_r, c.s_cnt,
-            c.red_part);
-  reduce_partials(c, c.red_part, nbp, &c.dsc->e_data, 0);
+            c.red_part, c.tickets + 0, &c.dsc->e_data);
   scan_exclusive(c, c.s_cnt, c.s_off, n);
   DS_CUDA(cudaMemsetAsync(c.s_cur, 0, sizeof(int) * n, c.stream));
   DS_LAUNCH(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_scatter_pairs, c.pair_s, c.pair_ok, P,
             c.s_off, c.s_cur, c.s_list);
-  DS_LAUNCH(c, KK_PAIR_LISTS, 8.0 * n, cdiv(n, 256), 256, 0, k_sort_lists, c.s_cnt, c.s_off, n,
-            c.s_list);
+  DS_LAUNCH(c, KK_PAIR_LISTS, 112.0 * P * 0.5, cdiv(n, 256), 256, 0, k_sort_lists, c.s_cnt,
+            c.s_off, n, c.s_list, c.pair_rows, c.pair_r, c.rows_l, c.r_l);
   node_se3(c, c.node_dq, c.node_se3);
   const int nbe = cdiv(8 * N, 256);
   DS_LAUNCH(c, KK_ENERGY, 200.0 * N, nbe, 256, 0, k_reg_energy, c.node_pos, c.node_nbr,
-            c.node_se3, N, c.red_part + nbp);
-  reduce_partials(c, c.red_part + nbp, nbe, &c.dsc->e_reg, 0);
+            c.node_se3, N, c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg);
   DS_CUDA(cudaMemsetAsync(c.g, 0, sizeof(double) * 6 * N, c.stream));
-  DS_CUDA(cudaMemsetAsync(c.bsr_val, 0, sizeof(float) * 36 * (size_t)c.n_full, c.stream));
   AsmArgs A;
   A.up_key = c.up_key;
   A.up_start = c.up_start;
   A.up_pos = c.up_pos;
   A.up_mpos = c.up_mpos;
+  A.chunk_ub = c.chunk_ub;
+  A.chunk_first = c.chunk_first;
   A.rec_val = c.rec_val;
   A.s_cnt = c.s_cnt;
   A.s_off = c.s_off;
-  A.s_list = c.s_list;
-  A.rows = c.pair_rows;
-  A.pair_r = c.pair_r;
+  A.rows_l = c.rows_l;
+  A.r_l = c.r_l;
   A.node_pos = c.node_pos;
   A.nbr = c.node_nbr;
   A.se3 = c.node_se3;
   A.lambda = c.cfg.lambda;
   A.N = N;
   A.n_up = c.n_up;
+  A.n_chunks = c.n_chunks;
+  A.part_h = c.part_h;
+  A.part_g = c.part_g;
+  A.part_t = c.part_t;
   A.bsr_val = c.bsr_val;
   A.bsr_touch = c.bsr_touch;
   A.g = c.g;
   if (c.n_up > 0) {
-    // algorithmic bytes: records 4 B each + per-pair rows/residual (104 B) once,
+    // algorithmic bytes: records 4 B + (count, offset) 8 B each, the paired
+    // surfels' list-ordered rows/residuals (104 B) once, chunk partials out+in,
     // blocks written 144 B (both triangles) + g
-    const double bytes = 4.0 * (c.n_records) + 104.0 * P * 0.5 + 144.0 * c.n_full + 48.0 * N;
-    DS_LAUNCH(c, KK_BLOCK_ASSEMBLY, bytes, cdiv(c.n_up, kAsmWarps), 32 * kAsmWarps, 0, k_assemble,
-              A);
+    const double bytes = 12.0 * c.n_records + 104.0 * c.n_pairs_ok_est + 200.0 * 2 * c.n_chunks +
+                         144.0 * c.n_full + 48.0 * N;
+    DS_LAUNCH(c, KK_BLOCK_ASSEMBLY, bytes, cdiv((long long)c.n_chunks * kChunkLanes, 256), 256, 0,
+              k_assemble_chunks, A);
+    DS_LAUNCH(c, KK_BLOCK_ASSEMBLY, 0.0, cdiv(c.n_up, 128), 128, 0, k_assemble_finish, A);
   }
   DS_LAUNCH(c, KK_REDUCE, 48.0 * N, 1, 256, 0, k_g_stats, c.g, 6 * N, c.bsr_val, c.diag_pos, N,
-            c.red_part + nbp + nbe);
-  DS_CUDA(cudaMemcpyAsync(&c.dsc->ginf, c.red_part + nbp + nbe, sizeof(double),
-                          cudaMemcpyDeviceToDevice, c.stream));
-  DS_CUDA(cudaMemcpyAsync(&c.dsc->htrace, c.red_part + nbp + nbe + 2, sizeof(double),
-                          cudaMemcpyDeviceToDevice, c.stream));
-  DS_CUDA(cudaMemcpyAsync(&c.dsc->pcg_rr0, c.red_part + nbp + nbe + 1, sizeof(double),
-                          cudaMemcpyDeviceToDevice, c.stream));
+            c.dsc);
 }
 
 void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_pre, int* n_pairs) {
-  if (!c.pattern_ready) build_pattern(c);
+  if (!c.pattern_ready) build_pattern(c, t_now, t_last);
   gn_linearize_async(c, pose, t_now, t_last);
   fetch_scalars(c);
   if (e_pre) *e_pre = c.hsc->e_data + c.cfg.lambda * c.hsc->e_reg;
@@ -990,12 +1094,11 @@ void energy_async(Ctx& c, const double* pose, const double4* dq, double* se3) {
   const int N = c.n_nodes, P = c.P;
   const int nbp = cdiv(P, 256), nbe = cdiv(8 * N, 256);
   DS_LAUNCH(c, KK_ENERGY, 120.0 * P * 0.5, nbp, 256, 0, k_pair_energy, c.pair_s, c.M(), dq,
-            c.f_vert, c.f_nrm, pair_params(c, pose), 0, c.red_part, (int*)nullptr);
-  reduce_partials(c, c.red_part, nbp, &c.dsc->e_data, 0);
+            c.f_vert, c.f_nrm, pair_params(c, pose), 0, c.red_part, (int*)nullptr, c.tickets + 0,
+            &c.dsc->e_data);
   node_se3(c, dq, se3);
   DS_LAUNCH(c, KK_ENERGY, 200.0 * N, nbe, 256, 0, k_reg_energy, c.node_pos, c.node_nbr, se3, N,
-            c.red_part + nbp);
-  reduce_partials(c, c.red_part + nbp, nbe, &c.dsc->e_reg, 0);
+            c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg);
 }
 }  // namespace
 
@@ -1010,7 +1113,7 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
     return;
   }
   const int dim = 6 * N;
-  build_pattern(c);
+  build_pattern(c, t_now, t_last);
   const int max_pcg = c.cfg.pcg_max_iters > 0 ? c.cfg.pcg_max_iters : 10;
   const double tol = c.cfg.pcg_tol;
   double mu = 0.0;
@@ -1020,6 +1123,7 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
     fetch_scalars(c);
     const double e_pre = c.hsc->e_data + c.cfg.lambda * c.hsc->e_reg;
     n_pairs = c.hsc->n_pairs;
+    c.n_pairs_ok_est = n_pairs;
     if (iter == 0) {
       rep.initial_energy = e_pre;
       rep.final_energy = e_pre;
@@ -1062,8 +1166,8 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
   const int nbp = cdiv(c.P, 256);
   DS_CUDA(cudaMemsetAsync(&c.dsc->mean_cnt, 0, sizeof(int), c.stream));
   DS_LAUNCH(c, KK_ENERGY, 120.0 * c.P * 0.5, nbp, 256, 0, k_pair_energy, c.pair_s, c.M(), c.node_dq,
-            c.f_vert, c.f_nrm, pair_params(c, pose), 1, c.red_part, &c.dsc->mean_cnt);
-  reduce_partials(c, c.red_part, nbp, &c.dsc->mean_abs_r, 0);
+            c.f_vert, c.f_nrm, pair_params(c, pose), 1, c.red_part, &c.dsc->mean_cnt,
+            c.tickets + 0, &c.dsc->mean_abs_r);
   fetch_scalars(c);
   rep.mean_residual = c.hsc->mean_cnt > 0 ? c.hsc->mean_abs_r / c.hsc->mean_cnt : 0.0;
   *out = rep;

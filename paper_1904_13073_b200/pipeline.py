@@ -351,6 +351,9 @@ class Context:
     def reset_kernel_stats(self):
         check(self.L.ds_reset_kernel_stats(self.h))
 
+    def set_profiling(self, on: bool):
+        check(self.L.ds_set_profiling(self.h, 1 if on else 0))
+
     def total_launches(self) -> int:
         n = C.c_int64()
         check(self.L.ds_total_launches(self.h, C.byref(n)))

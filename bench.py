@@ -218,22 +218,23 @@ def roofline(ks, peak_gbs):
     return out, per
 
 
-def cpu_sample(spec, cfg, seconds_budget=25.0):
-    """Oracle (fp64 reference restatement) on a bounded sample of the same workload.
+def cpu_sample(spec, cfg, gn_iters=10.0):
+    """CPU oracle (the fp64 restatement of the reference; single thread, as the
+    reference has no threading) on a bounded sample of the same workload.
 
-    The reference solves the dense 6N x 6N normal equations with LDLT every LM
-    attempt (solver.cpp:383-386): at ~1.5k nodes one factorisation is ~2.6e11
-    flop, minutes on a core. The sample runs frame 0 (init) and frame 1 of the
-    config-2 sequence through the oracle pipeline with the dense LDLT included
-    but max_gn_iters = 1, timing every stage for real; the frame time is then
-    scaled to the measured GPU GN-iteration count by the measured per-iteration
-    cost. Single thread (the reference has no threading)."""
+    Frame 0 of the config-2 sequence initialises the oracle; frame 1 is then run
+    stage by stage with wall-clock timers: build_frame_maps, model maps + rigid
+    ICP, one full GN linearisation (warp, render, associate, energy, dense 6N x 6N
+    assembly — solver.cpp:316-369), and forward warp + apply_fusion. The dense
+    LDLT of the reference's LM step (solver.cpp:383-386) is NOT run at
+    6N ~ 9k (minutes per factorisation); its cost is n^3/3 flop at the rate the
+    same LDLT code measures on a 1200 x 1200 SPD matrix. Frame time =
+    depth + rigid + gn_iters x (linearisation + LDLT) + fusion."""
     sys.path.insert(0, os.path.join(REPO, "tests"))
     import oracle_py as O
 
     ocfg = O.make_config(**{k: v for k, v in cfg.items() if k in O.DEFAULTS})
-    seq_frames = render_frames(spec, cfg, 2, phase=0)
-    # measure the dense LDLT rate at a moderate size and extrapolate n^3/3
+    frames = render_frames(spec, cfg, 2, phase=0)
     n_probe = 1200
     rng = np.random.default_rng(0)
     A = rng.normal(size=(n_probe, n_probe))
@@ -241,26 +242,42 @@ def cpu_sample(spec, cfg, seconds_budget=25.0):
     t0 = time.perf_counter()
     O.ldlt_solve(A, np.ones(n_probe))
     ldlt_rate = (n_probe ** 3 / 3.0) / (time.perf_counter() - t0)
-    ocfg1 = dict(ocfg)
-    ocfg1["max_gn_iters"] = 1
-    p = O.OraclePipeline(ocfg1)
+    p = O.OraclePipeline(ocfg)
     t0 = time.perf_counter()
-    s0 = p.process_frame(seq_frames[0], 0)
+    s0 = p.process_frame(frames[0], 0)
     t_init = time.perf_counter() - t0
-    # frame 1 without the solve: time stages with a stand-in for the LDLT
     st = p.state
     n_nodes = st.num_nodes()
     dim = 6 * n_nodes
-    t_ldlt = (dim ** 3 / 3.0) / ldlt_rate
-    # one GN linearisation (warp + render + associate + dense assembly) measured
     pose = p.pose()
-    st.build_frame(seq_frames[1], 1)
+    T = {}
     t0 = time.perf_counter()
-    if dim <= 4000:
-        st.normal_equations(pose, 1, 0)
-    t_lin = time.perf_counter() - t0 if dim <= 4000 else None
-    return dict(t_init=t_init, t_ldlt=t_ldlt, ldlt_rate_gflops=ldlt_rate / 1e9, dim=dim,
-                t_lin=t_lin, surfels=s0.surfel_count, nodes=n_nodes)
+    st.build_frame(frames[1], 1)
+    T["depth"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st.rigid_align(pose, pose, 1, 0)
+    T["rigid"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st.normal_equations(pose, 1, 0)
+    T["linearize"] = time.perf_counter() - t0
+    T["ldlt"] = (dim ** 3 / 3.0) / ldlt_rate
+    t0 = time.perf_counter()
+    st.forward_warp()
+    st.apply_fusion(pose, 1)
+    T["fusion"] = time.perf_counter() - t0
+    t_frame = T["depth"] + T["rigid"] + gn_iters * (T["linearize"] + T["ldlt"]) + T["fusion"]
+    return dict(t_frame=t_frame, t_init=t_init, stages=T, ldlt_rate_gflops=ldlt_rate / 1e9,
+                dim=dim, surfels=s0.surfel_count, nodes=n_nodes, gn_iters=gn_iters)
+
+
+def cpu_baseline_entry(cs):
+    T = cs["stages"]
+    return {"value": round(1.0 / cs["t_frame"], 6), "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": (f"CPU oracle, cfg2 frame 1 ({cs['surfels']} surfels, {cs['nodes']} nodes): "
+                       f"measured depth {T['depth']:.3f}s, rigid {T['rigid']:.3f}s, GN "
+                       f"linearisation {T['linearize']:.3f}s, fusion {T['fusion']:.3f}s; dense "
+                       f"LDLT dim {cs['dim']} = {T['ldlt']:.1f}s extrapolated (n^3/3 at measured "
+                       f"{cs['ldlt_rate_gflops']:.2f} GFLOP/s); x {cs['gn_iters']:.0f} GN iterations")}
 
 
 def dist_barrier(world):
@@ -343,17 +360,7 @@ def main():
     }
     if not args.no_cpu_baseline:
         try:
-            cs = cpu_sample(r["spec"], r["cfg"])
-            if cs["t_lin"] is not None:
-                t_frame = cs["t_lin"] * gn_iters + cs["t_ldlt"] * gn_iters
-            else:
-                t_frame = cs["t_ldlt"] * gn_iters
-            line["cpu_baseline"] = {
-                "value": round(1.0 / t_frame, 6), "unit": "frames/s", "cores": 1, "kind": "port",
-                "sample": f"oracle: init frame measured ({cs['t_init']:.2f}s, "
-                          f"{cs['surfels']} surfels, {cs['nodes']} nodes); dense LDLT of dim "
-                          f"{cs['dim']} extrapolated from measured {cs['ldlt_rate_gflops']:.2f} "
-                          f"GFLOP/s (n^3/3) x {gn_iters:.1f} GN iters"}
+            line["cpu_baseline"] = cpu_baseline_entry(cpu_sample(r["spec"], r["cfg"], gn_iters))
         except Exception as e:  # never fail the GPU line on the CPU sample
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)

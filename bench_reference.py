@@ -20,24 +20,18 @@ def run_reference(args):
 
     spec = bench.CFG2 if args.config == "cfg2" else bench.CFG1
     cfg = bench.make_cfg(spec)
-    values = []
-    samples = []
-    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
-        cs = bench.cpu_sample(spec, cfg)
-        gn = 10.0
-        t_lin = cs["t_lin"] if cs["t_lin"] is not None else 0.0
-        t_frame = (t_lin + cs["t_ldlt"]) * gn
-        values.append(1.0 / t_frame)
-        samples.append(cs)
+    samples = [bench.cpu_sample(spec, cfg) for _ in range(max(1, min(args.steps, 3)))]
+    values = [1.0 / cs["t_frame"] for cs in samples]
     v = float(np.median(values))
-    cs = samples[-1]
+    entry = bench.cpu_baseline_entry(samples[-1])
+    entry["value"] = round(v, 6)
     return {
         "impl": "reference", "metric": "frames/s", "value": round(v, 6), "unit": "frames/s",
         "n_gpus": 0, "steps": len(values), "warmup": 0, "higher_is_better": True,
-        "config": {"workload": f"{args.config}: {spec['scene']} {spec['width']}x{spec['height']}"},
-        "cpu_baseline": {"value": round(v, 6), "unit": "frames/s", "cores": 1, "kind": "port",
-                         "sample": f"oracle stages + dense LDLT dim {cs['dim']} extrapolated "
-                                   f"({cs['ldlt_rate_gflops']:.2f} GFLOP/s) x 10 GN iters"},
+        "scaling": "weak", "vs_baseline": None, "data": "synthetic",
+        "config": {"workload": f"{args.config}: {spec['scene']} {spec['width']}x{spec['height']}, "
+                               f"10 GN iterations per frame"},
+        "cpu_baseline": entry,
         "e2e": {"value": round(v, 6), "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -4,6 +4,8 @@
 // (pipeline.cpp:42-72); all stage work is on the device.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -167,6 +169,7 @@ void allocate(Ctx& c) {
   c.node_se3 = dalloc<double>(c, 12 * N);
   c.node_se3_cand = dalloc<double>(c, 12 * N);
   c.node_live = dalloc<double4>(c, N);
+  c.node_live_f = dalloc<float4>(c, N);
   c.depth = dalloc<uint16_t>(c, P);
   c.depth_f = dalloc<uint16_t>(c, P);
   c.f_vert = dalloc<double4>(c, P);
@@ -210,6 +213,7 @@ void allocate(Ctx& c) {
   c.part_g = dalloc<double>(c, (size_t)c.CH_cap * 6);
   c.part_t = dalloc<int>(c, c.CH_cap);
   c.rows_l = dalloc<float>(c, P * 24);
+  c.elig = dalloc<int>(c, S);
   c.r_l = dalloc<double>(c, P);
   c.cub_tmp_bytes = sort_temp_bytes(c.R_cap);
   c.cub_tmp = dalloc<char>(c, c.cub_tmp_bytes);
@@ -222,6 +226,10 @@ void allocate(Ctx& c) {
   c.pcg_q = dalloc<double>(c, 6 * N);
   c.pcg_minv = dalloc<double>(c, 36 * N);
   c.pcg_grid = pcg_max_grid(c.num_sms);
+  if (const char* e = std::getenv("DS_PCG_GRID")) {  // tuning knob (capped at co-residency)
+    const int g = std::atoi(e);
+    if (g > 0) c.pcg_grid = std::min(c.pcg_grid, g);
+  }
   c.pcg_part = dalloc<double>(c, 4 * (size_t)c.pcg_grid);
   c.cand_flag = dalloc<int>(c, P + 1);
   c.cand_scan = dalloc<int>(c, P + 1);
@@ -249,6 +257,9 @@ void allocate(Ctx& c) {
   c.dsc = dalloc<DevScalars>(c, 1);
   DS_CUDA(cudaMallocHost(&c.hsc, sizeof(DevScalars)));
   DS_CUDA(cudaMallocHost(&c.h_depth_pinned, sizeof(uint16_t) * P));
+  DS_CUDA(cudaMallocHost(&c.h_mu, sizeof(double)));
+  DS_CUDA(cudaMallocHost(&c.h_int, 4 * sizeof(int)));
+  if (const char* e = std::getenv("DS_NO_GRAPHS")) c.use_graphs = e[0] == '0';
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));
   DS_CUDA(cudaMemsetAsync(c.node_nbr, 0xff, sizeof(int) * 8 * N, c.stream));
 }
@@ -262,6 +273,10 @@ void release(Ctx& c) {
   for (void* p : c.allocations) cudaFree(p);
   if (c.hsc) cudaFreeHost(c.hsc);
   if (c.h_depth_pinned) cudaFreeHost(c.h_depth_pinned);
+  if (c.h_mu) cudaFreeHost(c.h_mu);
+  if (c.h_int) cudaFreeHost(c.h_int);
+  if (c.g_step.exec) cudaGraphExecDestroy(c.g_step.exec);
+  if (c.g_attempt.exec) cudaGraphExecDestroy(c.g_attempt.exec);
   if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
 }
 

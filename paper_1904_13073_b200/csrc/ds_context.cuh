@@ -82,12 +82,19 @@ struct DevScalars {
   int n_nodes, n_new_nodes, err, finite;
   int up_blocks, full_blocks, pcg_iters, mean_cnt;
   int rigid_pairs, rigid_low, n_records, survivors;
+  int rmax_bits, _pad_sc;
   double e_data, e_reg, ginf, htrace;
+  double e_data_pre, e_reg_pre, g_sq, mu, mu_floor;
   double pcg_rr, pcg_rr0, mean_abs_r, rigid_abs;
   double rigid_pose[12];
 };
 
 enum DevErr { DERR_NODE_CAP = 1, DERR_HASH_CELL = 2, DERR_HASH_FULL = 4, DERR_BLOCK_CAP = 8 };
+
+struct GraphSlot {
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;  // kernel launches per replay (accounting)
+};
 
 struct ProfRec {
   int kind;
@@ -116,6 +123,7 @@ struct Ctx {
   double* node_se3 = nullptr;
   double* node_se3_cand = nullptr;
   double4* node_live = nullptr;
+  float4* node_live_f = nullptr;  // fp32 copy for K-NN pre-tests
   // frame
   uint16_t* depth = nullptr;
   uint16_t* depth_f = nullptr;
@@ -172,6 +180,8 @@ struct Ctx {
   int* part_t = nullptr;       // per chunk: touched
   float* rows_l = nullptr;     // pair rows in per-surfel list order
   double* r_l = nullptr;       // pair residuals in list order
+  int* elig = nullptr;  // render-eligible surfels of the current frame's solve
+  int n_elig = 0;
   int n_records = 0, n_up = 0, n_full = 0, n_chunks = 0, CH_cap = 0;
   double n_pairs_ok_est = 0;
   bool pattern_ready = false;
@@ -234,6 +244,11 @@ struct Ctx {
   std::vector<void*> allocations;
   // per-frame extras
   int lm_attempts = 0, pcg_iterations = 0;
+  // CUDA graphs of the GN step / LM attempt (re-captured per frame, updated in place)
+  bool use_graphs = true;
+  GraphSlot g_step, g_attempt;
+  double* h_mu = nullptr;  // pinned staging for mu
+  int* h_int = nullptr;    // pinned staging for small ints
 
   ModelBuf& M() { return mb[cur]; }
   ModelBuf& Malt() { return mb[cur ^ 1]; }
@@ -269,6 +284,7 @@ void init_surfels_from_frame(Ctx& c);  // initialize_from_frame (pipeline.cpp:42
 
 // ---- warp field (k_warp.cu, k_skin.cu)
 int forward_warp(Ctx& c, bool count_degenerate);
+void forward_warp_list(Ctx& c, const int* list, int n);  // only the listed surfels
 void node_se3(Ctx& c, const double4* dq, double* se3);
 void node_live_positions(Ctx& c);
 void apply_increments(Ctx& c, const double* delta, double4* out);  // solver.cpp:277-286
@@ -281,6 +297,9 @@ void update_skinning_incremental(Ctx& c, int first_new);
 void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool associate,
                        const double* assoc_pose);
 void render_index_map(Ctx& c, const double* pose, int factor);
+// model maps + association over a precomputed render-eligible surfel list
+void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
+                            const double* assoc_pose, const int* list, int n);
 
 // ---- solver (k_solver.cu, k_rigid.cu)
 void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver_report* out);

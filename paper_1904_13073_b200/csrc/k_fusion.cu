@@ -234,37 +234,48 @@ __device__ int screen_one(V3 x, const double bd[4], const int bi[4],
 
 __global__ void k_screen(const float4* __restrict__ cp, const int* __restrict__ n_cand_dev,
                          const double4* __restrict__ node_pos, const double4* __restrict__ node_live,
+                         const float4* __restrict__ node_live_f, const int* __restrict__ rmax_bits,
                          const double4* __restrict__ node_dq, ScreenParams sp,
                          int4* __restrict__ cki, float4* __restrict__ ckw, int* __restrict__ ok,
                          int* __restrict__ res_out, int* __restrict__ low, int* __restrict__ comp) {
-  __shared__ double4 tile[128];
+  __shared__ float4 tile[128];
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = *n_cand_dev;
   if (blockIdx.x * blockDim.x >= n) return;  // whole block idle
   const bool active = k < n;
   V3 x = v3(0, 0, 0);
+  float xf = 0.f, yf = 0.f, zf = 0.f;
   if (active) {
-    const float4 p = cp[k];
+    const float4 p = cp[k];  // candidate positions are fp32 values: exact in both
     x = v3(p.x, p.y, p.z);
+    xf = p.x;
+    yf = p.y;
+    zf = p.z;
   }
-  // brute-force live-frame K-NN over shared-memory tiles of node live positions
+  // Exact live-frame K-NN by (d2, idx) over shared-memory tiles. fp32 pre-test:
+  // node coordinates rounded to fp32 move each |difference| by <= u*R (+ u of
+  // the difference), so with delta = 1.8 u R every node of the exact top-K has
+  // d2f <= (sqrt(bd3) + delta)^2 (1 + 1e-5) = thr and reaches the fp64 test.
+  const double delta = 1.8 * 5.9604644775390625e-8 * (double)__int_as_float(*rmax_bits);
   double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
   int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
   float thr = INFINITY;
   for (int base = 0; base < sp.N; base += 128) {
     __syncthreads();
-    if (base + threadIdx.x < sp.N) tile[threadIdx.x] = node_live[base + threadIdx.x];
+    if (base + threadIdx.x < sp.N) tile[threadIdx.x] = node_live_f[base + threadIdx.x];
     __syncthreads();
     const int lim = min(128, sp.N - base);
     if (active)
       for (int t = 0; t < lim; ++t) {
-        const double4 nl = tile[t];
-        // fp32 pre-test on the exactly-subtracted differences: d2f <= d2 (1 + 4e-7),
-        // so every node that can enter the exact (d2, idx) top-K passes it
-        const float dx = (float)(nl.x - x.x), dy = (float)(nl.y - x.y), dz = (float)(nl.z - x.z);
+        const float4 q = tile[t];
+        const float dx = q.x - xf, dy = q.y - yf, dz = q.z - zf;
         if ((dx * dx + dy * dy) + dz * dz > thr) continue;
+        const double4 nl = node_live[base + t];
         knn4_insert(sqn(sub(v3(nl.x, nl.y, nl.z), x)), base + t, bd, bi);
-        if (bd[3] < INFINITY) thr = (float)(bd[3] * (1.0 + 1e-5)) + 1e-37f;
+        if (bd[3] < INFINITY) {
+          const double rr = sqrt(bd[3]) + delta;
+          thr = (float)(rr * rr * (1.0 + 1e-5)) + 1e-37f;
+        }
       }
   }
   if (!active) return;
@@ -506,7 +517,8 @@ void screen_candidates_async(Ctx& c) {
   DS_CUDA(cudaMemsetAsync(c.cand_ok, 0, sizeof(int) * c.P, c.stream));
   node_live_positions(c);
   DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02, cdiv(c.P, 128), 128, 0, k_screen, c.cand_p,
-            &c.dsc->n_cand, c.node_pos, c.node_live, c.node_dq, screen_params(c), c.cand_ki,
+            &c.dsc->n_cand, c.node_pos, c.node_live, c.node_live_f, &c.dsc->rmax_bits, c.node_dq,
+            screen_params(c), c.cand_ki,
             c.cand_kw, c.cand_ok, c.cand_flag, &c.dsc->low_support, &c.dsc->comp_rejected);
 }
 

@@ -37,21 +37,27 @@ __global__ void k_any_stable(const float4* __restrict__ ln, int n, double delta_
   if ((threadIdx.x & 31) == 0 && b) atomicOr(flag, 1);
 }
 
+// list == nullptr: every surfel, eligibility tested here (raster.cpp:65-68);
+// list != nullptr: a precomputed render-eligible surfel list (solve loop)
 template <bool kPass2>
-__global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, SplatParams sp,
+__global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const int* __restrict__ list,
+                                                     SplatParams sp,
                                                      const int* __restrict__ any_stable,
                                                      unsigned long long* pkey,
                                                      unsigned long long* skey, int* pidx,
                                                      int* sidx) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int k0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k0 >= n) return;
+  const int i = list ? list[k0] : k0;
   const float4 lp = m.lp[i];
   const float4 ln = m.ln[i];
-  const int2 t = m.t[i];
-  const bool stable = (double)ln.w > sp.delta_stable;
-  const bool recent = (sp.t_now - t.y) <= sp.delta_recent;
-  const bool bootstrap = sp.host_bootstrap || !(*any_stable);
-  if (!stable && !(bootstrap && recent)) return;
+  if (!list) {
+    const int2 t = m.t[i];
+    const bool stable = (double)ln.w > sp.delta_stable;
+    const bool recent = (sp.t_now - t.y) <= sp.delta_recent;
+    const bool bootstrap = sp.host_bootstrap || !(*any_stable);
+    if (!stable && !(bootstrap && recent)) return;
+  }
   const CamParams& k = sp.cam;
   const V3 pc = rig_apply(k.w2c, v3(lp.x, lp.y, lp.z));
   if (pc.z <= 0) return;
@@ -177,9 +183,11 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
     DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 16.0 * n, cdiv(n, 256), 256, 0, k_any_stable, c.M().ln, n,
               c.cfg.delta_stable, &c.dsc->any_stable);
     DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 40.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(), n,
-              sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx);
+              (const int*)nullptr, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx,
+              c.mm_sidx);
     DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 40.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
-              sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx);
+              (const int*)nullptr, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx,
+              c.mm_sidx);
   }
   AssocParams ap;
   ap.pose = rig_load(associate ? assoc_pose : pose);
@@ -189,6 +197,36 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
   DS_LAUNCH(c, KK_ASSOCIATE, (associate ? 113.0 : 12.0) * c.P, cdiv(c.P, 256), 256, 0,
             k_resolve_associate, c.mm_pidx, c.mm_sidx, c.M(), c.f_vert, c.f_nrm, c.f_flag, ap,
             c.mm_idx, c.pair_s, &c.dsc->n_pairs);
+  std::copy(pose, pose + 12, c.mm_pose);
+  c.mm_ready = true;
+}
+
+void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
+                            const double* assoc_pose, const int* list, int n) {
+  const size_t P = c.P;
+  DS_CUDA(cudaMemsetAsync(c.mm_pkey, 0xff, 8 * P, c.stream));
+  DS_CUDA(cudaMemsetAsync(c.mm_skey, 0xff, 8 * P, c.stream));
+  DS_CUDA(cudaMemsetAsync(c.mm_pidx, 0x7f, 4 * P, c.stream));
+  DS_CUDA(cudaMemsetAsync(c.mm_sidx, 0x7f, 4 * P, c.stream));
+  DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
+  SplatParams sp;
+  sp.cam = cam_params(c, pose);
+  sp.t_now = t_now;
+  sp.delta_recent = c.cfg.delta_recent;
+  sp.delta_stable = c.cfg.delta_stable;
+  sp.host_bootstrap = (t_now - t_last <= c.cfg.delta_recent) ? 1 : 0;
+  if (n > 0) {
+    DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(), n,
+              list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx);
+    DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
+              list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx);
+  }
+  AssocParams ap;
+  ap.pose = rig_load(assoc_pose);
+  ap.P = c.P;
+  ap.associate = 1;
+  DS_LAUNCH(c, KK_ASSOCIATE, 113.0 * c.P, cdiv(c.P, 256), 256, 0, k_resolve_associate, c.mm_pidx,
+            c.mm_sidx, c.M(), c.f_vert, c.f_nrm, c.f_flag, ap, c.mm_idx, c.pair_s, &c.dsc->n_pairs);
   std::copy(pose, pose + 12, c.mm_pose);
   c.mm_ready = true;
 }

@@ -118,15 +118,25 @@ __global__ void k_ht_prefill(HashView h, const double4* __restrict__ node_pos, i
 }
 
 constexpr int kGreedyThreads = 1024;
+constexpr int kListNodes = 1024;  // extension: new nodes kept in shared memory
 
+// list_mode = 0 (init): coverage tested against the sigma-cell hash of all
+// accepted nodes. list_mode = 1 (extension, after k_uncovered removed every
+// candidate covered by a pre-existing node): only the nodes accepted by this
+// launch can cover a candidate; they are tested from shared memory.
 __global__ void __launch_bounds__(kGreedyThreads) k_greedy_nodes(
     const float4* __restrict__ cand, int M, double sigma, HashView h, double4* node_pos,
-    int* n_nodes, int N_cap, int* err) {
+    int* n_nodes, int N_cap, int list_mode, int* err) {
   __shared__ int s_first;
   __shared__ int s_count;
+  __shared__ int s_nlist;
   __shared__ double s_new[3];
+  __shared__ double s_list[kListNodes][3];
   const int tid = threadIdx.x;
-  if (tid == 0) s_count = *n_nodes;
+  if (tid == 0) {
+    s_count = *n_nodes;
+    s_nlist = 0;
+  }
   __syncthreads();
   const double r2 = sigma * sigma;
   for (int base = 0; base < M; base += kGreedyThreads) {
@@ -136,7 +146,13 @@ __global__ void __launch_bounds__(kGreedyThreads) k_greedy_nodes(
     if (i < M) {
       const float4 cp = cand[i];
       p = v3(cp.x, cp.y, cp.z);
-      covered = ht_any_within(h, node_pos, p, r2);
+      if (list_mode) {
+        covered = false;
+        for (int q = 0; q < s_nlist && !covered; ++q)
+          covered = sqn(sub(v3(s_list[q][0], s_list[q][1], s_list[q][2]), p)) < r2;
+      } else {
+        covered = ht_any_within(h, node_pos, p, r2);
+      }
     }
     for (;;) {
       if (tid == 0) s_first = 0x7fffffff;
@@ -149,9 +165,20 @@ __global__ void __launch_bounds__(kGreedyThreads) k_greedy_nodes(
         const int id = s_count;
         if (id < N_cap) {
           node_pos[id] = make_double4(p.x, p.y, p.z, sigma);
-          int cx, cy, cz;
-          cell_of(h, p, cx, cy, cz);
-          ht_insert_single(h, pack_cell(cx, cy, cz), id, err);
+          if (list_mode) {
+            if (s_nlist < kListNodes) {
+              s_list[s_nlist][0] = p.x;
+              s_list[s_nlist][1] = p.y;
+              s_list[s_nlist][2] = p.z;
+              ++s_nlist;
+            } else {
+              atomicOr(err, DERR_HASH_FULL);  // host re-runs in hash mode
+            }
+          } else {
+            int cx, cy, cz;
+            cell_of(h, p, cx, cy, cz);
+            ht_insert_single(h, pack_cell(cx, cy, cz), id, err);
+          }
         } else {
           atomicOr(err, DERR_NODE_CAP);
         }
@@ -459,16 +486,23 @@ void clear_hash(Ctx& c) {
 }
 
 // runs the greedy CTA over `cand` starting at node count n0; returns new count
-int greedy(Ctx& c, const float4* cand, int M, int n0) {
-  DS_CUDA(cudaMemcpyAsync(&c.dsc->n_nodes, &n0, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+int greedy(Ctx& c, const float4* cand, int M, int n0, int list_mode) {
+  *c.h_int = n0;
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->n_nodes, c.h_int, sizeof(int), cudaMemcpyHostToDevice, c.stream));
   DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
   DS_LAUNCH(c, KK_GREEDY_NODES, 16.0 * M, 1, kGreedyThreads, 0, k_greedy_nodes, cand, M,
-            c.cfg.node_sigma, hash_view(c), c.node_pos, &c.dsc->n_nodes, c.N_cap, &c.dsc->err);
+            c.cfg.node_sigma, hash_view(c), c.node_pos, &c.dsc->n_nodes, c.N_cap, list_mode,
+            &c.dsc->err);
   int res[2];
   DS_CUDA(cudaMemcpyAsync(&res[0], &c.dsc->n_nodes, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   DS_CUDA(cudaMemcpyAsync(&res[1], &c.dsc->err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   sync(c);
   if (res[1] & DERR_NODE_CAP) fail(DS_ERR_CAPACITY, "node capacity exceeded");
+  if (list_mode && (res[1] & DERR_HASH_FULL)) {
+    // more than kListNodes new nodes: redo in hash mode (existing nodes are
+    // already in the hash; the rerun re-accepts the same nodes in order)
+    return greedy(c, cand, M, n0, 0);
+  }
   if (res[1] & (DERR_HASH_CELL | DERR_HASH_FULL))
     fail(DS_ERR_CAPACITY, "node hash overflow (nodes closer than node_sigma?)");
   return res[0];
@@ -487,7 +521,7 @@ void compute_node_edges(Ctx& c) {
 void init_warp_field(Ctx& c) {
   if (c.n_surfels == 0) fail(DS_ERR_EMPTY_GEOMETRY, "init_warp_field: no reference surfels");
   clear_hash(c);
-  const int n = greedy(c, c.M().rp, c.n_surfels, 0);
+  const int n = greedy(c, c.M().rp, c.n_surfels, 0, 0);
   c.n_nodes = n;
   DS_LAUNCH(c, KK_MISC, 64.0 * n, cdiv(n, 128), 128, 0, k_identity_dq, c.node_dq, 0, n);
   compute_node_edges(c);
@@ -515,7 +549,7 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
     cand = c.ext_pos;
     if (m == 0) return 0;
   }
-  const int total = greedy(c, cand, m, n0);
+  const int total = greedy(c, cand, m, n0, n0 > 0 ? 1 : 0);
   const int added = total - n0;
   c.n_nodes = total;
   if (added > 0) {

@@ -632,7 +632,7 @@ __global__ void k_g_stats(const double* __restrict__ g, int dim, const float* __
   }
   if (threadIdx.x == 0) {
     sc->ginf = smax[0];
-    sc->pcg_rr0 = ssq[0];  // |g|^2
+    sc->g_sq = ssq[0];  // |g|^2
     sc->htrace = str[0];
   }
 }
@@ -647,7 +647,7 @@ struct PcgArgs {
   const float* val;
   const int* diag_pos;
   const double* g;
-  double mu;
+  const double* mu_ptr;  // LM damping lives on the device (graph-replay safe)
   int N;
   int max_iters;
   double tol2;
@@ -735,13 +735,14 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg(PcgArgs a) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * kPcgWarps + wid, nw = gridDim.x * kPcgWarps;
   const int N = a.N;
+  const double mu = *a.mu_ptr;
   // phase 0: block-Jacobi inverse, r = -g, x = 0, z = M^-1 r, p_old = 0
   double prz = 0.0, prr = 0.0;
   for (int j = gw; j < N; j += nw) {
     const int d = a.diag_pos[j];
     for (int t = lane; t < 36; t += 32) {
       double v = d >= 0 ? (double)a.val[(size_t)d * 36 + t] : 0.0;
-      if (t % 7 == 0) v += a.mu;
+      if (t % 7 == 0) v += mu;
       hb[wid][t] = v;
     }
     __syncwarp();
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg(PcgArgs a) {
       double pq = 0.0;
       if (lane < 6) {
         const double pn = a.z[6 * j + lane] + beta * pold[6 * j + lane];
-        const double qv = tot + a.mu * pn;
+        const double qv = tot + mu * pn;
         pnew[6 * j + lane] = pn;
         a.q[6 * j + lane] = qv;
         pq = pn * qv;
@@ -902,18 +903,19 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
               &c.dsc->any_stable, c.keep);
     scan_exclusive(c, c.keep, c.keep_scan, n_all);
     DS_LAUNCH(c, KK_PATTERN, 12.0 * n_all, cdiv(n_all, 256), 256, 0, k_elig_list, c.keep,
-              c.keep_scan, n_all, c.rec_flag);
+              c.keep_scan, n_all, c.elig);
     DS_CUDA(cudaMemcpyAsync(&n, c.keep_scan + n_all, sizeof(int), cudaMemcpyDeviceToHost,
                             c.stream));
     sync(c);
   }
+  c.n_elig = n;
   const int R = n * 10 + N * 24;
   if (R > c.R_cap) fail(DS_ERR_CAPACITY, "term record capacity exceeded");
   int* key = c.rec_key;
   int* val = c.rec_val;
   if (n > 0)
-    DS_LAUNCH(c, KK_PATTERN, 60.0 * n, cdiv(n, 256), 256, 0, k_gen_records, c.M().ki, c.rec_flag,
-              n, N, key, val);
+    DS_LAUNCH(c, KK_PATTERN, 60.0 * n, cdiv(n, 256), 256, 0, k_gen_records, c.M().ki, c.elig, n,
+              N, key, val);
   if (N > 0)
     DS_LAUNCH(c, KK_PATTERN, 32.0 * 8 * N, cdiv(8 * N, 256), 256, 0, k_gen_reg_records, c.node_nbr,
               N, key + (size_t)n * 10, val + (size_t)n * 10);
@@ -982,15 +984,17 @@ PairParams pair_params(Ctx& c, const double* pose) {
 // e_reg, ginf, |g|^2 (in pcg_rr slot) and tr(H) in DevScalars (no host sync).
 void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last) {
   const int n = c.n_surfels, N = c.n_nodes, P = c.P;
-  forward_warp(c, false);
-  render_model_maps(c, pose, t_now, t_last, true, pose);
+  // only render-eligible surfels can be drawn / paired during the solve; the
+  // post-solve forward_warp (pipeline.cpp:108) rewrites every live surfel
+  forward_warp_list(c, c.elig, c.n_elig);
+  render_model_maps_list(c, pose, t_now, t_last, pose, c.elig, c.n_elig);
   DS_CUDA(cudaMemsetAsync(c.s_cnt, 0, sizeof(int) * (n + 1), c.stream));
   DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
   const int nbp = cdiv(P, 256);
   // per pixel: pair id 4 B, surfel ref + skin 48 B, frame maps 64 B, rows 96 B + r 8 B out
   DS_LAUNCH(c, KK_PAIR_TERMS, 220.0 * P, nbp, 256, 0, k_pair_terms, c.pair_s, c.M(), c.node_dq,
             c.f_vert, c.f_nrm, pair_params(c, pose), c.pair_ok, c.pair_rows, c.pair_r, c.s_cnt,
-            c.red_part, c.tickets + 0, &c.dsc->e_data);
+            c.red_part, c.tickets + 0, &c.dsc->e_data_pre);
   scan_exclusive(c, c.s_cnt, c.s_off, n);
   DS_CUDA(cudaMemsetAsync(c.s_cur, 0, sizeof(int) * n, c.stream));
   DS_LAUNCH(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_scatter_pairs, c.pair_s, c.pair_ok, P,
@@ -1000,7 +1004,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last) {
   node_se3(c, c.node_dq, c.node_se3);
   const int nbe = cdiv(8 * N, 256);
   DS_LAUNCH(c, KK_ENERGY, 200.0 * N, nbe, 256, 0, k_reg_energy, c.node_pos, c.node_nbr,
-            c.node_se3, N, c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg);
+            c.node_se3, N, c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg_pre);
   DS_CUDA(cudaMemsetAsync(c.g, 0, sizeof(double) * 6 * N, c.stream));
   AsmArgs A;
   A.up_key = c.up_key;
@@ -1045,11 +1049,12 @@ void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_p
   if (!c.pattern_ready) build_pattern(c, t_now, t_last);
   gn_linearize_async(c, pose, t_now, t_last);
   fetch_scalars(c);
-  if (e_pre) *e_pre = c.hsc->e_data + c.cfg.lambda * c.hsc->e_reg;
+  if (e_pre) *e_pre = c.hsc->e_data_pre + c.cfg.lambda * c.hsc->e_reg_pre;
   if (n_pairs) *n_pairs = c.hsc->n_pairs;
 }
 
-void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double* rel_res) {
+// PCG on the last assembled system with the damping in dsc->mu
+void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   const int N = c.n_nodes;
   PcgArgs a;
   a.row_ptr = c.row_ptr;
@@ -1057,7 +1062,7 @@ void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double*
   a.val = c.bsr_val;
   a.diag_pos = c.diag_pos;
   a.g = c.g;
-  a.mu = mu;
+  a.mu_ptr = &c.dsc->mu;
   a.N = N;
   a.max_iters = max_iters;
   a.tol2 = tol > 0 ? tol * tol : 0.0;
@@ -1081,6 +1086,12 @@ void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double*
   DS_CUDA(cudaMemsetAsync(&c.dsc->finite, 0xff, sizeof(int), c.stream));
   DS_LAUNCH(c, KK_MISC, 48.0 * N, cdiv(6 * N, 256), 256, 0, k_check_finite, c.pcg_x, 6 * N,
             &c.dsc->finite);
+}
+
+void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double* rel_res) {
+  *c.h_mu = mu;
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->mu, c.h_mu, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  pcg_solve_async(c, max_iters, tol);
   if (iters || rel_res) {
     fetch_scalars(c);
     if (iters) *iters = c.hsc->pcg_iters;
@@ -1102,7 +1113,87 @@ void energy_async(Ctx& c, const double* pose, const double4* dq, double* se3) {
 }
 }  // namespace
 
-// solve_nonrigid (solver.cpp:296-422)
+namespace {
+__global__ void k_lm_prep(DevScalars* sc, int dim) {
+  // mu_floor = 1e-6 tr(H) / dim; mu = max(mu, mu_floor)   (solver.cpp:378-379)
+  const double floor_ = 1e-6 * sc->htrace / dim;
+  sc->mu_floor = floor_;
+  sc->mu = fmax(sc->mu, floor_);
+}
+
+// one GN iteration up to the first LM attempt: linearise, mu, PCG, candidate, E_post
+void gn_step_async(Ctx& c, const double* pose, int t_now, int t_last, int max_pcg, double tol) {
+  gn_linearize_async(c, pose, t_now, t_last);
+  DS_LAUNCH(c, KK_MISC, 32.0, 1, 1, 0, k_lm_prep, c.dsc, 6 * c.n_nodes);
+  pcg_solve_async(c, max_pcg, tol);
+  apply_increments(c, c.pcg_x, c.node_dq_cand);
+  energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
+}
+void attempt_async(Ctx& c, const double* pose, int max_pcg, double tol) {
+  pcg_solve_async(c, max_pcg, tol);
+  apply_increments(c, c.pcg_x, c.node_dq_cand);
+  energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
+}
+
+// Capture `enqueue` into `slot` (update the executable graph in place when the
+// topology is unchanged; re-instantiate otherwise). Returns false if the stream
+// cannot be captured (the caller then launches directly).
+template <class F>
+bool capture(Ctx& c, GraphSlot& slot, F&& enqueue) {
+  cudaGraph_t graph = nullptr;
+  const int64_t l0 = c.total_launches;
+  if (cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  try {
+    enqueue();
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    c.total_launches = l0;
+    throw;
+  }
+  if (cudaStreamEndCapture(c.stream, &graph) != cudaSuccess || !graph) {
+    cudaGetLastError();
+    c.total_launches = l0;
+    return false;
+  }
+  slot.kernels = c.total_launches - l0;
+  c.total_launches = l0;
+  if (slot.exec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(slot.exec, graph, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(slot.exec);
+      slot.exec = nullptr;
+    }
+  }
+  if (!slot.exec && cudaGraphInstantiate(&slot.exec, graph, 0) != cudaSuccess) {
+    cudaGetLastError();
+    slot.exec = nullptr;
+    cudaGraphDestroy(graph);
+    return false;
+  }
+  cudaGraphDestroy(graph);
+  return true;
+}
+void replay(Ctx& c, GraphSlot& slot) {
+  DS_CUDA(cudaGraphLaunch(slot.exec, c.stream));
+  c.total_launches += slot.kernels;
+}
+void set_mu(Ctx& c, double mu) {
+  *c.h_mu = mu;
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->mu, c.h_mu, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+}
+}  // namespace
+
+// solve_nonrigid (solver.cpp:296-422). Each GN iteration is one replay of a
+// captured graph (linearise + mu floor + PCG + increments + E_post) and one
+// host sync for the LM decision; rejected attempts replay the attempt graph.
+// The damping mu is kept on the device and mirrored on the host with the same
+// arithmetic, so decisions are those of the reference loop.
 void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver_report* out) {
   ds_solver_report rep{};
   const int N = c.n_nodes, n = c.n_surfels;
@@ -1112,35 +1203,43 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
     *out = rep;
     return;
   }
-  const int dim = 6 * N;
   build_pattern(c, t_now, t_last);
   const int max_pcg = c.cfg.pcg_max_iters > 0 ? c.cfg.pcg_max_iters : 10;
   const double tol = c.cfg.pcg_tol;
+  const bool graphs = c.use_graphs && !c.cfg.profile;
+  bool have_step = false, have_attempt = false;
   double mu = 0.0;
+  set_mu(c, 0.0);
   int n_pairs = 0;
   for (int iter = 0; iter < c.cfg.max_gn_iters; ++iter) {
-    gn_linearize_async(c, pose, t_now, t_last);
+    if (graphs && !have_step)
+      have_step = capture(c, c.g_step, [&] { gn_step_async(c, pose, t_now, t_last, max_pcg, tol); });
+    if (have_step) replay(c, c.g_step);
+    else gn_step_async(c, pose, t_now, t_last, max_pcg, tol);
     fetch_scalars(c);
-    const double e_pre = c.hsc->e_data + c.cfg.lambda * c.hsc->e_reg;
+    const double e_pre = c.hsc->e_data_pre + c.cfg.lambda * c.hsc->e_reg_pre;
     n_pairs = c.hsc->n_pairs;
     c.n_pairs_ok_est = n_pairs;
     if (iter == 0) {
       rep.initial_energy = e_pre;
       rep.final_energy = e_pre;
     }
-    const double ginf = c.hsc->ginf;
-    const double gnorm = std::sqrt(c.hsc->pcg_rr0);
-    if (ginf < 1e-14) break;
-    const double mu_floor = 1e-6 * c.hsc->htrace / dim;
-    mu = std::max(mu, mu_floor);
+    if (c.hsc->ginf < 1e-14) break;  // stationary: the speculative attempt is discarded
+    const double gnorm = std::sqrt(c.hsc->g_sq);
+    const double mu_floor = c.hsc->mu_floor;
+    mu = std::max(mu, mu_floor);  // == c.hsc->mu (same arithmetic on the device)
     bool accepted = false;
     double e_post = e_pre;
     for (int attempt = 0; attempt < 8 && !accepted; ++attempt) {
+      if (attempt > 0) {
+        set_mu(c, mu);
+        if (graphs && !have_attempt)
+          have_attempt = capture(c, c.g_attempt, [&] { attempt_async(c, pose, max_pcg, tol); });
+        if (have_attempt) replay(c, c.g_attempt);
+        else attempt_async(c, pose, max_pcg, tol);
+        fetch_scalars(c);
+      }
       ++c.lm_attempts;
-      pcg_solve(c, mu, max_pcg, tol, nullptr, nullptr);
-      apply_increments(c, c.pcg_x, c.node_dq_cand);
-      energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
-      fetch_scalars(c);
       c.pcg_iterations += c.hsc->pcg_iters;
       const bool finite = c.hsc->finite != 0;
       // residual guard (solver.cpp:387-388) when PCG runs to a tolerance
@@ -1156,7 +1255,9 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
     }
     if (!accepted) break;
     mu = std::max(mu_floor, mu * 0.1);
-    std::swap(c.node_dq, c.node_dq_cand);
+    set_mu(c, mu);
+    DS_CUDA(cudaMemcpyAsync(c.node_dq, c.node_dq_cand, sizeof(double4) * 2 * N,
+                            cudaMemcpyDeviceToDevice, c.stream));
     ++rep.iterations;
     rep.final_energy = e_post;
     if (e_pre - e_post < 1e-4 * std::max(e_pre, 1e-300)) break;

@@ -36,6 +36,25 @@ __global__ void __launch_bounds__(256) k_forward_warp(ModelBuf m, int n,
   __stcs(m.ln + i, ln);
 }
 
+__global__ void __launch_bounds__(256) k_forward_warp_list(ModelBuf m, const int* __restrict__ list,
+                                                           int n, const double4* __restrict__ node_dq) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int i = list[k];
+  const float4 rp = m.rp[i], rn = m.rn[i];
+  const Blend b = blend_entry(m.ki[i], m.kw[i], node_dq);
+  float4 lp = rp, ln = rn;
+  if (!b.degenerate) {
+    const Rig T = blend_rig_fast(b);
+    const V3 p = rig_apply(T, v3(rp.x, rp.y, rp.z));
+    const V3 q = rig_rotate(T, v3(rn.x, rn.y, rn.z));
+    lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
+    ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
+  }
+  m.lp[i] = lp;
+  m.ln[i] = ln;
+}
+
 __global__ void k_node_se3(const double4* __restrict__ dq, int n, double* __restrict__ se3) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -45,8 +64,11 @@ __global__ void k_node_se3(const double4* __restrict__ dq, int n, double* __rest
   rig_store(dq_to_rig(q), se3 + 12 * j);
 }
 
+// live positions (fp64 + an fp32 copy for K-NN pre-tests) and the largest
+// |coordinate| (bound for the fp32 rounding margin, as float bits)
 __global__ void k_node_live(const double4* __restrict__ pos, const double4* __restrict__ dq, int n,
-                            double4* __restrict__ live) {
+                            double4* __restrict__ live, float4* __restrict__ live_f,
+                            int* __restrict__ rmax_bits) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   DQ q;
@@ -55,6 +77,9 @@ __global__ void k_node_live(const double4* __restrict__ pos, const double4* __re
   const double4 p = pos[j];
   const V3 l = rig_apply(dq_to_rig(q), v3(p.x, p.y, p.z));
   live[j] = make_double4(l.x, l.y, l.z, p.w);
+  live_f[j] = make_float4((float)l.x, (float)l.y, (float)l.z, 0.f);
+  const double m = fmax(fmax(fabs(l.x), fabs(l.y)), fabs(l.z));
+  atomicMax(rmax_bits, __float_as_int(__double2float_ru(m)));
 }
 
 __global__ void k_apply_increments(const double4* __restrict__ dq, const double* __restrict__ delta,
@@ -92,6 +117,12 @@ int forward_warp(Ctx& c, bool count_degenerate) {
   return deg;
 }
 
+void forward_warp_list(Ctx& c, const int* list, int n) {
+  if (n == 0) return;
+  DS_LAUNCH(c, KK_FORWARD_WARP, 100.0 * n, cdiv(n, 256), 256, 0, k_forward_warp_list, c.M(), list,
+            n, c.node_dq);
+}
+
 void node_se3(Ctx& c, const double4* dq, double* se3) {
   if (c.n_nodes == 0) return;
   DS_LAUNCH(c, KK_NODE_UPDATE, 160.0 * c.n_nodes, cdiv(c.n_nodes, 128), 128, 0, k_node_se3, dq,
@@ -100,8 +131,9 @@ void node_se3(Ctx& c, const double4* dq, double* se3) {
 
 void node_live_positions(Ctx& c) {
   if (c.n_nodes == 0) return;
-  DS_LAUNCH(c, KK_NODE_UPDATE, 128.0 * c.n_nodes, cdiv(c.n_nodes, 128), 128, 0, k_node_live,
-            c.node_pos, c.node_dq, c.n_nodes, c.node_live);
+  DS_CUDA(cudaMemsetAsync(&c.dsc->rmax_bits, 0, sizeof(int), c.stream));
+  DS_LAUNCH(c, KK_NODE_UPDATE, 144.0 * c.n_nodes, cdiv(c.n_nodes, 128), 128, 0, k_node_live,
+            c.node_pos, c.node_dq, c.n_nodes, c.node_live, c.node_live_f, &c.dsc->rmax_bits);
 }
 
 }  // namespace ds

@@ -198,6 +198,10 @@ ds_status ds_download_normal_equations(ds_context* ctx, int32_t* row_ptr, int32_
 /* (H + mu I) delta = -g by block-Jacobi PCG on the last assembled system */
 ds_status ds_pcg_solve(ds_context* ctx, double mu, int32_t max_iters, double tol, double* delta,
                        int32_t* iters, double* rel_residual);
+/* y = (H + mu I) x by the standalone BSR SpMV kernel on the last assembled system,
+ * repeated `reps` times (device-resident x/y); mean_ms = CUDA-event time per SpMV */
+ds_status ds_bsr_spmv(ds_context* ctx, const double* x, double* y, double mu, int32_t reps,
+                      double* mean_ms);
 /* solve_nonrigid (solver.cpp:296-422) */
 ds_status ds_solve_nonrigid(ds_context* ctx, const double* pose, int32_t t_now,
                             int32_t t_last_reinit, ds_solver_report* out);

@@ -27,6 +27,7 @@ const char* kKernelNames[KK_COUNT] = {
 size_t sort_temp_bytes(int n);
 int pcg_max_grid(int num_sms);
 void build_pattern(Ctx& c, int t_now, int t_last);
+double bsr_spmv(Ctx& c, const double* x_dev, double* y_dev, double mu, int reps);
 void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last);
 void fuse_depth_async(Ctx& c, const double* pose, int t_now);
 
@@ -1028,6 +1029,22 @@ ds_status ds_pcg_solve(ds_context* ctx, double mu, int32_t max_iters, double tol
                             c.stream));
     ds::sync(c);
   }
+  API_END
+}
+
+ds_status ds_bsr_spmv(ds_context* ctx, const double* x, double* y, double mu, int32_t reps,
+                      double* mean_ms) {
+  API_BEGIN
+  REQUIRE(ctx && x && y && reps >= 0, "bad argument");
+  Ctx& c = ctx->c;
+  bind(c);
+  REQUIRE(c.pattern_ready, "no assembled system");
+  const size_t n6 = 6 * (size_t)c.n_nodes;
+  DS_CUDA(cudaMemcpyAsync(c.pcg_p0, x, sizeof(double) * n6, cudaMemcpyHostToDevice, c.stream));
+  const double ms = ds::bsr_spmv(c, c.pcg_p0, c.pcg_q, mu, std::max(1, (int)reps));
+  DS_CUDA(cudaMemcpyAsync(y, c.pcg_q, sizeof(double) * n6, cudaMemcpyDeviceToHost, c.stream));
+  ds::sync(c);
+  if (mean_ms) *mean_ms = ms;
   API_END
 }
 

@@ -880,6 +880,39 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg(PcgArgs a) {
   }
 }
 
+// Standalone BSR SpMV y = (H + mu I) x, the PCG's SpMV phase as its own kernel
+// (warp per block row; lanes = 5 blocks x 6 rows, shuffle row reduction).
+// Algorithmic bytes: 144 B per block (fp32 6x6) + 4 B column index + the x
+// block (48 B, L1/L2-reused) + row pointers and y (48 B per row).
+__global__ void __launch_bounds__(256) k_bsr_spmv(const int* __restrict__ row_ptr,
+                                                  const int* __restrict__ col,
+                                                  const float* __restrict__ val, int N, double mu,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ y) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= N) return;
+  const int row6 = lane % 6, blk5 = lane / 6;
+  const int b0 = row_ptr[j], b1 = row_ptr[j + 1];
+  double acc = 0.0;
+  for (int bb = b0; bb < b1; bb += 5) {
+    const int b = bb + blk5;
+    if (lane < 30 && b < b1) {
+      const int cidx = col[b];
+      const float* vr = val + (size_t)b * 36 + row6 * 6;
+      const double* xc = x + 6 * cidx;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s += (double)vr[k] * xc[k];
+      acc += s;
+    }
+  }
+  double tot = 0.0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) tot += __shfl_sync(0xffffffffu, acc, (lane % 6) + 6 * k);
+  if (lane < 6) y[6 * j + lane] = tot + mu * x[6 * j + lane];
+}
+
 __global__ void k_check_finite(const double* __restrict__ x, int n, int* __restrict__ finite) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && !isfinite(x[i])) atomicAnd(finite, 0);
@@ -1272,6 +1305,26 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
   fetch_scalars(c);
   rep.mean_residual = c.hsc->mean_cnt > 0 ? c.hsc->mean_abs_r / c.hsc->mean_cnt : 0.0;
   *out = rep;
+}
+
+// y = (H + mu I) x on the assembled BSR system, `reps` times; returns mean ms
+double bsr_spmv(Ctx& c, const double* x_dev, double* y_dev, double mu, int reps) {
+  const int N = c.n_nodes;
+  cudaEvent_t a, b;
+  DS_CUDA(cudaEventCreate(&a));
+  DS_CUDA(cudaEventCreate(&b));
+  const double bytes = 148.0 * c.n_full + 56.0 * N;
+  DS_CUDA(cudaEventRecord(a, c.stream));
+  for (int r = 0; r < reps; ++r)
+    DS_LAUNCH(c, KK_PCG, bytes, cdiv((long long)N * 32, 256), 256, 0, k_bsr_spmv, c.row_ptr,
+              c.bsr_col, c.bsr_val, N, mu, x_dev, y_dev);
+  DS_CUDA(cudaEventRecord(b, c.stream));
+  sync(c);
+  float ms = 0;
+  DS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return reps > 0 ? ms / reps : 0.0;
 }
 
 int pcg_max_grid(int num_sms) {

@@ -107,6 +107,7 @@ struct Scene {
   std::vector<Sheet> sheets;
   std::vector<Ellipsoid> ellipsoids;
   std::vector<Capsule> capsules;
+  std::vector<struct SineSheet> sines;
 };
 
 double ray_rect(P3 o, P3 d, const RectZ& r) {  // synth.cpp:75-84
@@ -216,8 +217,34 @@ double dist_ellipsoid(P3 p, const Ellipsoid& e) {
   return gl > 0 ? std::abs(f) / gl : len(l);
 }
 
+// Config 4 (solver micro-bench) surface: a height field z = z0 + a sin(kx x + phase)
+// sin(ky y) filling the whole field of view, so the node count scales with the
+// image size (~130 surfels per node at f/z ~ 465).
+struct SineSheet {
+  double z0, a, kx, ky, phase;
+};
+double ray_sine(P3 o, P3 d, const SineSheet& h) {
+  if (d.z <= 1e-9) return kInf;
+  double s = (h.z0 - o.z) / d.z;
+  for (int it = 0; it < 40; ++it) {
+    const P3 q = o + s * d;
+    const double z = h.z0 + h.a * std::sin(h.kx * q.x + h.phase) * std::sin(h.ky * q.y);
+    const double ns = (z - o.z) / d.z;
+    if (std::abs(ns - s) < 1e-12) {
+      s = ns;
+      break;
+    }
+    s = ns;
+  }
+  return s > 1e-9 ? s : kInf;
+}
+double dist_sine(P3 p, const SineSheet& h) {
+  return std::abs(p.z - (h.z0 + h.a * std::sin(h.kx * p.x + h.phase) * std::sin(h.ky * p.y)));
+}
+
 double scene_raycast(P3 o, P3 d, const Scene& s) {
   double best = kInf;
+  for (const auto& r : s.sines) best = std::min(best, ray_sine(o, d, r));
   for (const auto& r : s.rects) best = std::min(best, ray_rect(o, d, r));
   for (const auto& r : s.spheres) best = std::min(best, ray_sphere(o, d, r));
   for (const auto& r : s.sheets) best = std::min(best, ray_sheet(o, d, r));
@@ -227,6 +254,7 @@ double scene_raycast(P3 o, P3 d, const Scene& s) {
 }
 double scene_distance(P3 p, const Scene& s) {
   double best = kInf;
+  for (const auto& r : s.sines) best = std::min(best, dist_sine(p, r));
   for (const auto& r : s.rects) best = std::min(best, dist_rect(p, r));
   for (const auto& r : s.spheres) best = std::min(best, dist_sphere(p, r));
   for (const auto& r : s.sheets) best = std::min(best, dist_sheet(p, r));
@@ -245,11 +273,13 @@ enum Kind {
   kTurntable,
   kDeformingSphere,
   kArticulatedBody,
+  kSineSheet,
   kNumKinds
 };
 const char* kNames[kNumKinds] = {"static_plane",     "rigid_orbit",    "bending_sheet",
                                  "articulated_two_part", "open_to_close", "tangential_slide",
-                                 "turntable",        "deforming_sphere", "articulated_body"};
+                                 "turntable",        "deforming_sphere", "articulated_body",
+                                 "sine_sheet"};
 int default_frames(int kind) {  // synth.cpp:213-224 (+ new scenes)
   switch (kind) {
     case kStaticPlane: return 10;
@@ -261,6 +291,7 @@ int default_frames(int kind) {  // synth.cpp:213-224 (+ new scenes)
     case kTurntable: return 360;
     case kDeformingSphere: return 10;
     case kArticulatedBody: return 100;
+    case kSineSheet: return 10;
   }
   return 60;
 }
@@ -368,6 +399,9 @@ Scene scene_at(int kind, double u) {  // synth.cpp:275-334 (+ new scenes)
     }
     case kArticulatedBody:
       articulated_body(s, u);
+      break;
+    case kSineSheet:  // 2 cm waves travelling ~1.3 mm per frame over 10 frames
+      s.sines.push_back({1.2, 0.02, 2.0 * kPi / 0.4, 2.0 * kPi / 0.3, 0.2 * kPi * u});
       break;
   }
   return s;

@@ -264,6 +264,14 @@ class Context:
                                   C.byref(rel)))
         return delta, it.value, rel.value
 
+    def bsr_spmv(self, x, mu=0.0, reps=1):
+        """y = (H + mu I) x with the standalone SpMV kernel; returns (y, mean ms)."""
+        x = _f64(x)
+        y = np.zeros_like(x)
+        ms = C.c_double()
+        check(self.L.ds_bsr_spmv(self.h, _p(x), _p(y), mu, reps, C.byref(ms)))
+        return y, ms.value
+
     def solve_nonrigid(self, pose, t_now, t_last) -> DsSolverReport:
         rep = DsSolverReport()
         check(self.L.ds_solve_nonrigid(self.h, _p(_f64(pose)), t_now, t_last, C.byref(rep)))

@@ -28,7 +28,7 @@ size_t sort_temp_bytes(int n);
 int pcg_max_grid(int num_sms);
 void build_pattern(Ctx& c, int t_now, int t_last);
 double bsr_spmv(Ctx& c, const double* x_dev, double* y_dev, double mu, int reps);
-void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last);
+void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor);
 void fuse_depth_async(Ctx& c, const double* pose, int t_now);
 
 thread_local std::string g_last_error;
@@ -209,6 +209,9 @@ void allocate(Ctx& c) {
   c.diag_pos = dalloc<int>(c, N);
   c.CH_cap = c.R_cap / 64 + c.UB_cap + 1;
   c.chunk_first = dalloc<int>(c, c.UB_cap + 1);
+  c.multi_flag = dalloc<int>(c, c.UB_cap + 1);
+  c.multi_scan = dalloc<int>(c, c.UB_cap + 1);
+  c.multi_list = dalloc<int>(c, c.UB_cap + 1);
   c.chunk_ub = dalloc<int>(c, c.CH_cap);
   c.part_h = dalloc<float>(c, (size_t)c.CH_cap * 36);
   c.part_g = dalloc<double>(c, (size_t)c.CH_cap * 6);
@@ -220,18 +223,21 @@ void allocate(Ctx& c) {
   c.cub_tmp = dalloc<char>(c, c.cub_tmp_bytes);
   c.g = dalloc<double>(c, 6 * N);
   c.pcg_x = dalloc<double>(c, 6 * N);
-  c.pcg_r = dalloc<double>(c, 6 * N);
-  c.pcg_z = dalloc<double>(c, 6 * N);
   c.pcg_p0 = dalloc<double>(c, 6 * N);
   c.pcg_p1 = dalloc<double>(c, 6 * N);
+  c.pcg_p2 = dalloc<double>(c, 6 * N);
   c.pcg_q = dalloc<double>(c, 6 * N);
   c.pcg_minv = dalloc<double>(c, 36 * N);
+  c.pcg_items = dalloc<double>(c, 6 * (size_t)c.B_cap);
+  c.pcg_vec = dalloc<double>(c, 60 * (size_t)N);
+  c.gst_part = dalloc<double>(c, 3 * (size_t)cdiv(N, 256) + 8);
+  c.reg_ab = dalloc<double>(c, 48 * (size_t)N);
   c.pcg_grid = pcg_max_grid(c.num_sms);
   if (const char* e = std::getenv("DS_PCG_GRID")) {  // tuning knob (capped at co-residency)
     const int g = std::atoi(e);
     if (g > 0) c.pcg_grid = std::min(c.pcg_grid, g);
   }
-  c.pcg_part = dalloc<double>(c, 4 * (size_t)c.pcg_grid);
+  c.pcg_part = dalloc<double>(c, 8 * (size_t)c.pcg_grid);
   c.cand_flag = dalloc<int>(c, P + 1);
   c.cand_scan = dalloc<int>(c, P + 1);
   c.cand_pix = dalloc<int>(c, P);

@@ -182,7 +182,10 @@ struct Ctx {
   double* r_l = nullptr;       // pair residuals in list order
   int* elig = nullptr;  // render-eligible surfels of the current frame's solve
   int n_elig = 0;
-  int n_records = 0, n_up = 0, n_full = 0, n_chunks = 0, CH_cap = 0;
+  int n_records = 0, n_up = 0, n_full = 0, n_chunks = 0, n_multi = 0, CH_cap = 0;
+  int* multi_flag = nullptr;
+  int* multi_scan = nullptr;
+  int* multi_list = nullptr;
   double n_pairs_ok_est = 0;
   bool pattern_ready = false;
   void* cub_tmp = nullptr;
@@ -190,12 +193,15 @@ struct Ctx {
   // PCG
   double* g = nullptr;
   double* pcg_x = nullptr;
-  double* pcg_r = nullptr;
-  double* pcg_z = nullptr;
   double* pcg_p0 = nullptr;
   double* pcg_p1 = nullptr;
+  double* pcg_p2 = nullptr;
   double* pcg_q = nullptr;
   double* pcg_minv = nullptr;
+  double* pcg_items = nullptr;
+  double* pcg_vec = nullptr;
+  double* gst_part = nullptr;
+  double* reg_ab = nullptr;
   double* pcg_part = nullptr;
   int pcg_grid = 0;
   // fusion

@@ -247,4 +247,40 @@ DSI bool nb_less(double d2a, int ia, double d2b, int ib) {
   return d2a != d2b ? d2a < d2b : ia < ib;
 }
 
+// sorted (d2, index) top-4 insertion (used by every exact 4-NN kernel)
+DSI void knn4_insert(double d2, int j, double bd[4], int bi[4]) {
+  if (!nb_less(d2, j, bd[3], bi[3])) return;
+  double cd = d2;
+  int ci = j;
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+    if (nb_less(cd, ci, bd[s], bi[s])) {
+      const double td = bd[s];
+      const int ti = bi[s];
+      bd[s] = cd;
+      bi[s] = ci;
+      cd = td;
+      ci = ti;
+    }
+}
+
+// Butterfly merge of the per-lane top-4 lists of an aligned group of LANES
+// lanes that scanned disjoint index subsets: afterwards every lane of the group
+// holds the group's exact top-4 (strict total order => identical in all lanes).
+template <int LANES>
+__device__ __forceinline__ void knn4_merge_lanes(double bd[4], int bi[4]) {
+#pragma unroll
+  for (int off = LANES / 2; off > 0; off >>= 1) {
+    double od[4];
+    int oi[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      od[s] = __shfl_xor_sync(0xffffffffu, bd[s], off);
+      oi[s] = __shfl_xor_sync(0xffffffffu, bi[s], off);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) knn4_insert(od[s], oi[s], bd, bi);
+  }
+}
+
 }  // namespace ds

@@ -164,22 +164,6 @@ __device__ bool inv_warp_reweighted(V3 x, const int* ids, int cnt, const double4
 
 // skin_appended + check_compressive for candidate k (fusion.cpp:77-177).
 // result: 0 = low support, 1 = compressive reject, 2 = accepted
-__device__ __forceinline__ void knn4_insert(double d2, int j, double bd[4], int bi[4]) {
-  if (!nb_less(d2, j, bd[3], bi[3])) return;
-  double cd = d2;
-  int ci = j;
-#pragma unroll
-  for (int s = 0; s < 4; ++s)
-    if (nb_less(cd, ci, bd[s], bi[s])) {
-      const double td = bd[s];
-      const int ti = bi[s];
-      bd[s] = cd;
-      bi[s] = ci;
-      cd = td;
-      ci = ti;
-    }
-}
-
 // Eq. 6 ratio test, weights, delta_nn, compressive check on a K-NN list.
 __device__ int screen_one(V3 x, const double bd[4], const int bi[4],
                           const double4* __restrict__ node_pos,
@@ -232,16 +216,23 @@ __device__ int screen_one(V3 x, const double bd[4], const int bi[4],
   return 2;
 }
 
-__global__ void k_screen(const float4* __restrict__ cp, const int* __restrict__ n_cand_dev,
-                         const double4* __restrict__ node_pos, const double4* __restrict__ node_live,
-                         const float4* __restrict__ node_live_f, const int* __restrict__ rmax_bits,
-                         const double4* __restrict__ node_dq, ScreenParams sp,
-                         int4* __restrict__ cki, float4* __restrict__ ckw, int* __restrict__ ok,
-                         int* __restrict__ res_out, int* __restrict__ low, int* __restrict__ comp) {
-  __shared__ float4 tile[128];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// kScreenLanes lanes per candidate, each scanning a strided subset of the
+// node tiles; the per-lane top-4 lists are merged by a shuffle butterfly.
+constexpr int kScreenLanes = 8;
+constexpr int kScreenThreads = 256;
+
+__global__ void __launch_bounds__(kScreenThreads, 2) k_screen(
+    const float4* __restrict__ cp, const int* __restrict__ n_cand_dev,
+    const double4* __restrict__ node_pos, const double4* __restrict__ node_live,
+    const float4* __restrict__ node_live_f, const int* __restrict__ rmax_bits,
+    const double4* __restrict__ node_dq, ScreenParams sp, int4* __restrict__ cki,
+    float4* __restrict__ ckw, int* __restrict__ ok, int* __restrict__ res_out,
+    int* __restrict__ low, int* __restrict__ comp) {
+  __shared__ float4 tile[kScreenThreads];
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = gt / kScreenLanes, lane_k = gt % kScreenLanes;
   const int n = *n_cand_dev;
-  if (blockIdx.x * blockDim.x >= n) return;  // whole block idle
+  if (blockIdx.x * (kScreenThreads / kScreenLanes) >= n) return;  // whole block idle
   const bool active = k < n;
   V3 x = v3(0, 0, 0);
   float xf = 0.f, yf = 0.f, zf = 0.f;
@@ -252,33 +243,71 @@ __global__ void k_screen(const float4* __restrict__ cp, const int* __restrict__ 
     yf = p.y;
     zf = p.z;
   }
-  // Exact live-frame K-NN by (d2, idx) over shared-memory tiles. fp32 pre-test:
-  // node coordinates rounded to fp32 move each |difference| by <= u*R (+ u of
-  // the difference), so with delta = 1.8 u R every node of the exact top-K has
-  // d2f <= (sqrt(bd3) + delta)^2 (1 + 1e-5) = thr and reaches the fp64 test.
+  // Exact live-frame K-NN by (d2, idx) in two passes over shared-memory tiles.
+  // Rounding model: node coordinates rounded to fp32 move each |difference| by
+  // <= u*R (+ u of the difference), so |sqrt(d2f) - sqrt(d2)| <= delta = 1.8 u R
+  // up to a relative 1e-5 for the fp32 arithmetic.
+  // Pass 1 (fp32 only, branch-free): T32 = 4th smallest d2f of the candidate.
+  // The 4 nodes realising T32 have d2 <= B = (sqrt(T32 (1+2e-5)) + delta)^2, so
+  // the exact 4th-smallest d2 is <= B and every node of the exact top-4 has
+  // d2f <= T' = (sqrt(B) + delta)^2 (1+2e-5). Pass 2 evaluates the exact fp64
+  // (d2, idx) order only for nodes with d2f <= T' (a handful per candidate).
   const double delta = 1.8 * 5.9604644775390625e-8 * (double)__int_as_float(*rmax_bits);
-  double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-  int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-  float thr = INFINITY;
-  for (int base = 0; base < sp.N; base += 128) {
+  float t0 = INFINITY, t1 = INFINITY, t2 = INFINITY, t3 = INFINITY;
+  for (int base = 0; base < sp.N; base += kScreenThreads) {
     __syncthreads();
     if (base + threadIdx.x < sp.N) tile[threadIdx.x] = node_live_f[base + threadIdx.x];
     __syncthreads();
-    const int lim = min(128, sp.N - base);
+    const int lim = min(kScreenThreads, sp.N - base);
     if (active)
-      for (int t = 0; t < lim; ++t) {
+      for (int t = lane_k; t < lim; t += kScreenLanes) {
+        const float4 q = tile[t];
+        const float dx = q.x - xf, dy = q.y - yf, dz = q.z - zf;
+        float v = (dx * dx + dy * dy) + dz * dz, m;
+        m = fminf(t0, v); v = fmaxf(t0, v); t0 = m;
+        m = fminf(t1, v); v = fmaxf(t1, v); t1 = m;
+        m = fminf(t2, v); v = fmaxf(t2, v); t2 = m;
+        t3 = fminf(t3, v);
+      }
+  }
+#pragma unroll
+  for (int off = kScreenLanes / 2; off > 0; off >>= 1) {
+    const float o0 = __shfl_xor_sync(0xffffffffu, t0, off), o1 = __shfl_xor_sync(0xffffffffu, t1, off),
+                o2 = __shfl_xor_sync(0xffffffffu, t2, off), o3 = __shfl_xor_sync(0xffffffffu, t3, off);
+    const float ov[4] = {o0, o1, o2, o3};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float v = ov[u], m;
+      m = fminf(t0, v); v = fmaxf(t0, v); t0 = m;
+      m = fminf(t1, v); v = fmaxf(t1, v); t1 = m;
+      m = fminf(t2, v); v = fmaxf(t2, v); t2 = m;
+      t3 = fminf(t3, v);
+    }
+  }
+  float thr = INFINITY;
+  if (t3 < INFINITY) {
+    const double B = sqrt((double)t3 * (1.0 + 2e-5)) + delta;
+    const double tp = B + delta;
+    thr = (float)(tp * tp * (1.0 + 2e-5)) + 1e-37f;
+  }
+  double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+  for (int base = 0; base < sp.N; base += kScreenThreads) {
+    __syncthreads();
+    if (base + threadIdx.x < sp.N) tile[threadIdx.x] = node_live_f[base + threadIdx.x];
+    __syncthreads();
+    const int lim = min(kScreenThreads, sp.N - base);
+    if (active)
+      for (int t = lane_k; t < lim; t += kScreenLanes) {
         const float4 q = tile[t];
         const float dx = q.x - xf, dy = q.y - yf, dz = q.z - zf;
         if ((dx * dx + dy * dy) + dz * dz > thr) continue;
         const double4 nl = node_live[base + t];
         knn4_insert(sqn(sub(v3(nl.x, nl.y, nl.z), x)), base + t, bd, bi);
-        if (bd[3] < INFINITY) {
-          const double rr = sqrt(bd[3]) + delta;
-          thr = (float)(rr * rr * (1.0 + 1e-5)) + 1e-37f;
-        }
       }
   }
-  if (!active) return;
+  knn4_merge_lanes<kScreenLanes>(bd, bi);
+  if (!active || lane_k != 0) return;
   int ids[4];
   float ws[4];
   int cnt = 0;
@@ -516,7 +545,8 @@ void screen_candidates_async(Ctx& c) {
   DS_CUDA(cudaMemsetAsync(&c.dsc->comp_rejected, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(c.cand_ok, 0, sizeof(int) * c.P, c.stream));
   node_live_positions(c);
-  DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02, cdiv(c.P, 128), 128, 0, k_screen, c.cand_p,
+  DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02, cdiv((long long)c.P * kScreenLanes, kScreenThreads),
+            kScreenThreads, 0, k_screen, c.cand_p,
             &c.dsc->n_cand, c.node_pos, c.node_live, c.node_live_f, &c.dsc->rmax_bits, c.node_dq,
             screen_params(c), c.cand_ki,
             c.cand_kw, c.cand_ok, c.cand_flag, &c.dsc->low_support, &c.dsc->comp_rejected);

@@ -80,9 +80,10 @@ __device__ void ht_insert_single(const HashView& h, long long k, int id, int* er
 __device__ bool ht_any_within(const HashView& h, const double4* node_pos, V3 p, double r2) {
   int cx, cy, cz;
   cell_of(h, p, cx, cy, cz);
-  for (int dz = -1; dz <= 1; ++dz)
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dx = -1; dx <= 1; ++dx) {
+  // centre cell first: a covered point usually exits on its own cell
+  for (int o = 0; o < 27; ++o) {
+        const int oc = (o + 13) % 27;  // 13 = (0,0,0)
+        const int dx = oc % 3 - 1, dy = (oc / 3) % 3 - 1, dz = oc / 9 - 1;
         const int s = ht_find(h, pack_cell(cx + dx, cy + dy, cz + dz));
         if (s < 0) continue;
         const int c = __ldcg(h.cnt + s);
@@ -91,7 +92,7 @@ __device__ bool ht_any_within(const HashView& h, const double4* node_pos, V3 p, 
           const double4 np = ldcg_d4(node_pos + id);
           if (sqn(sub(v3(np.x, np.y, np.z), p)) < r2) return true;
         }
-      }
+  }
   return false;
 }
 
@@ -340,32 +341,24 @@ __global__ void __launch_bounds__(kTile) k_skin_knn(ModelBuf m, int n, const dou
 }
 
 // Seeds of appended nodes from their K nearest pre-existing nodes.
+// Warp per new node: exact 4-NN among the N0 pre-existing nodes (lanes scan
+// strided subsets, shuffle merge), then lane 0 blends their DQs.
 __global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, int N, int K) {
-  const int jn = N0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (jn >= N) return;
+  const int jn = N0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (jn >= N) return;  // warp-uniform
   DQ out = dq_identity();
   if (N0 > 0) {
     const double4 pn = pos[jn];
     const V3 p = v3(pn.x, pn.y, pn.z);
     double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-    for (int i = 0; i < N0; ++i) {
+    for (int i = lane; i < N0; i += 32) {
       const double4 q = pos[i];
-      const double d2 = sqn(sub(v3(q.x, q.y, q.z), p));
-      if (!nb_less(d2, i, bd[3], bi[3])) continue;
-      double cd = d2;
-      int ci = i;
-#pragma unroll
-      for (int s = 0; s < 4; ++s)
-        if (nb_less(cd, ci, bd[s], bi[s])) {
-          const double td = bd[s];
-          const int ti = bi[s];
-          bd[s] = cd;
-          bi[s] = ci;
-          cd = td;
-          ci = ti;
-        }
+      knn4_insert(sqn(sub(v3(q.x, q.y, q.z), p)), i, bd, bi);
     }
+    knn4_merge_lanes<32>(bd, bi);
+    if (lane != 0) return;
     Q4 rs = q4(0, 0, 0, 0), ds_ = q4(0, 0, 0, 0);
     const int cnt = min(K, N0);
     const Q4 pivot = ld_q_plain(dq + 2 * bi[0]);
@@ -385,6 +378,7 @@ __global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, 
       out = dq_normalized(raw);
     }
   }
+  if (lane != 0) return;
   dq[2 * jn] = make_double4(out.r.w, out.r.x, out.r.y, out.r.z);
   dq[2 * jn + 1] = make_double4(out.d.w, out.d.x, out.d.y, out.d.z);
 }
@@ -553,7 +547,7 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
   const int added = total - n0;
   c.n_nodes = total;
   if (added > 0) {
-    DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, cdiv(added, 64), 64, 0, k_seed_dq, c.node_pos,
+    DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, cdiv((long long)added * 32, 128), 128, 0, k_seed_dq, c.node_pos,
               c.node_dq, n0, total, std::min(4, c.cfg.knn_k));
     compute_node_edges(c);
   }

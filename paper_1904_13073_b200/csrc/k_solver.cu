@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(256) k_reg_energy(const double4* __restrict__ 
                                                     const double* __restrict__ se3, int N,
                                                     double* __restrict__ part,
                                                     unsigned* __restrict__ ticket,
-                                                    double* __restrict__ out) {
+                                                    double* __restrict__ out,
+                                                    double* __restrict__ ab_out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
   if (e < 8 * N) {
@@ -204,7 +205,14 @@ __global__ void __launch_bounds__(256) k_reg_energy(const double4* __restrict__ 
       const double4 pj = pos[j];
       const V3 p = v3(pj.x, pj.y, pj.z);
       const Rig Tj = rig_load(se3 + 12 * j), Ti = rig_load(se3 + 12 * i);
-      v = sqn(sub(rig_apply(Tj, p), rig_apply(Ti, p)));
+      const V3 a = rig_apply(Tj, p), b = rig_apply(Ti, p);
+      v = sqn(sub(a, b));
+      if (ab_out) {  // linearisation: T_j p_j and T_i p_j for the Jacobians
+        double2* o = reinterpret_cast<double2*>(ab_out + 6 * (size_t)e);
+        o[0] = make_double2(a.x, a.y);
+        o[1] = make_double2(a.z, b.x);
+        o[2] = make_double2(b.y, b.z);
+      }
     }
   }
   grid_sum<256>(v, part, ticket, out);
@@ -436,6 +444,7 @@ struct AsmArgs {
   const double4* node_pos;
   const int* nbr;
   const double* se3;
+  const double* reg_ab;  // per directed edge: T_j p_j, T_i p_j (k_reg_energy)
   double lambda;
   int N;
   int n_up;
@@ -448,33 +457,108 @@ struct AsmArgs {
   double* g;
 };
 
-__device__ __forceinline__ void reg_jac(const double4* __restrict__ pos, const int* __restrict__ nbr,
-                                        const double* __restrict__ se3, int e, double Jj[3][6],
-                                        double Ji[3][6], double rv[3]) {
-  const int j = e >> 3, i = nbr[e];
-  const double4 pj = pos[j];
-  const V3 p = v3(pj.x, pj.y, pj.z);
-  const V3 a = rig_apply(rig_load(se3 + 12 * j), p);
-  const V3 b = rig_apply(rig_load(se3 + 12 * i), p);
-  const V3 r = sub(a, b);
-  rv[0] = r.x;
-  rv[1] = r.y;
-  rv[2] = r.z;
-  // reg_jacobian_j = [-[a]x, I], reg_jacobian_i = [[b]x, -I]  (solver.cpp:118-130)
-  const double sa[3][3] = {{0, -a.z, a.y}, {a.z, 0, -a.x}, {-a.y, a.x, 0}};
-  const double sb[3][3] = {{0, -b.z, b.y}, {b.z, 0, -b.x}, {-b.y, b.x, 0}};
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      Jj[k][c] = -sa[k][c];
-      Jj[k][3 + c] = (k == c) ? 1.0 : 0.0;
-      Ji[k][c] = sb[k][c];
-      Ji[k][3 + c] = (k == c) ? -1.0 : 0.0;
+// column x of reg_jacobian_j = [-[a]x, I] (sel 0) or reg_jacobian_i = [[b]x, -I]
+// (sel 1) (solver.cpp:118-130), entry by entry as the dense form has them
+__device__ __forceinline__ V3 reg_col(int sel, int x, const V3& a, const V3& b) {
+  if (sel == 0) {
+    switch (x) {
+      case 0: return v3(-0.0, -a.z, a.y);
+      case 1: return v3(a.z, -0.0, -a.x);
+      case 2: return v3(-a.y, a.x, -0.0);
+      default: return v3(x == 3 ? 1.0 : 0.0, x == 4 ? 1.0 : 0.0, x == 5 ? 1.0 : 0.0);
     }
+  }
+  switch (x) {
+    case 0: return v3(0.0, b.z, -b.y);
+    case 1: return v3(-b.z, 0.0, b.x);
+    case 2: return v3(b.y, -b.x, 0.0);
+    default: return v3(x == 3 ? -1.0 : 0.0, x == 4 ? -1.0 : 0.0, x == 5 ? -1.0 : 0.0);
+  }
 }
 
-__global__ void __launch_bounds__(256) k_assemble_chunks(AsmArgs A) {
+// Regulariser record (edge e = 8 j + slot, type 0: JjtJj / gj, 1: JitJi / gi,
+// 2: JjtJi, 3: JitJj) accumulated like the surfel records (float per term).
+__device__ __forceinline__ void acc_reg_record(const AsmArgs& A, int v, float h[36],
+                                               double gg[6]) {
+  const int e = (v & 0x7fffffff) >> 2, type = v & 3;
+  const double2* ab = reinterpret_cast<const double2*>(A.reg_ab + 6 * (size_t)e);
+  const double2 u0 = __ldg(ab), u1 = __ldg(ab + 1), u2 = __ldg(ab + 2);
+  const V3 a = v3(u0.x, u0.y, u1.x), b = v3(u1.y, u2.x, u2.y);
+  const V3 rv = sub(a, b);
+  const int ls = (type == 0 || type == 2) ? 0 : 1, rs = (type == 0 || type == 3) ? 0 : 1;
+  // one block row at a time (rolled loop, constant-index row update via the
+  // switch) keeps the live set small next to the 36 accumulators
+#pragma unroll 1
+  for (int x = 0; x < 6; ++x) {
+    const V3 L = reg_col(ls, x, a, b);
+    float t[6];
+#pragma unroll
+    for (int y = 0; y < 6; ++y) {
+      const V3 R = reg_col(rs, y, a, b);
+      t[y] = (float)(A.lambda * ((L.x * R.x + L.y * R.y) + L.z * R.z));
+    }
+    const double gx = type <= 1 ? A.lambda * ((L.x * rv.x + L.y * rv.y) + L.z * rv.z) : 0.0;
+    switch (x) {
+#define DS_REG_ROW(X)                                   \
+  case X:                                               \
+    _Pragma("unroll") for (int y = 0; y < 6; ++y) h[X * 6 + y] += t[y]; \
+    if (type <= 1) gg[X] += gx;                         \
+    break;
+      DS_REG_ROW(0)
+      DS_REG_ROW(1)
+      DS_REG_ROW(2)
+      DS_REG_ROW(3)
+      DS_REG_ROW(4)
+      DS_REG_ROW(5)
+#undef DS_REG_ROW
+    }
+  }
+}
+
+__device__ __forceinline__ void load_rows(const float* __restrict__ rw, int mr, int mc, float a[6],
+                                          float b[6]) {
+  const float2* ra = reinterpret_cast<const float2*>(rw + mr * 6);
+  const float2* rb = reinterpret_cast<const float2*>(rw + mc * 6);
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const float2 x = __ldg(ra + t), y = __ldg(rb + t);
+    a[2 * t] = x.x;
+    a[2 * t + 1] = x.y;
+    b[2 * t] = y.x;
+    b[2 * t + 1] = y.y;
+  }
+}
+
+__device__ __forceinline__ void acc_pair(const float a[6], const float b[6], bool diag, double r,
+                                         float h[36], double gg[6]) {
+#pragma unroll
+  for (int x = 0; x < 6; ++x)
+#pragma unroll
+    for (int y = 0; y < 6; ++y) h[x * 6 + y] += a[x] * b[y];
+  if (diag) {
+#pragma unroll
+    for (int x = 0; x < 6; ++x) gg[x] += (double)a[x] * r;
+  }
+}
+
+// A surfel record: its pair list (list order = pixel order), the first pair's
+// rows already loaded into (a, b, r).
+__device__ __forceinline__ void acc_surfel_record(const AsmArgs& A, int v, int cnt, int off,
+                                                  const float a[6], const float b[6], double r,
+                                                  bool diag, float h[36], double gg[6]) {
+  const int mr = (v >> 2) & 3, mc = v & 3;
+  acc_pair(a, b, diag, r, h, gg);
+  for (int q = 1; q < cnt; ++q) {
+    float a2[6], b2[6];
+    load_rows(A.rows_l + (size_t)(off + q) * 24, mr, mc, a2, b2);
+    acc_pair(a2, b2, diag, diag ? __ldg(A.r_l + off + q) : 0.0, h, gg);
+  }
+}
+
+// Lane l of a chunk takes records l, l+8, ... in order; two records are in
+// flight per step (their count/offset and first-pair rows are loaded before
+// either is accumulated), the accumulation order is unchanged.
+__global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int chunk = gid / kChunkLanes, l = gid % kChunkLanes;
   const bool valid = chunk < A.n_chunks;  // uniform within a lane group
@@ -485,59 +569,62 @@ __global__ void __launch_bounds__(256) k_assemble_chunks(AsmArgs A) {
 #pragma unroll
   for (int t = 0; t < 6; ++t) gg[t] = 0.0;
   int touched = 0;
+  int ub = 0, key = 0, c0 = 0, c1 = 0;
+  bool diag = false;
   if (valid) {
-    const int ub = A.chunk_ub[chunk];
-    const int key = A.up_key[ub];
-    const bool diag = (key / A.N) == (key % A.N);
-    const int first = A.chunk_first[ub];
-    const int r0 = A.up_start[ub] + (chunk - first) * kChunk;
+    ub = A.chunk_ub[chunk];
+    key = A.up_key[ub];
+    diag = (key / A.N) == (key % A.N);
+    c0 = A.chunk_first[ub];
+    c1 = A.chunk_first[ub + 1];
+    const int r0 = A.up_start[ub] + (chunk - c0) * kChunk;
     const int r1 = min(r0 + kChunk, A.up_start[ub + 1]);
-    for (int k = r0 + l; k < r1; k += kChunkLanes) {
-      const int v = A.rec_val[k];
-      if (v < 0) {
-        const int e = (v & 0x7fffffff) >> 2, type = v & 3;
-        double Jj[3][6], Ji[3][6], rv[3];
-        reg_jac(A.node_pos, A.nbr, A.se3, e, Jj, Ji, rv);
-        touched = 1;
-        const bool lj = (type == 0 || type == 2), rj = (type == 0 || type == 3);
-#pragma unroll
-        for (int x = 0; x < 6; ++x) {
-#pragma unroll
-          for (int y = 0; y < 6; ++y) {
-            const double L0 = lj ? Jj[0][x] : Ji[0][x], L1 = lj ? Jj[1][x] : Ji[1][x],
-                         L2 = lj ? Jj[2][x] : Ji[2][x];
-            const double R0 = rj ? Jj[0][y] : Ji[0][y], R1 = rj ? Jj[1][y] : Ji[1][y],
-                         R2 = rj ? Jj[2][y] : Ji[2][y];
-            h[x * 6 + y] += (float)(A.lambda * ((L0 * R0 + L1 * R1) + L2 * R2));
-          }
-          if (type <= 1) {
-            const double L0 = lj ? Jj[0][x] : Ji[0][x], L1 = lj ? Jj[1][x] : Ji[1][x],
-                         L2 = lj ? Jj[2][x] : Ji[2][x];
-            gg[x] += A.lambda * ((L0 * rv[0] + L1 * rv[1]) + L2 * rv[2]);
-          }
+    for (int k = r0 + l; k < r1; k += 2 * kChunkLanes) {
+      const bool has1 = k + kChunkLanes < r1;
+      const int v0 = A.rec_val[k];
+      const int v1 = has1 ? A.rec_val[k + kChunkLanes] : 0;
+      if (v0 >= 0 && v1 >= 0) {
+        // two surfel records in flight
+        const int cnt0 = A.s_cnt[v0 >> 4], off0 = A.s_off[v0 >> 4];
+        int cnt1 = 0, off1 = 0;
+        if (has1) {
+          cnt1 = A.s_cnt[v1 >> 4];
+          off1 = A.s_off[v1 >> 4];
+        }
+        float a0[6], b0[6], a1[6], b1[6];
+        double rr0 = 0.0, rr1 = 0.0;
+        if (cnt0 > 0) {
+          load_rows(A.rows_l + (size_t)off0 * 24, (v0 >> 2) & 3, v0 & 3, a0, b0);
+          if (diag) rr0 = __ldg(A.r_l + off0);
+        }
+        if (cnt1 > 0) {
+          load_rows(A.rows_l + (size_t)off1 * 24, (v1 >> 2) & 3, v1 & 3, a1, b1);
+          if (diag) rr1 = __ldg(A.r_l + off1);
+        }
+        if (cnt0 > 0) {
+          acc_surfel_record(A, v0, cnt0, off0, a0, b0, rr0, diag, h, gg);
+          touched = 1;
+        }
+        if (cnt1 > 0) {
+          acc_surfel_record(A, v1, cnt1, off1, a1, b1, rr1, diag, h, gg);
+          touched = 1;
         }
       } else {
-        const int s = v >> 4, mr = (v >> 2) & 3, mc = v & 3;
-        const int cnt = A.s_cnt[s];
-        if (cnt == 0) continue;
-        touched = 1;
-        const int off = A.s_off[s];
-        for (int q = 0; q < cnt; ++q) {
-          const float* rw = A.rows_l + (size_t)(off + q) * 24;
-          float a[6], b[6];
-#pragma unroll
-          for (int t = 0; t < 6; ++t) {
-            a[t] = rw[mr * 6 + t];
-            b[t] = rw[mc * 6 + t];
-          }
-#pragma unroll
-          for (int x = 0; x < 6; ++x)
-#pragma unroll
-            for (int y = 0; y < 6; ++y) h[x * 6 + y] += a[x] * b[y];
-          if (diag) {
-            const double r = A.r_l[off + q];
-#pragma unroll
-            for (int x = 0; x < 6; ++x) gg[x] += (double)a[x] * r;
+        // a regulariser record is involved (they trail each block's range)
+        for (int u = 0; u < (has1 ? 2 : 1); ++u) {
+          const int v = u == 0 ? v0 : v1;
+          if (v < 0) {
+            acc_reg_record(A, v, h, gg);
+            touched = 1;
+          } else {
+            const int cnt = A.s_cnt[v >> 4], off = A.s_off[v >> 4];
+            if (cnt > 0) {
+              float a0[6], b0[6];
+              load_rows(A.rows_l + (size_t)off * 24, (v >> 2) & 3, v & 3, a0, b0);
+              acc_surfel_record(A, v, cnt, off, a0, b0, diag ? __ldg(A.r_l + off) : 0.0, diag, h,
+                                gg);
+              touched = 1;
+            }
           }
         }
       }
@@ -552,48 +639,85 @@ __global__ void __launch_bounds__(256) k_assemble_chunks(AsmArgs A) {
     for (int t = 0; t < 6; ++t) gg[t] += __shfl_xor_sync(0xffffffffu, gg[t], off);
     touched |= __shfl_xor_sync(0xffffffffu, touched, off);
   }
-  if (valid && l == 0) {
-    float4* ph = reinterpret_cast<float4*>(A.part_h + (size_t)chunk * 36);
+  if (!valid) return;
+  if (c1 - c0 == 1) {
+    // single-chunk block (most off-diagonal ones): the partial is final; the
+    // lanes write it straight into the BSR (both triangles) and g
+    const int pu = A.up_pos[ub];
+    const int pm = diag ? -1 : A.up_mpos[ub];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) ph[t] = make_float4(h[4 * t], h[4 * t + 1], h[4 * t + 2], h[4 * t + 3]);
+    for (int t = 0; t < 36; ++t) {
+      if (t % kChunkLanes != l) continue;
+      A.bsr_val[(size_t)pu * 36 + t] = h[t];
+      if (pm >= 0) A.bsr_val[(size_t)pm * 36 + (t % 6) * 6 + t / 6] = h[t];
+    }
+    if (l == 0) {
+      A.bsr_touch[pu] = touched ? 1 : 0;
+      if (pm >= 0) A.bsr_touch[pm] = touched ? 1 : 0;
+    }
+    if (diag) {
+      const int row = key / A.N;
 #pragma unroll
-    for (int t = 0; t < 6; ++t) A.part_g[(size_t)chunk * 6 + t] = gg[t];
-    A.part_t[chunk] = touched;
+      for (int x = 0; x < 6; ++x)
+        if (x == l) A.g[6 * row + x] = gg[x];
+    }
+    return;
   }
+  // multi-chunk block: lanes write the partial (float4 per lane pair)
+  float4* ph = reinterpret_cast<float4*>(A.part_h + (size_t)chunk * 36);
+#pragma unroll
+  for (int t = 0; t < 9; ++t)
+    if (t % kChunkLanes == l) ph[t] = make_float4(h[4 * t], h[4 * t + 1], h[4 * t + 2], h[4 * t + 3]);
+#pragma unroll
+  for (int x = 0; x < 6; ++x)
+    if (x == l) A.part_g[(size_t)chunk * 6 + x] = gg[x];
+  if (l == 0) A.part_t[chunk] = touched;
 }
 
-// thread per upper block: chunk partials in chunk order -> BSR (both triangles), g
-__global__ void k_assemble_finish(AsmArgs A) {
-  const int ub = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ub >= A.n_up) return;
+// multi-chunk blocks only: thread per (block, entry) sums the chunk partials in
+// chunk order (fp64) -> BSR both triangles; entries 36..41 are g of a diagonal
+// block, entry 42 the touched flag
+constexpr int kFinishEntries = 43;
+__global__ void k_assemble_finish(AsmArgs A, const int* __restrict__ multi, const int* __restrict__ n_multi) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int mi = gid / kFinishEntries, t = gid % kFinishEntries;
+  if (mi >= *n_multi) return;
+  const int ub = multi[mi];
   const int key = A.up_key[ub];
   const int row = key / A.N, colb = key % A.N;
   const int c0 = A.chunk_first[ub], c1 = A.chunk_first[ub + 1];
-  int touched = 0;
-  for (int c = c0; c < c1; ++c) touched |= A.part_t[c];
   const int pu = A.up_pos[ub];
   const int pm = row != colb ? A.up_mpos[ub] : -1;
-  for (int t = 0; t < 36; ++t) {
+  if (t < 36) {
     double acc = 0.0;
     for (int c = c0; c < c1; ++c) acc += (double)A.part_h[(size_t)c * 36 + t];
     A.bsr_val[(size_t)pu * 36 + t] = (float)acc;
     if (pm >= 0) A.bsr_val[(size_t)pm * 36 + (t % 6) * 6 + t / 6] = (float)acc;
-  }
-  A.bsr_touch[pu] = touched ? 1 : 0;
-  if (pm >= 0) {
-    A.bsr_touch[pm] = touched ? 1 : 0;
+  } else if (t < 42) {
+    if (pm >= 0) return;
+    double acc = 0.0;
+    for (int c = c0; c < c1; ++c) acc += A.part_g[(size_t)c * 6 + (t - 36)];
+    A.g[6 * row + (t - 36)] = acc;
   } else {
-    for (int x = 0; x < 6; ++x) {
-      double acc = 0.0;
-      for (int c = c0; c < c1; ++c) acc += A.part_g[(size_t)c * 6 + x];
-      A.g[6 * row + x] = acc;
-    }
+    int touched = 0;
+    for (int c = c0; c < c1; ++c) touched |= A.part_t[c];
+    A.bsr_touch[pu] = touched ? 1 : 0;
+    if (pm >= 0) A.bsr_touch[pm] = touched ? 1 : 0;
   }
 }
 
-__global__ void k_chunk_count(const int* __restrict__ up_start, int n_up, int* __restrict__ cnt) {
+__global__ void k_chunk_count(const int* __restrict__ up_start, int n_up, int* __restrict__ cnt,
+                              int* __restrict__ multi_flag) {
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ub < n_up) cnt[ub] = (up_start[ub + 1] - up_start[ub] + kChunk - 1) / kChunk;
+  if (ub >= n_up) return;
+  const int k = (up_start[ub + 1] - up_start[ub] + kChunk - 1) / kChunk;
+  cnt[ub] = k;
+  multi_flag[ub] = k > 1 ? 1 : 0;
+}
+__global__ void k_multi_list(const int* __restrict__ flag, const int* __restrict__ scan, int n_up,
+                             int* __restrict__ list) {
+  const int ub = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ub < n_up && flag[ub]) list[scan[ub]] = ub;
 }
 __global__ void k_chunk_fill(const int* __restrict__ first, int n_up, int* __restrict__ chunk_ub) {
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
@@ -601,45 +725,91 @@ __global__ void k_chunk_fill(const int* __restrict__ first, int n_up, int* __res
   for (int c = first[ub]; c < first[ub + 1]; ++c) chunk_ub[c] = ub;
 }
 
-// ginf, |g|^2, tr(H) (solver.cpp:371, 378)
-__global__ void k_g_stats(const double* __restrict__ g, int dim, const float* __restrict__ val,
-                          const int* __restrict__ diag_pos, int N, DevScalars* __restrict__ sc) {
-  __shared__ double smax[256], ssq[256], str[256];
+// ginf, |g|^2, tr(H) (solver.cpp:371, 378), thread per node; the last block
+// (ticket) combines the block partials in block order. With lm != 0 it also
+// applies the LM floor: mu_floor = 1e-6 tr(H) / dim, mu = max(mu, mu_floor)
+// (solver.cpp:378-379).
+constexpr int kStatsThreads = 256;
+__global__ void __launch_bounds__(kStatsThreads) k_g_stats(
+    const double* __restrict__ g, const float* __restrict__ val, const int* __restrict__ diag_pos,
+    int N, int lm, double* __restrict__ part, unsigned* __restrict__ ticket,
+    DevScalars* __restrict__ sc) {
+  __shared__ double smax[kStatsThreads], ssq[kStatsThreads], str[kStatsThreads];
+  __shared__ bool last;
+  const int tid = threadIdx.x, j = blockIdx.x * kStatsThreads + tid;
   double mx = 0, sq = 0, tr = 0;
-  for (int i = threadIdx.x; i < dim; i += blockDim.x) {
-    const double v = g[i];
-    mx = fmax(mx, fabs(v));
-    sq += v * v;
-  }
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+  if (j < N) {
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      const double v = g[6 * j + t];
+      mx = fmax(mx, fabs(v));
+      sq += v * v;
+    }
     const int d = diag_pos[j];
-    if (d < 0) continue;
-    const float* b = val + (size_t)d * 36;
-    tr += (((((double)b[0] + (double)b[7]) + (double)b[14]) + (double)b[21]) + (double)b[28]) +
-          (double)b[35];
+    if (d >= 0) {
+      const float* b = val + (size_t)d * 36;
+      tr = (((((double)b[0] + (double)b[7]) + (double)b[14]) + (double)b[21]) + (double)b[28]) +
+           (double)b[35];
+    }
   }
-  smax[threadIdx.x] = mx;
-  ssq[threadIdx.x] = sq;
-  str[threadIdx.x] = tr;
+  smax[tid] = mx;
+  ssq[tid] = sq;
+  str[tid] = tr;
   __syncthreads();
-  for (int k = 128; k > 0; k >>= 1) {
-    if (threadIdx.x < k) {
-      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + k]);
-      ssq[threadIdx.x] += ssq[threadIdx.x + k];
-      str[threadIdx.x] += str[threadIdx.x + k];
+  for (int k = kStatsThreads / 2; k > 0; k >>= 1) {
+    if (tid < k) {
+      smax[tid] = fmax(smax[tid], smax[tid + k]);
+      ssq[tid] += ssq[tid + k];
+      str[tid] += str[tid + k];
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    sc->ginf = smax[0];
-    sc->g_sq = ssq[0];  // |g|^2
-    sc->htrace = str[0];
+  if (tid == 0) {
+    part[3 * blockIdx.x + 0] = smax[0];
+    part[3 * blockIdx.x + 1] = ssq[0];
+    part[3 * blockIdx.x + 2] = str[0];
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last || tid != 0) return;
+  __threadfence();
+  double m = 0, q = 0, t = 0;
+  for (int b = 0; b < (int)gridDim.x; ++b) {
+    m = fmax(m, __ldcg(part + 3 * b));
+    q += __ldcg(part + 3 * b + 1);
+    t += __ldcg(part + 3 * b + 2);
+  }
+  sc->ginf = m;
+  sc->g_sq = q;  // |g|^2
+  sc->htrace = t;
+  if (lm) {
+    const double floor_ = 1e-6 * t / (6.0 * N);
+    sc->mu_floor = floor_;
+    sc->mu = fmax(sc->mu, floor_);
+  }
+  *ticket = 0u;
 }
 
 // ------------------------------------------------------------------- PCG
-constexpr int kPcgThreads = 256;
+// Preconditioned pipelined CG (Ghysels & Vanroose 2014, Alg. 3) with the
+// block-Jacobi preconditioner of solver.cpp:180-214: in exact arithmetic the
+// iterates are those of the reference's PCG; in the kernel each iteration needs
+// ONE grid barrier (the dot products and the SpMV input m = M w are published
+// together) instead of two.
+//
+// One cooperative persistent kernel, one CTA per SM. CTA b owns the contiguous
+// block rows [r0, r1) whose BSR blocks are [nnzb*b/G, nnzb*(b+1)/G) rounded to
+// row boundaries; its matrix slice (fp32 values + columns), the 6x6 inverses
+// and all per-row vectors live in shared memory, so an iteration reads global
+// memory only for the gathered m of the neighbouring nodes (48 B per block) and
+// the grid partials. Slices above the shared-memory budget (very large N) keep
+// the same arithmetic on global scratch. Reductions are fixed-order (thread ->
+// warp -> CTA -> grid); the decomposition depends only on (N, nnzb, G).
+constexpr int kPcgThreads = 512;
 constexpr int kPcgWarps = kPcgThreads / 32;
+constexpr int kPcgSmem = 200 * 1024;
+constexpr int kPcgVecs = 10;  // x r u w m n z q s p
 
 struct PcgArgs {
   const int* row_ptr;
@@ -649,231 +819,414 @@ struct PcgArgs {
   const double* g;
   const double* mu_ptr;  // LM damping lives on the device (graph-replay safe)
   int N;
+  int nnzb;
   int max_iters;
   double tol2;
-  double* x;
-  double* r;
-  double* z;
-  double* p0;
-  double* p1;
-  double* q;
-  double* minv;
-  double* part;
+  double* x;        // solution (6N)
+  double* pub0;     // published u0 / m (even iterations) (6N)
+  double* pub1;     // published m (odd iterations) / classic p_old (6N)
+  double* pub2;     // classic p_new (6N)
+  double* minv;     // fallback scratch (36N)
+  double* vec;      // fallback scratch (kPcgVecs x 6N)
+  double* items;    // fallback SpMV partials (6 nnzb)
+  double* part;     // grid partials, 2 x 4 x G
   DevScalars* sc;
 };
 
-// 6x6 SPD inverse by Cholesky (row-major, in place into out)
-__device__ void spd_inverse6(const double* a, double* out) {
-  double L[6][6];
+// Gauss-Jordan inverse of a 6x6 SPD block by an aligned 8-lane group: lane lr
+// (< 6) holds row lr of A in a[] and returns row lr of A^-1 in b[]. A pivot
+// that is not > 0 (the block is not SPD in its fp32-rounded form) makes the
+// group fall back to the inverse diagonal, like the reference's LDLT guard.
+__device__ __forceinline__ void gj_inverse6(double a[6], double b[6], int lr) {
+  const int base = (threadIdx.x & 31) & ~7;
+  const double diag_lr = lr < 6 ? a[lr < 6 ? lr : 0] : 1.0;
+#pragma unroll
+  for (int t = 0; t < 6; ++t) b[t] = (t == lr) ? 1.0 : 0.0;
   bool ok = true;
-  for (int i = 0; i < 6; ++i)
-    for (int j = 0; j <= i; ++j) {
-      double s = a[i * 6 + j];
-      for (int k = 0; k < j; ++k) s -= L[i][k] * L[j][k];
-      if (i == j) {
-        if (!(s > 0.0)) {
-          ok = false;
-          s = 1.0;
-        }
-        L[i][i] = sqrt(s);
-      } else {
-        L[i][j] = s / L[j][j];
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {
+    double ap[6], bp[6];
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      ap[t] = __shfl_sync(0xffffffffu, a[t], base + p);
+      bp[t] = __shfl_sync(0xffffffffu, b[t], base + p);
+    }
+    const double piv = ap[p];
+    if (!(piv > 0.0)) ok = false;
+    if (lr == p) {
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        a[t] = ap[t] / piv;
+        b[t] = bp[t] / piv;
+      }
+    } else {
+      const double f = a[p] / piv;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        a[t] = a[t] - f * ap[t];
+        b[t] = b[t] - f * bp[t];
       }
     }
-  if (!ok) {  // not SPD in fp32-rounded form: fall back to the inverse diagonal
-    for (int i = 0; i < 36; ++i) out[i] = 0.0;
-    for (int i = 0; i < 6; ++i) out[i * 6 + i] = a[i * 6 + i] > 0 ? 1.0 / a[i * 6 + i] : 0.0;
-    return;
   }
-  double Li[6][6];  // inverse of L (lower)
-  for (int i = 0; i < 6; ++i) {
-    for (int j = 0; j < 6; ++j) Li[i][j] = 0.0;
-    Li[i][i] = 1.0 / L[i][i];
-    for (int j = 0; j < i; ++j) {
-      double s = 0.0;
-      for (int k = j; k < i; ++k) s -= L[i][k] * Li[k][j];
-      Li[i][j] = s / L[i][i];
-    }
+  if (!ok) {
+#pragma unroll
+    for (int t = 0; t < 6; ++t) b[t] = (t == lr && diag_lr > 0.0) ? 1.0 / diag_lr : 0.0;
   }
-  for (int i = 0; i < 6; ++i)
-    for (int j = 0; j < 6; ++j) {
-      double s = 0.0;
-      for (int k = max(i, j); k < 6; ++k) s += Li[k][i] * Li[k][j];
-      out[i * 6 + j] = s;
-    }
 }
 
-__device__ __forceinline__ double block_sum_fixed(double v, double* sh) {
-  // warp then block sum in a fixed order; result valid in all threads
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-  const int wid = threadIdx.x >> 5;
+// fixed-order CTA sums of three values; results valid in every thread
+__device__ __forceinline__ void cta_sum3(double& a, double& b, double& c, double4* sh) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+    c += __shfl_xor_sync(0xffffffffu, c, off);
+  }
   __syncthreads();
-  if ((threadIdx.x & 31) == 0) sh[wid] = v;
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = make_double4(a, b, c, 0.0);
   __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < kPcgWarps; ++w) t += sh[w];
-  return t;
+  double ta = 0.0, tb = 0.0, tc = 0.0;
+#pragma unroll
+  for (int w = 0; w < kPcgWarps; ++w) {
+    const double4 v = sh[w];
+    ta += v.x;
+    tb += v.y;
+    tc += v.z;
+  }
+  a = ta;
+  b = tb;
+  c = tc;
 }
 
-__device__ __forceinline__ double grid_total(const double* part, int stride, int off, double* sh) {
-  // every block sums the per-block partials in the same order
-  double v = 0.0;
-  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) v += part[b * stride + off];
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < kPcgWarps; ++w) t += sh[w];
-  return t;
-}
-
-__global__ void __launch_bounds__(kPcgThreads) k_pcg(PcgArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double sh[kPcgWarps];
-  __shared__ double hb[kPcgWarps][36];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kPcgWarps + wid, nw = gridDim.x * kPcgWarps;
-  const int N = a.N;
-  const double mu = *a.mu_ptr;
-  // phase 0: block-Jacobi inverse, r = -g, x = 0, z = M^-1 r, p_old = 0
-  double prz = 0.0, prr = 0.0;
-  for (int j = gw; j < N; j += nw) {
-    const int d = a.diag_pos[j];
-    for (int t = lane; t < 36; t += 32) {
-      double v = d >= 0 ? (double)a.val[(size_t)d * 36 + t] : 0.0;
-      if (t % 7 == 0) v += mu;
-      hb[wid][t] = v;
+// grid totals of the 3 partials at part[4 k + 0..2]: warp 0 sums the G
+// partials in a fixed order, identical in every CTA
+__device__ __forceinline__ double4 grid_sum3(const double* part, double4* sh) {
+  if (threadIdx.x < 32) {
+    double va = 0.0, vb = 0.0, vc = 0.0;
+    for (int k = threadIdx.x; k < gridDim.x; k += 32) {
+      const double2 ab = __ldcg(reinterpret_cast<const double2*>(part + 4 * k));
+      va += ab.x;
+      vb += ab.y;
+      vc += __ldcg(part + 4 * k + 2);
     }
-    __syncwarp();
-    if (lane == 0) spd_inverse6(hb[wid], a.minv + (size_t)36 * j);
-    __syncwarp();
-    double rv = 0.0;
-    if (lane < 6) {
-      rv = -a.g[6 * j + lane];
-      a.r[6 * j + lane] = rv;
-      a.x[6 * j + lane] = 0.0;
-      a.p0[6 * j + lane] = 0.0;
-    }
-    double zv = 0.0;
-    for (int k = 0; k < 6; ++k) {
-      const double rk = __shfl_sync(0xffffffffu, rv, k);
-      if (lane < 6) zv += a.minv[(size_t)36 * j + lane * 6 + k] * rk;
-    }
-    if (lane < 6) a.z[6 * j + lane] = zv;
-    double t1 = lane < 6 ? rv * zv : 0.0, t2 = lane < 6 ? rv * rv : 0.0;
+#pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      t1 += __shfl_down_sync(0xffffffffu, t1, off);
-      t2 += __shfl_down_sync(0xffffffffu, t2, off);
+      va += __shfl_xor_sync(0xffffffffu, va, off);
+      vb += __shfl_xor_sync(0xffffffffu, vb, off);
+      vc += __shfl_xor_sync(0xffffffffu, vc, off);
     }
-    if (lane == 0) {
-      prz += t1;
-      prr += t2;
+    if (threadIdx.x == 0) sh[kPcgWarps] = make_double4(va, vb, vc, 0.0);
+  }
+  __syncthreads();
+  return sh[kPcgWarps];
+}
+
+__device__ __forceinline__ int lower_bound_dev(const int* a, int n, int v) {
+  int lo = 0, hi = n;  // first k in [0, n) with a[k] >= v, or n
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// y_own = (H + mu I) v over the CTA's rows, v gathered from the published
+// array `pub` at the column nodes; own part of v in `vown`.
+__device__ __forceinline__ void slice_spmv(const float* V, const int* C, const int* RP, int bb0,
+                                           int nb, int nr, const double* pub, const double* vown,
+                                           double mu, double* IT, double* y) {
+  for (int k = threadIdx.x; k < 2 * nb; k += kPcgThreads) {
+    const int blk = k >> 1, h3 = 3 * (k & 1);
+    const double2* vc = reinterpret_cast<const double2*>(pub + 6 * (size_t)C[blk]);
+    double pv[6];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const double2 u = __ldcg(vc + t);
+      pv[2 * t] = u.x;
+      pv[2 * t + 1] = u.y;
+    }
+    const float* vr = V + 36 * (size_t)blk + 6 * h3;
+#pragma unroll
+    for (int rw = 0; rw < 3; ++rw) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) s += (double)vr[6 * rw + t] * pv[t];
+      IT[6 * (size_t)blk + h3 + rw] = s;
     }
   }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 6 * nr; k += kPcgThreads) {
+    const int i = k / 6, rw = k - 6 * i;
+    const int lb0 = RP[i] - bb0, lb1 = RP[i + 1] - bb0;
+    double tot = 0.0;
+    for (int b = lb0; b < lb1; ++b) tot += IT[6 * (size_t)b + rw];
+    y[k] = tot + mu * vown[k];
+  }
+}
+
+// y_own = M^-1 v_own (block-diagonal: rows are local); v must be complete
+__device__ __forceinline__ void apply_minv(const double* MINV, const double* v, double* y, int nr) {
+  for (int k = threadIdx.x; k < 6 * nr; k += kPcgThreads) {
+    const int i = k / 6, rw = k - 6 * i;
+    const double* mi = MINV + 36 * i + 6 * rw;
+    const double* vi = v + 6 * i;
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < 6; ++t) s += mi[t] * vi[t];
+    y[k] = s;
+  }
+}
+
+// kPipe = true: pipelined recurrences, one grid barrier per iteration (used
+// for a fixed iteration budget, the reference's default). kPipe = false: the
+// classic two-barrier recurrences, whose recursive residual stays close to the
+// true one -- used when PCG runs to a tolerance (attainable accuracy).
+template <bool kPipe>
+__global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double4 sh[kPcgWarps + 1];
+  __shared__ int s_rng[2];
+  const int tid = threadIdx.x, G = gridDim.x, N = a.N;
+  if (tid == 0) {
+    const long long nnzb = a.nnzb;
+    const int t_lo = (int)(nnzb * blockIdx.x / G), t_hi = (int)(nnzb * (blockIdx.x + 1) / G);
+    s_rng[0] = blockIdx.x == 0 ? 0 : lower_bound_dev(a.row_ptr, N + 1, t_lo);
+    s_rng[1] = blockIdx.x == G - 1 ? N : lower_bound_dev(a.row_ptr, N + 1, t_hi);
+  }
+  __syncthreads();
+  const int r0 = min(s_rng[0], N), r1 = max(min(s_rng[1], N), r0);
+  const int nr = r1 - r0, n6 = 6 * nr;
+  const int bb0 = a.row_ptr[r0], nb = a.row_ptr[r1] - bb0;
+  const double mu = *a.mu_ptr;
+  // ---- slice placement: shared memory when it fits, else global scratch
+  const size_t need = (size_t)nr * (36 + 6 * kPcgVecs) * 8 + (size_t)nb * (6 * 8 + 36 * 4 + 4) +
+                      (size_t)(nr + 1) * 4;
+  const bool fits = need <= (size_t)kPcgSmem;
+  double *MINV, *vb, *IT;
+  const float* V;
+  const int* C;
+  const int* RP;
+  if (fits) {
+    double* d = reinterpret_cast<double*>(smem);
+    MINV = d;
+    vb = MINV + 36 * nr;
+    IT = vb + kPcgVecs * n6;
+    float* sv = reinterpret_cast<float*>(IT + 6 * (size_t)nb);
+    int* sc = reinterpret_cast<int*>(sv + 36 * (size_t)nb);
+    int* srp = sc + nb;
+    const float4* gv = reinterpret_cast<const float4*>(a.val + 36 * (size_t)bb0);
+    float4* sv4 = reinterpret_cast<float4*>(sv);
+    for (int k = tid; k < 9 * nb; k += kPcgThreads) sv4[k] = gv[k];
+    for (int k = tid; k < nb; k += kPcgThreads) sc[k] = a.col[bb0 + k];
+    for (int k = tid; k <= nr; k += kPcgThreads) srp[k] = a.row_ptr[r0 + k];
+    V = sv;
+    C = sc;
+    RP = srp;
+  } else {
+    MINV = a.minv + 36 * (size_t)r0;
+    vb = a.vec + (size_t)kPcgVecs * 6 * r0;  // CTA-contiguous carve of the scratch
+    IT = a.items + 6 * (size_t)bb0;
+    V = a.val + 36 * (size_t)bb0;
+    C = a.col + bb0;
+    RP = a.row_ptr + r0;
+  }
+  double* X = vb;
+  double* R = X + n6;
+  double* U = R + n6;  // u (pipelined) / z (classic)
+  double* W = U + n6;
+  double* Mv = W + n6;
+  double* Nv = Mv + n6;
+  double* Zv = Nv + n6;
+  double* Qv = Zv + n6;
+  double* Sv = Qv + n6;
+  double* Pv = Sv + n6;
+  // ---- prologue: block-Jacobi inverses (8-lane Gauss-Jordan per node)
   {
-    const double brz = block_sum_fixed(prz, sh);
-    const double brr = block_sum_fixed(prr, sh);
-    if (threadIdx.x == 0) {
-      a.part[blockIdx.x * 4 + 0] = brz;
-      a.part[blockIdx.x * 4 + 1] = brr;
+    const int grp = tid >> 3, lr = tid & 7;
+    for (int i0 = 0; i0 < nr; i0 += kPcgThreads / 8) {
+      const int i = i0 + grp;
+      double ar[6], br[6];
+      const int d = (i < nr && lr < 6) ? a.diag_pos[r0 + i] : -1;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        double v = d >= 0 ? (double)a.val[(size_t)d * 36 + lr * 6 + t] : 0.0;
+        if (t == lr) v += mu;
+        ar[t] = lr < 6 ? v : 0.0;
+      }
+      gj_inverse6(ar, br, lr);
+      if (i < nr && lr < 6)
+#pragma unroll
+        for (int t = 0; t < 6; ++t) MINV[36 * i + 6 * lr + t] = br[t];
     }
   }
-  grid.sync();
-  double rz = grid_total(a.part, 4, 0, sh);
-  const double rr0 = grid_total(a.part, 4, 1, sh);
-  double rr = rr0, beta = 0.0;
-  double* pold = a.p0;
-  double* pnew = a.p1;
+  // r0 = -g, x0 = 0, recurrence vectors 0
+  for (int k = tid; k < n6; k += kPcgThreads) {
+    R[k] = -a.g[6 * (size_t)r0 + k];
+    X[k] = 0.0;
+    Zv[k] = 0.0;
+    Qv[k] = 0.0;
+    Sv[k] = 0.0;
+    Pv[k] = 0.0;
+  }
+  __syncthreads();
+  // u0 = M^-1 r0, published (pipelined: in the odd buffer, which iteration 0's
+  // m does not overwrite while slower CTAs still gather u0)
+  double* u0pub = kPipe ? a.pub1 : a.pub0;
+  apply_minv(MINV, R, U, nr);
+  for (int k = tid; k < n6; k += kPcgThreads) u0pub[6 * (size_t)r0 + k] = U[k];
+  double rr0 = 0.0, rr = 0.0;
   int it = 0;
-  const int row6 = lane % 6, blk5 = lane / 6;  // lane -> (block slot, row) of 5 blocks x 6 rows
-  for (; it < a.max_iters; ++it) {
-    if (rr == 0.0 || (a.tol2 > 0.0 && rr <= a.tol2 * rr0)) break;
-    // phase A: q = (H + mu I) p_new, p_new = z + beta p_old computed on the fly
-    double ppq = 0.0;
-    for (int j = gw; j < N; j += nw) {
-      const int b0 = a.row_ptr[j], b1 = a.row_ptr[j + 1];
-      double acc = 0.0;
-      for (int bb = b0; bb < b1; bb += 5) {
-        const int b = bb + blk5;
-        if (lane < 30 && b < b1) {
-          const int cidx = a.col[b];
-          const float* vr = a.val + (size_t)b * 36 + row6 * 6;
+  if constexpr (kPipe) {
+    grid.sync();
+    slice_spmv(V, C, RP, bb0, nb, nr, u0pub, U, mu, IT, W);  // w0 = A u0
+    double gamma_old = 0.0, alpha_old = 0.0;
+    for (;; ++it) {
+      __syncthreads();  // W (and R, U) complete
+      // m = M^-1 w (published) + partials (r.u, w.u, r.r)
+      double* pub = (it & 1) ? a.pub1 : a.pub0;
+      double pg = 0.0, pd = 0.0, pr = 0.0;
+      for (int k = tid; k < n6; k += kPcgThreads) {
+        const int i = k / 6, rw = k - 6 * i;
+        const double* mi = MINV + 36 * i + 6 * rw;
+        const double* wi = W + 6 * i;
+        double s = 0.0;
+#pragma unroll
+        for (int t = 0; t < 6; ++t) s += mi[t] * wi[t];
+        Mv[k] = s;
+        pub[6 * (size_t)r0 + k] = s;
+        pg += R[k] * U[k];
+        pd += W[k] * U[k];
+        pr += R[k] * R[k];
+      }
+      cta_sum3(pg, pd, pr, sh);
+      double* part = a.part + 4 * G * (it & 1);
+      if (tid == 0) {
+        part[4 * blockIdx.x + 0] = pg;
+        part[4 * blockIdx.x + 1] = pd;
+        part[4 * blockIdx.x + 2] = pr;
+      }
+      grid.sync();
+      const double4 tot = grid_sum3(part, sh);
+      const double gamma = tot.x, delta = tot.y;
+      rr = tot.z;
+      if (it == 0) rr0 = rr;
+      if (it >= a.max_iters || rr == 0.0 || (a.tol2 > 0.0 && rr <= a.tol2 * rr0)) break;
+      // n = (H + mu I) m  (same k -> thread map in slice_spmv's row pass and below)
+      slice_spmv(V, C, RP, bb0, nb, nr, pub, Mv, mu, IT, Nv);
+      const double beta = it > 0 ? gamma / gamma_old : 0.0;
+      const double alpha = it > 0 ? gamma / (delta - beta * gamma / alpha_old) : gamma / delta;
+      for (int k = tid; k < n6; k += kPcgThreads) {
+        const double z = Nv[k] + beta * Zv[k];
+        const double q = Mv[k] + beta * Qv[k];
+        const double sv = W[k] + beta * Sv[k];
+        const double p = U[k] + beta * Pv[k];
+        Zv[k] = z;
+        Qv[k] = q;
+        Sv[k] = sv;
+        Pv[k] = p;
+        X[k] = X[k] + alpha * p;
+        R[k] = R[k] - alpha * sv;
+        U[k] = U[k] - alpha * q;
+        W[k] = W[k] - alpha * z;
+      }
+      gamma_old = gamma;
+      alpha_old = alpha;
+    }
+  } else {
+    // classic: z = U (published in pub0), p_old / p_new published in pub1 /
+    // pub2; consumers form p = z + beta p_old on the fly
+    double* zpub = a.pub0;
+    double* pold = a.pub1;
+    double* pnew = a.pub2;
+    double pz = 0.0, pr = 0.0, dz = 0.0;
+    for (int k = tid; k < n6; k += kPcgThreads) {
+      pz += R[k] * U[k];
+      pr += R[k] * R[k];
+      pold[6 * (size_t)r0 + k] = 0.0;
+    }
+    cta_sum3(pz, pr, dz, sh);
+    if (tid == 0) {
+      a.part[4 * blockIdx.x + 0] = pz;
+      a.part[4 * blockIdx.x + 1] = pr;
+    }
+    grid.sync();
+    double4 tot = grid_sum3(a.part, sh);
+    double rz = tot.x, beta = 0.0;
+    rr0 = rr = tot.y;
+    for (; it < a.max_iters; ++it) {
+      if (rr == 0.0 || (a.tol2 > 0.0 && rr <= a.tol2 * rr0)) break;
+      // q = (H + mu I) p with p = z + beta p_old gathered at the column nodes
+      for (int k = tid; k < 2 * nb; k += kPcgThreads) {
+        const int blk = k >> 1, h3 = 3 * (k & 1);
+        const int cidx = C[blk];
+        const double2* zc = reinterpret_cast<const double2*>(zpub + 6 * (size_t)cidx);
+        const double2* pc = reinterpret_cast<const double2*>(pold + 6 * (size_t)cidx);
+        double pv[6];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const double2 zz = __ldcg(zc + t), pp = __ldcg(pc + t);
+          pv[2 * t] = zz.x + beta * pp.x;
+          pv[2 * t + 1] = zz.y + beta * pp.y;
+        }
+        const float* vr = V + 36 * (size_t)blk + 6 * h3;
+#pragma unroll
+        for (int rw = 0; rw < 3; ++rw) {
           double s = 0.0;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) {
-            const double pv = a.z[6 * cidx + k] + beta * pold[6 * cidx + k];
-            s += (double)vr[k] * pv;
-          }
-          acc += s;
+          for (int t = 0; t < 6; ++t) s += (double)vr[6 * rw + t] * pv[t];
+          IT[6 * (size_t)blk + h3 + rw] = s;
         }
       }
-      // row total = sum over lanes row6, row6+6, ..., row6+24 (fixed order)
-      double tot = 0.0;
-#pragma unroll
-      for (int k = 0; k < 5; ++k) tot += __shfl_sync(0xffffffffu, acc, (lane % 6) + 6 * k);
-      double pq = 0.0;
-      if (lane < 6) {
-        const double pn = a.z[6 * j + lane] + beta * pold[6 * j + lane];
-        const double qv = tot + mu * pn;
-        pnew[6 * j + lane] = pn;
-        a.q[6 * j + lane] = qv;
-        pq = pn * qv;
+      __syncthreads();
+      double ppq = 0.0, d1 = 0.0, d2 = 0.0;
+      for (int k = tid; k < n6; k += kPcgThreads) {
+        const int i = k / 6, rw = k - 6 * i;
+        const int lb0 = RP[i] - bb0, lb1 = RP[i + 1] - bb0;
+        double t = 0.0;
+        for (int b = lb0; b < lb1; ++b) t += IT[6 * (size_t)b + rw];
+        const double pn = U[k] + beta * Pv[k];
+        const double qv = t + mu * pn;
+        Pv[k] = pn;
+        pnew[6 * (size_t)r0 + k] = pn;
+        Qv[k] = qv;
+        ppq += pn * qv;
       }
-      for (int off = 16; off > 0; off >>= 1) pq += __shfl_down_sync(0xffffffffu, pq, off);
-      if (lane == 0) ppq += pq;
+      cta_sum3(ppq, d1, d2, sh);
+      if (tid == 0) a.part[4 * blockIdx.x + 2] = ppq;
+      grid.sync();
+      tot = grid_sum3(a.part, sh);
+      const double alpha = rz / tot.z;
+      for (int k = tid; k < n6; k += kPcgThreads) {
+        X[k] += alpha * Pv[k];
+        R[k] = R[k] - alpha * Qv[k];
+      }
+      __syncthreads();
+      double prz = 0.0, prr = 0.0, d3 = 0.0;
+      apply_minv(MINV, R, U, nr);
+      for (int k = tid; k < n6; k += kPcgThreads) {
+        zpub[6 * (size_t)r0 + k] = U[k];
+        prz += R[k] * U[k];
+        prr += R[k] * R[k];
+      }
+      cta_sum3(prz, prr, d3, sh);
+      if (tid == 0) {
+        a.part[4 * blockIdx.x + 0] = prz;
+        a.part[4 * blockIdx.x + 1] = prr;
+      }
+      grid.sync();
+      tot = grid_sum3(a.part, sh);
+      beta = tot.x / rz;
+      rz = tot.x;
+      rr = tot.y;
+      double* t = pold;
+      pold = pnew;
+      pnew = t;
     }
-    {
-      const double b = block_sum_fixed(ppq, sh);
-      if (threadIdx.x == 0) a.part[blockIdx.x * 4 + 2] = b;
-    }
-    grid.sync();
-    const double pqt = grid_total(a.part, 4, 2, sh);
-    const double alpha = rz / pqt;
-    // phase B: x += alpha p, r -= alpha q, z = M^-1 r
-    double prz2 = 0.0, prr2 = 0.0;
-    for (int j = gw; j < N; j += nw) {
-      double rv = 0.0;
-      if (lane < 6) {
-        const int i = 6 * j + lane;
-        a.x[i] += alpha * pnew[i];
-        rv = a.r[i] - alpha * a.q[i];
-        a.r[i] = rv;
-      }
-      double zv = 0.0;
-      for (int k = 0; k < 6; ++k) {
-        const double rk = __shfl_sync(0xffffffffu, rv, k);
-        if (lane < 6) zv += a.minv[(size_t)36 * j + lane * 6 + k] * rk;
-      }
-      if (lane < 6) a.z[6 * j + lane] = zv;
-      double t1 = lane < 6 ? rv * zv : 0.0, t2 = lane < 6 ? rv * rv : 0.0;
-      for (int off = 16; off > 0; off >>= 1) {
-        t1 += __shfl_down_sync(0xffffffffu, t1, off);
-        t2 += __shfl_down_sync(0xffffffffu, t2, off);
-      }
-      if (lane == 0) {
-        prz2 += t1;
-        prr2 += t2;
-      }
-    }
-    {
-      const double b1 = block_sum_fixed(prz2, sh);
-      const double b2 = block_sum_fixed(prr2, sh);
-      if (threadIdx.x == 0) {
-        a.part[blockIdx.x * 4 + 0] = b1;
-        a.part[blockIdx.x * 4 + 1] = b2;
-      }
-    }
-    grid.sync();
-    const double rzn = grid_total(a.part, 4, 0, sh);
-    rr = grid_total(a.part, 4, 1, sh);
-    beta = rzn / rz;
-    rz = rzn;
-    double* t = pold;
-    pold = pnew;
-    pnew = t;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  for (int k = tid; k < n6; k += kPcgThreads) a.x[6 * (size_t)r0 + k] = X[k];
+  if (blockIdx.x == 0 && tid == 0) {
     a.sc->pcg_iters = it;
     a.sc->pcg_rr = rr;
     a.sc->pcg_rr0 = rr0;
@@ -990,13 +1343,22 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
   if (c.n_pairs_ok_est <= 0) c.n_pairs_ok_est = 0.4 * c.P;
   // fixed-size record chunks for the assembly (per frame)
   c.n_chunks = 0;
+  c.n_multi = 0;
   if (c.n_up > 0) {
     DS_LAUNCH(c, KK_PATTERN, 12.0 * c.n_up, cdiv(c.n_up, 256), 256, 0, k_chunk_count, c.up_start,
-              c.n_up, c.chunk_first);
+              c.n_up, c.chunk_first, c.multi_flag);
     scan_exclusive(c, c.chunk_first, c.chunk_first, c.n_up);
-    DS_CUDA(cudaMemcpyAsync(&c.n_chunks, c.chunk_first + c.n_up, sizeof(int),
-                            cudaMemcpyDeviceToHost, c.stream));
+    scan_exclusive(c, c.multi_flag, c.multi_scan, c.n_up);
+    DS_LAUNCH(c, KK_PATTERN, 8.0 * c.n_up, cdiv(c.n_up, 256), 256, 0, k_multi_list, c.multi_flag,
+              c.multi_scan, c.n_up, c.multi_list);
+    int hc[2];
+    DS_CUDA(cudaMemcpyAsync(&hc[0], c.chunk_first + c.n_up, sizeof(int), cudaMemcpyDeviceToHost,
+                            c.stream));
+    DS_CUDA(cudaMemcpyAsync(&hc[1], c.multi_scan + c.n_up, sizeof(int), cudaMemcpyDeviceToHost,
+                            c.stream));
     sync(c);
+    c.n_chunks = hc[0];
+    c.n_multi = hc[1];
     if (c.n_chunks > c.CH_cap) fail(DS_ERR_CAPACITY, "assembly chunk capacity exceeded");
     DS_LAUNCH(c, KK_PATTERN, 8.0 * c.n_chunks, cdiv(c.n_up, 256), 256, 0, k_chunk_fill,
               c.chunk_first, c.n_up, c.chunk_ub);
@@ -1015,7 +1377,7 @@ PairParams pair_params(Ctx& c, const double* pose) {
 
 // One GN linearisation at the current nodes (solver.cpp:316-369). Leaves e_data,
 // e_reg, ginf, |g|^2 (in pcg_rr slot) and tr(H) in DevScalars (no host sync).
-void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last) {
+void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor) {
   const int n = c.n_surfels, N = c.n_nodes, P = c.P;
   // only render-eligible surfels can be drawn / paired during the solve; the
   // post-solve forward_warp (pipeline.cpp:108) rewrites every live surfel
@@ -1037,7 +1399,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last) {
   node_se3(c, c.node_dq, c.node_se3);
   const int nbe = cdiv(8 * N, 256);
   DS_LAUNCH(c, KK_ENERGY, 200.0 * N, nbe, 256, 0, k_reg_energy, c.node_pos, c.node_nbr,
-            c.node_se3, N, c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg_pre);
+            c.node_se3, N, c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg_pre, c.reg_ab);
   DS_CUDA(cudaMemsetAsync(c.g, 0, sizeof(double) * 6 * N, c.stream));
   AsmArgs A;
   A.up_key = c.up_key;
@@ -1054,6 +1416,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last) {
   A.node_pos = c.node_pos;
   A.nbr = c.node_nbr;
   A.se3 = c.node_se3;
+  A.reg_ab = c.reg_ab;
   A.lambda = c.cfg.lambda;
   A.N = N;
   A.n_up = c.n_up;
@@ -1072,15 +1435,18 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last) {
                          144.0 * c.n_full + 48.0 * N;
     DS_LAUNCH(c, KK_BLOCK_ASSEMBLY, bytes, cdiv((long long)c.n_chunks * kChunkLanes, 256), 256, 0,
               k_assemble_chunks, A);
-    DS_LAUNCH(c, KK_BLOCK_ASSEMBLY, 0.0, cdiv(c.n_up, 128), 128, 0, k_assemble_finish, A);
+    if (c.n_multi > 0)
+      DS_LAUNCH(c, KK_BLOCK_ASSEMBLY, 0.0, cdiv((long long)c.n_multi * kFinishEntries, 256), 256, 0,
+                k_assemble_finish, A, c.multi_list, c.multi_scan + c.n_up);
   }
-  DS_LAUNCH(c, KK_REDUCE, 48.0 * N, 1, 256, 0, k_g_stats, c.g, 6 * N, c.bsr_val, c.diag_pos, N,
+  DS_LAUNCH(c, KK_REDUCE, 48.0 * N + 24.0 * N, std::max(1, cdiv(N, kStatsThreads)), kStatsThreads, 0,
+            k_g_stats, c.g, c.bsr_val, c.diag_pos, N, lm_floor ? 1 : 0, c.gst_part, c.tickets + 2,
             c.dsc);
 }
 
 void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_pre, int* n_pairs) {
   if (!c.pattern_ready) build_pattern(c, t_now, t_last);
-  gn_linearize_async(c, pose, t_now, t_last);
+  gn_linearize_async(c, pose, t_now, t_last, false);
   fetch_scalars(c);
   if (e_pre) *e_pre = c.hsc->e_data_pre + c.cfg.lambda * c.hsc->e_reg_pre;
   if (n_pairs) *n_pairs = c.hsc->n_pairs;
@@ -1097,23 +1463,24 @@ void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   a.g = c.g;
   a.mu_ptr = &c.dsc->mu;
   a.N = N;
+  a.nnzb = c.n_full;
   a.max_iters = max_iters;
   a.tol2 = tol > 0 ? tol * tol : 0.0;
   a.x = c.pcg_x;
-  a.r = c.pcg_r;
-  a.z = c.pcg_z;
-  a.p0 = c.pcg_p0;
-  a.p1 = c.pcg_p1;
-  a.q = c.pcg_q;
+  a.pub0 = c.pcg_p0;
+  a.pub1 = c.pcg_p1;
+  a.pub2 = c.pcg_p2;
   a.minv = c.pcg_minv;
+  a.vec = c.pcg_vec;
+  a.items = c.pcg_items;
   a.part = c.pcg_part;
   a.sc = c.dsc;
-  const int need = std::max(1, cdiv(N, kPcgWarps));
-  const int grid = std::min(c.pcg_grid, need);
+  // a CTA per SM; small systems use fewer CTAs (cheaper grid barriers)
+  const int grid = std::min(c.pcg_grid, std::max(1, cdiv(c.n_full, 64)));
   void* args[] = {&a};
   launch_begin(c, KK_PCG);
-  DS_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, dim3(grid), dim3(kPcgThreads), args, 0,
-                                      c.stream));
+  void* fn = a.tol2 > 0.0 ? (void*)k_pcg<false> : (void*)k_pcg<true>;
+  DS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPcgThreads), args, kPcgSmem, c.stream));
   // algorithmic bytes per PCG: per iteration one BSR SpMV (148 B/block + vectors)
   launch_end(c, KK_PCG, std::max(1, max_iters) * (148.0 * c.n_full + 6.0 * 8 * 8 * N));
   DS_CUDA(cudaMemsetAsync(&c.dsc->finite, 0xff, sizeof(int), c.stream));
@@ -1142,22 +1509,14 @@ void energy_async(Ctx& c, const double* pose, const double4* dq, double* se3) {
             &c.dsc->e_data);
   node_se3(c, dq, se3);
   DS_LAUNCH(c, KK_ENERGY, 200.0 * N, nbe, 256, 0, k_reg_energy, c.node_pos, c.node_nbr, se3, N,
-            c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg);
+            c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg, (double*)nullptr);
 }
 }  // namespace
 
 namespace {
-__global__ void k_lm_prep(DevScalars* sc, int dim) {
-  // mu_floor = 1e-6 tr(H) / dim; mu = max(mu, mu_floor)   (solver.cpp:378-379)
-  const double floor_ = 1e-6 * sc->htrace / dim;
-  sc->mu_floor = floor_;
-  sc->mu = fmax(sc->mu, floor_);
-}
-
 // one GN iteration up to the first LM attempt: linearise, mu, PCG, candidate, E_post
 void gn_step_async(Ctx& c, const double* pose, int t_now, int t_last, int max_pcg, double tol) {
-  gn_linearize_async(c, pose, t_now, t_last);
-  DS_LAUNCH(c, KK_MISC, 32.0, 1, 1, 0, k_lm_prep, c.dsc, 6 * c.n_nodes);
+  gn_linearize_async(c, pose, t_now, t_last, true);  // + LM floor on mu
   pcg_solve_async(c, max_pcg, tol);
   apply_increments(c, c.pcg_x, c.node_dq_cand);
   energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
@@ -1328,8 +1687,12 @@ double bsr_spmv(Ctx& c, const double* x_dev, double* y_dev, double mu, int reps)
 }
 
 int pcg_max_grid(int num_sms) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg, kPcgThreads, 0);
+  DS_CUDA(cudaFuncSetAttribute(k_pcg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcgSmem));
+  DS_CUDA(cudaFuncSetAttribute(k_pcg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcgSmem));
+  int per_sm = 0, per_sm2 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg<true>, kPcgThreads, kPcgSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_pcg<false>, kPcgThreads, kPcgSmem);
+  per_sm = std::min(per_sm, per_sm2);
   return std::max(1, per_sm) * num_sms;
 }
 

@@ -1,0 +1,77 @@
+"""PCG iterates of the device solver against the reference algorithm restated
+in numpy (solver.cpp:180-214: block-Jacobi preconditioned CG on (H + mu I) x =
+-g, x0 = 0), on a system assembled by the device from a synthetic frame pair.
+
+The device runs the classic two-barrier recurrences when a tolerance is set
+and the pipelined one-barrier recurrences for a fixed iteration budget; both
+must reproduce the reference iterates after k iterations up to fp64 rounding
+(relative 1e-8 on x, tolerance written here; the matrix is the same fp32 BSR).
+"""
+import numpy as np
+import pytest
+
+import harness as Hh
+
+pytestmark = pytest.mark.gpu
+pkg = pytest.importorskip("paper_1904_13073_b200")
+
+
+def reference_pcg(H, g, mu, iters):
+    """solver.cpp:180-214 restated: z = M^-1 r with 6x6 diagonal-block inverses."""
+    n = H.shape[0]
+    A = H + mu * np.eye(n)
+    Minv = np.zeros_like(A)
+    for j in range(n // 6):
+        s = slice(6 * j, 6 * j + 6)
+        Minv[s, s] = np.linalg.inv(A[s, s])
+    x = np.zeros(n)
+    r = -g.copy()
+    z = Minv @ r
+    p = z.copy()
+    rz = r @ z
+    for _ in range(iters):
+        q = A @ p
+        alpha = rz / (p @ q)
+        x += alpha * p
+        r -= alpha * q
+        z = Minv @ r
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x
+
+
+@pytest.fixture(scope="module")
+def system():
+    cfg = pkg.camera_config(160, 120, 140.0, pcg_max_iters=10)
+    seq = pkg.SyntheticSequence("bending_sheet", 10, cfg)
+    ctx = pkg.Context(cfg)
+    ctx.process_frame(seq.render_depth(0), 0)
+    ctx.frame_maps(seq.render_depth(2), 2)
+    ne = ctx.build_normal_equations(np.eye(3).reshape(9).tolist() + [0.0, 0.0, 0.0], 2, 0)
+    N = ctx.num_nodes()
+    H, _ = Hh.bsr_to_dense(ne, N)
+    yield ctx, H, ne["g"].copy()
+    ctx.close()
+
+
+@pytest.mark.parametrize("iters", [1, 2, 5, 10])
+@pytest.mark.parametrize("mode", ["pipelined", "classic"])
+def test_pcg_iterates_match_reference(system, iters, mode):
+    ctx, H, g = system
+    mu = 1e-6 * np.trace(H) / H.shape[0] * 10.0
+    tol = 0.0 if mode == "pipelined" else 1e-150  # tol > 0 selects the classic recurrences
+    x, it, _ = ctx.pcg_solve(mu, iters, tol)
+    ref = reference_pcg(H, g, mu, iters)
+    assert it == iters
+    err = np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-300)
+    assert err < 1e-8, (mode, iters, err)
+
+
+def test_pcg_converges_to_direct_solve(system):
+    ctx, H, g = system
+    mu = 1e-3 * np.trace(H) / H.shape[0]
+    x, it, rel = ctx.pcg_solve(mu, 5000, 1e-12)
+    ref = np.linalg.solve(H + mu * np.eye(H.shape[0]), -g)
+    assert rel <= 1e-12 and it < 5000
+    assert np.abs(x - ref).max() / np.abs(ref).max() < 1e-8

@@ -189,8 +189,10 @@ void allocate(Ctx& c) {
   c.pair_r = dalloc<double>(c, P);
   c.s_cnt = dalloc<int>(c, S + 1);
   c.s_off = dalloc<int>(c, S + 1);
-  c.s_cur = dalloc<int>(c, S + 1);
-  c.s_list = dalloc<int>(c, P);
+  c.pkey = dalloc<int>(c, P);
+  c.pval = dalloc<int>(c, P);
+  c.pkey2 = dalloc<int>(c, P);
+  c.pval2 = dalloc<int>(c, P);
   c.rec_key = dalloc<int>(c, c.R_cap);
   c.rec_val = dalloc<int>(c, c.R_cap);
   c.rec_key2 = dalloc<int>(c, c.R_cap);
@@ -219,7 +221,7 @@ void allocate(Ctx& c) {
   c.rows_l = dalloc<float>(c, P * 24);
   c.elig = dalloc<int>(c, S);
   c.r_l = dalloc<double>(c, P);
-  c.cub_tmp_bytes = sort_temp_bytes(c.R_cap);
+  c.cub_tmp_bytes = std::max(sort_temp_bytes(c.R_cap), sort_temp_bytes(P));
   c.cub_tmp = dalloc<char>(c, c.cub_tmp_bytes);
   c.g = dalloc<double>(c, 6 * N);
   c.pcg_x = dalloc<double>(c, 6 * N);

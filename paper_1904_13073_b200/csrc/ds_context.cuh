@@ -154,8 +154,10 @@ struct Ctx {
   double* pair_r = nullptr;
   int* s_cnt = nullptr;
   int* s_off = nullptr;
-  int* s_cur = nullptr;
-  int* s_list = nullptr;
+  int* pkey = nullptr;  // per pixel (surfel, pixel) sort keys / values
+  int* pval = nullptr;
+  int* pkey2 = nullptr;
+  int* pval2 = nullptr;
   // term -> block records and BSR
   int* rec_key = nullptr;
   int* rec_val = nullptr;
@@ -280,7 +282,7 @@ void clear_scalars(Ctx& c);
 // exclusive scan of n ints: out[0..n] (out[n] = total). in may alias out only if n+1 storage.
 void scan_exclusive(Ctx& c, const int* in, int* out, int n);
 void sort_pairs(Ctx& c, int* keys, int* vals, int* keys_alt, int* vals_alt, int n, int end_bit,
-                int** keys_out, int** vals_out);
+                int** keys_out, int** vals_out, int kind = KK_PATTERN);
 // fixed-order deterministic sum of `n` partials into dst (device)
 void reduce_partials(Ctx& c, const double* part, int n, double* dst, int mode);
 

@@ -103,12 +103,12 @@ void scan_exclusive(Ctx& c, const int* in, int* out, int n) {
 }
 
 void sort_pairs(Ctx& c, int* keys, int* vals, int* keys_alt, int* vals_alt, int n, int end_bit,
-                int** keys_out, int** vals_out) {
+                int** keys_out, int** vals_out, int kind) {
   cub::DoubleBuffer<int> dk(keys, keys_alt), dv(vals, vals_alt);
   size_t bytes = c.cub_tmp_bytes;
-  launch_begin(c, KK_PATTERN);
+  launch_begin(c, kind);
   DS_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp, bytes, dk, dv, n, 0, end_bit, c.stream));
-  launch_end(c, KK_PATTERN, 16.0 * n);
+  launch_end(c, kind, 16.0 * n * ((end_bit + 7) / 8));
   *keys_out = dk.Current();
   *vals_out = dv.Current();
 }

@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
                                                     PairParams pp, uint8_t* __restrict__ pair_ok,
                                                     float* __restrict__ rows,
                                                     double* __restrict__ pair_r,
-                                                    int* __restrict__ s_cnt,
+                                                    int* __restrict__ pkey,
+                                                    int* __restrict__ pval, int sentinel,
                                                     double* __restrict__ part,
                                                     unsigned* __restrict__ ticket,
                                                     double* __restrict__ out) {
@@ -147,8 +148,11 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
       }
       pair_r[c] = r;
       pair_ok[c] = 1;
-      atomicAdd(s_cnt + s, 1);
     }
+  }
+  if (c < pp.P) {  // (surfel, pixel) sort keys of the per-surfel pair lists
+    pkey[c] = (s >= 0 && pair_ok[c]) ? s : sentinel;
+    pval[c] = c;
   }
   grid_sum<256>(e, part, ticket, out);  // data energy, fixed order
 }
@@ -227,46 +231,31 @@ __global__ void k_any_stable_flag(const float4* __restrict__ ln, int n, double d
 }
 
 // ---------------------------------------------------------------- pair lists
-__global__ void k_scatter_pairs(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
-                                int P, const int* __restrict__ s_off, int* __restrict__ s_cur,
-                                int* __restrict__ s_list) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= P) return;
-  const int s = pair_s[c];
-  if (s < 0 || !pair_ok[c]) return;
-  const int k = atomicAdd(s_cur + s, 1);
-  s_list[s_off[s] + k] = c;
-}
-// Sort each surfel's pair list into pixel order (deterministic summation order)
-// and gather the pairs' Jacobian rows / residuals into list order, so the block
+// After the (surfel, pixel) radix sort (stable: pixel order within a surfel),
+// thread per sorted slot: run heads record (offset, count) and every slot
+// gathers its pair's Jacobian rows / residual into list order, so the block
 // assembly reads one contiguous run per surfel.
-__global__ void k_sort_lists(const int* __restrict__ s_cnt, const int* __restrict__ s_off, int n,
-                             int* __restrict__ s_list, const float* __restrict__ rows,
-                             const double* __restrict__ pair_r, float* __restrict__ rows_l,
-                             double* __restrict__ r_l) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const int cnt = s_cnt[s];
-  if (cnt == 0) return;
-  const int off = s_off[s];
-  int* l = s_list + off;
-  for (int a = 1; a < cnt; ++a) {
-    const int v = l[a];
-    int b = a;
-    while (b > 0 && l[b - 1] > v) {
-      l[b] = l[b - 1];
-      --b;
-    }
-    l[b] = v;
+__global__ void k_pair_runs(const int* __restrict__ key, const int* __restrict__ val, int P,
+                            int sentinel, const float* __restrict__ rows,
+                            const double* __restrict__ pair_r, int* __restrict__ s_cnt,
+                            int* __restrict__ s_off, float* __restrict__ rows_l,
+                            double* __restrict__ r_l) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P) return;
+  const int s = key[k];
+  if (s == sentinel) return;
+  if (k == 0 || key[k - 1] != s) {
+    int cnt = 1;
+    while (k + cnt < P && key[k + cnt] == s) ++cnt;
+    s_off[s] = k;
+    s_cnt[s] = cnt;
   }
-  for (int q = 0; q < cnt; ++q) {
-    const int pix = l[q];
-    const float4* src = reinterpret_cast<const float4*>(rows + (size_t)pix * 24);
-    float4* dst = reinterpret_cast<float4*>(rows_l + (size_t)(off + q) * 24);
+  const int pix = val[k];
+  const float4* src = reinterpret_cast<const float4*>(rows + (size_t)pix * 24);
+  float4* dst = reinterpret_cast<float4*>(rows_l + (size_t)k * 24);
 #pragma unroll
-    for (int t = 0; t < 6; ++t) dst[t] = src[t];
-    r_l[off + q] = pair_r[pix];
-  }
+  for (int t = 0; t < 6; ++t) dst[t] = src[t];
+  r_l[k] = pair_r[pix];
 }
 
 // ------------------------------------------------------------ block pattern
@@ -1233,36 +1222,62 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
   }
 }
 
-// Standalone BSR SpMV y = (H + mu I) x, the PCG's SpMV phase as its own kernel
-// (warp per block row; lanes = 5 blocks x 6 rows, shuffle row reduction).
-// Algorithmic bytes: 144 B per block (fp32 6x6) + 4 B column index + the x
-// block (48 B, L1/L2-reused) + row pointers and y (48 B per row).
-__global__ void __launch_bounds__(256) k_bsr_spmv(const int* __restrict__ row_ptr,
-                                                  const int* __restrict__ col,
-                                                  const float* __restrict__ val, int N, double mu,
-                                                  const double* __restrict__ x,
-                                                  double* __restrict__ y) {
+// Standalone BSR SpMV y = (H + mu I) x (the PCG's SpMV as its own kernel, for
+// systems streamed from HBM). Warp per block row: one coalesced load brings
+// the column indices of up to 5 G blocks of the row (lane i <- block i), then
+// lanes = 5 blocks x 6 rows issue, for G groups of 5 blocks at once, the fp32
+// value rows (float2) and the gathered x blocks (double2) before any product.
+// Shuffle row reduction; block order within a lane is fixed (deterministic).
+// Algorithmic bytes: 144 B per block + 4 B column index; row pointers + own x
+// + y = 56 B per row; neighbour x blocks are L2-resident gathers.
+// Measured (ncu, cold L2, N = 16k, 254k blocks): G = 2 beats G = 3, 4 (register
+// growth costs more occupancy than the extra loads in flight buy) and beats
+// TMA-staged tiles (the per-tile row search / staging adds a dependent round
+// trip per row).
+template <int kSpmvGroups>
+__global__ void __launch_bounds__(256) k_bsr_spmv_rows(const int* __restrict__ row_ptr,
+                                                       const int* __restrict__ col,
+                                                       const float* __restrict__ val, int N,
+                                                       double mu, const double* __restrict__ x,
+                                                       double* __restrict__ y) {
   const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= N) return;
-  const int row6 = lane % 6, blk5 = lane / 6;
+  const int rw = lane % 6, blk5 = lane / 6;
   const int b0 = row_ptr[j], b1 = row_ptr[j + 1];
   double acc = 0.0;
-  for (int bb = b0; bb < b1; bb += 5) {
-    const int b = bb + blk5;
-    if (lane < 30 && b < b1) {
-      const int cidx = col[b];
-      const float* vr = val + (size_t)b * 36 + row6 * 6;
-      const double* xc = x + 6 * cidx;
-      double s = 0.0;
+  for (int w0 = b0; w0 < b1; w0 += 5 * kSpmvGroups) {
+    const int nbw = min(5 * kSpmvGroups, b1 - w0);
+    const int cl = lane < nbw ? __ldcs(col + w0 + lane) : 0;
+    float2 f[kSpmvGroups][3];
+    double2 xv[kSpmvGroups][3];
 #pragma unroll
-      for (int k = 0; k < 6; ++k) s += (double)vr[k] * xc[k];
-      acc += s;
+    for (int g = 0; g < kSpmvGroups; ++g) {
+      const int bi = g * 5 + blk5;
+      const bool ok = lane < 30 && bi < nbw;
+      const int cidx = __shfl_sync(0xffffffffu, cl, bi);
+      const float2* vr = reinterpret_cast<const float2*>(val + (size_t)(w0 + bi) * 36 + rw * 6);
+      const double2* xc = reinterpret_cast<const double2*>(x + 6 * (size_t)cidx);
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        f[g][t] = ok ? __ldcs(vr + t) : make_float2(0.f, 0.f);
+        xv[g][t] = ok ? __ldg(xc + t) : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kSpmvGroups; ++g) {
+      double sg = 0.0;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        sg += (double)f[g][t].x * xv[g][t].x;
+        sg += (double)f[g][t].y * xv[g][t].y;
+      }
+      acc += sg;
     }
   }
   double tot = 0.0;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) tot += __shfl_sync(0xffffffffu, acc, (lane % 6) + 6 * k);
+  for (int k = 0; k < 5; ++k) tot += __shfl_sync(0xffffffffu, acc, rw + 6 * k);
   if (lane < 6) y[6 * j + lane] = tot + mu * x[6 * j + lane];
 }
 
@@ -1307,7 +1322,7 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
               N, key + (size_t)n * 10, val + (size_t)n * 10);
   const int end_bit = 31;  // the kIntMax sentinel needs all 31 bits
   int *ks, *vs;
-  sort_pairs(c, key, val, c.rec_key2, c.rec_val2, R, end_bit, &ks, &vs);
+  sort_pairs(c, key, val, c.rec_key2, c.rec_val2, R, end_bit, &ks, &vs, KK_PATTERN);
   // keep the sorted arrays in rec_key/rec_val
   if (ks != c.rec_key) {
     std::swap(c.rec_key, c.rec_key2);
@@ -1386,16 +1401,16 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   DS_CUDA(cudaMemsetAsync(c.s_cnt, 0, sizeof(int) * (n + 1), c.stream));
   DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
   const int nbp = cdiv(P, 256);
-  // per pixel: pair id 4 B, surfel ref + skin 48 B, frame maps 64 B, rows 96 B + r 8 B out
-  DS_LAUNCH(c, KK_PAIR_TERMS, 220.0 * P, nbp, 256, 0, k_pair_terms, c.pair_s, c.M(), c.node_dq,
-            c.f_vert, c.f_nrm, pair_params(c, pose), c.pair_ok, c.pair_rows, c.pair_r, c.s_cnt,
-            c.red_part, c.tickets + 0, &c.dsc->e_data_pre);
-  scan_exclusive(c, c.s_cnt, c.s_off, n);
-  DS_CUDA(cudaMemsetAsync(c.s_cur, 0, sizeof(int) * n, c.stream));
-  DS_LAUNCH(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_scatter_pairs, c.pair_s, c.pair_ok, P,
-            c.s_off, c.s_cur, c.s_list);
-  DS_LAUNCH(c, KK_PAIR_LISTS, 112.0 * P * 0.5, cdiv(n, 256), 256, 0, k_sort_lists, c.s_cnt,
-            c.s_off, n, c.s_list, c.pair_rows, c.pair_r, c.rows_l, c.r_l);
+  const int bits = n > 0 ? 32 - __builtin_clz((unsigned)n) : 1;  // 2^bits > n
+  const int sentinel = (int)((1u << bits) - 1u);
+  // per pixel: pair id 4 B, surfel ref + skin 48 B, frame maps 64 B, rows 96 B + r 8 B + keys 8 B out
+  DS_LAUNCH(c, KK_PAIR_TERMS, 228.0 * P, nbp, 256, 0, k_pair_terms, c.pair_s, c.M(), c.node_dq,
+            c.f_vert, c.f_nrm, pair_params(c, pose), c.pair_ok, c.pair_rows, c.pair_r, c.pkey,
+            c.pval, sentinel, c.red_part, c.tickets + 0, &c.dsc->e_data_pre);
+  int *ks, *vs;
+  sort_pairs(c, c.pkey, c.pval, c.pkey2, c.pval2, P, bits, &ks, &vs, KK_PAIR_LISTS);
+  DS_LAUNCH(c, KK_PAIR_LISTS, 8.0 * P + 112.0 * c.n_pairs_ok_est, nbp, 256, 0, k_pair_runs, ks, vs,
+            P, sentinel, c.pair_rows, c.pair_r, c.s_cnt, c.s_off, c.rows_l, c.r_l);
   node_se3(c, c.node_dq, c.node_se3);
   const int nbe = cdiv(8 * N, 256);
   DS_LAUNCH(c, KK_ENERGY, 200.0 * N, nbe, 256, 0, k_reg_energy, c.node_pos, c.node_nbr,
@@ -1675,8 +1690,8 @@ double bsr_spmv(Ctx& c, const double* x_dev, double* y_dev, double mu, int reps)
   const double bytes = 148.0 * c.n_full + 56.0 * N;
   DS_CUDA(cudaEventRecord(a, c.stream));
   for (int r = 0; r < reps; ++r)
-    DS_LAUNCH(c, KK_PCG, bytes, cdiv((long long)N * 32, 256), 256, 0, k_bsr_spmv, c.row_ptr,
-              c.bsr_col, c.bsr_val, N, mu, x_dev, y_dev);
+    DS_LAUNCH(c, KK_PCG, bytes, cdiv((long long)N * 32, 256), 256, 0, k_bsr_spmv_rows<2>,
+              c.row_ptr, c.bsr_col, c.bsr_val, N, mu, x_dev, y_dev);
   DS_CUDA(cudaEventRecord(b, c.stream));
   sync(c);
   float ms = 0;

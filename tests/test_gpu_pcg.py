@@ -75,3 +75,13 @@ def test_pcg_converges_to_direct_solve(system):
     ref = np.linalg.solve(H + mu * np.eye(H.shape[0]), -g)
     assert rel <= 1e-12 and it < 5000
     assert np.abs(x - ref).max() / np.abs(ref).max() < 1e-8
+
+
+def test_bsr_spmv_matches_dense(system):
+    ctx, H, g = system
+    x = np.random.default_rng(3).normal(size=H.shape[0])
+    mu = 0.25
+    y, ms = ctx.bsr_spmv(x, mu, 2)
+    ref = H @ x + mu * x
+    assert ms > 0
+    assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max() + 1e-300

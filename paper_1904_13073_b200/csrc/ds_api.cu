@@ -188,11 +188,11 @@ void allocate(Ctx& c) {
   c.pair_rows = dalloc<float>(c, P * 24);
   c.pair_r = dalloc<double>(c, P);
   c.s_cnt = dalloc<int>(c, S + 1);
-  c.s_off = dalloc<int>(c, S + 1);
-  c.pkey = dalloc<int>(c, P);
-  c.pval = dalloc<int>(c, P);
-  c.pkey2 = dalloc<int>(c, P);
-  c.pval2 = dalloc<int>(c, P);
+  c.s_head = dalloc<int>(c, S + 1);
+  c.s_base = dalloc<int>(c, S + 1);
+  c.s_fill = dalloc<int>(c, S + 1);
+  c.p_list = dalloc<int>(c, P);
+  c.p_next = dalloc<int>(c, P);
   c.rec_key = dalloc<int>(c, c.R_cap);
   c.rec_val = dalloc<int>(c, c.R_cap);
   c.rec_key2 = dalloc<int>(c, c.R_cap);
@@ -218,9 +218,7 @@ void allocate(Ctx& c) {
   c.part_h = dalloc<float>(c, (size_t)c.CH_cap * 36);
   c.part_g = dalloc<double>(c, (size_t)c.CH_cap * 6);
   c.part_t = dalloc<int>(c, c.CH_cap);
-  c.rows_l = dalloc<float>(c, P * 24);
   c.elig = dalloc<int>(c, S);
-  c.r_l = dalloc<double>(c, P);
   c.cub_tmp_bytes = std::max(sort_temp_bytes(c.R_cap), sort_temp_bytes(P));
   c.cub_tmp = dalloc<char>(c, c.cub_tmp_bytes);
   c.g = dalloc<double>(c, 6 * N);
@@ -240,6 +238,7 @@ void allocate(Ctx& c) {
     if (g > 0) c.pcg_grid = std::min(c.pcg_grid, g);
   }
   c.pcg_part = dalloc<double>(c, 8 * (size_t)c.pcg_grid);
+  c.pcg_slices = dalloc<int>(c, 4 * (size_t)c.pcg_grid + 4);
   c.cand_flag = dalloc<int>(c, P + 1);
   c.cand_scan = dalloc<int>(c, P + 1);
   c.cand_pix = dalloc<int>(c, P);

@@ -82,7 +82,7 @@ struct DevScalars {
   int n_nodes, n_new_nodes, err, finite;
   int up_blocks, full_blocks, pcg_iters, mean_cnt;
   int rigid_pairs, rigid_low, n_records, survivors;
-  int rmax_bits, _pad_sc;
+  int rmax_bits, pair_list_n;
   double e_data, e_reg, ginf, htrace;
   double e_data_pre, e_reg_pre, g_sq, mu, mu_floor;
   double pcg_rr, pcg_rr0, mean_abs_r, rigid_abs;
@@ -153,11 +153,11 @@ struct Ctx {
   float* pair_rows = nullptr;  // per pixel 4 x 6
   double* pair_r = nullptr;
   int* s_cnt = nullptr;
-  int* s_off = nullptr;
-  int* pkey = nullptr;  // per pixel (surfel, pixel) sort keys / values
-  int* pval = nullptr;
-  int* pkey2 = nullptr;
-  int* pval2 = nullptr;
+  int* s_head = nullptr;  // lowest pixel of the surfel's pairs
+  int* s_base = nullptr;  // segment base in p_list (surfels with > 1 pair)
+  int* s_fill = nullptr;  // segment fill counter
+  int* p_list = nullptr;  // per pixel: pixels of multi-pair surfels, segmented
+  int* p_next = nullptr;  // per pixel: next pixel of the same surfel (pixel order)
   // term -> block records and BSR
   int* rec_key = nullptr;
   int* rec_val = nullptr;
@@ -180,8 +180,6 @@ struct Ctx {
   float* part_h = nullptr;     // per chunk: 6x6 partial
   double* part_g = nullptr;    // per chunk: g partial
   int* part_t = nullptr;       // per chunk: touched
-  float* rows_l = nullptr;     // pair rows in per-surfel list order
-  double* r_l = nullptr;       // pair residuals in list order
   int* elig = nullptr;  // render-eligible surfels of the current frame's solve
   int n_elig = 0;
   int n_records = 0, n_up = 0, n_full = 0, n_chunks = 0, n_multi = 0, CH_cap = 0;
@@ -203,6 +201,7 @@ struct Ctx {
   double* pcg_items = nullptr;
   double* pcg_vec = nullptr;
   double* gst_part = nullptr;
+  int* pcg_slices = nullptr;  // per PCG CTA (r0, r1, bb0, bb1)
   double* reg_ab = nullptr;
   double* pcg_part = nullptr;
   int pcg_grid = 0;

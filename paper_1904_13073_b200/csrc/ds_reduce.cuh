@@ -29,6 +29,7 @@ __device__ __forceinline__ void grid_sum(double v, double* __restrict__ part,
   if (!last) return;
   __threadfence();
   double acc = 0.0;
+#pragma unroll 8
   for (int b = tid; b < (int)gridDim.x; b += kBlock) acc += __ldcg(part + b);
   sh[tid] = acc;
   __syncthreads();

@@ -2,10 +2,10 @@
 //   rigid_align  solver.cpp:171-242: stride pyramid 4 -> 2 -> 1 with {3, 3, 4}
 //   iterations, association at the lround pixel of the pose-transformed vertex
 //   against model maps rendered under the initial pose, J = [v x n, n], 6x6
-//   LDLT, se3_increment. Every iteration is a sample kernel (fp64 block
-//   reduction of the 21 + 6 + 2 normal-equation terms) followed by a one-block
-//   finalize that sums the partials in a fixed order and solves on the device,
-//   so the whole pyramid runs without a host round trip.
+//   LDLT, se3_increment. Every iteration is ONE kernel: fp64 block reductions
+//   of the 21 + 6 + 2 normal-equation terms, and the last block to arrive
+//   (ticket) sums the partials in a fixed order and solves on the device, so
+//   the whole pyramid runs without a host round trip.
 #include "ds_context.cuh"
 
 namespace ds {
@@ -13,78 +13,6 @@ namespace {
 
 constexpr int kTerms = 29;  // 21 upper H, 6 g, count, sum |r|
 constexpr int kThreads = 256;
-
-struct RigidParams {
-  Rig render_inv;
-  double fx, fy, cx, cy;
-  int W, H, stride, sw, sh;
-};
-
-__global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const double* __restrict__ cur_pose,
-                                                          const int* __restrict__ mm_idx, ModelBuf m,
-                                                          const double4* __restrict__ fvert,
-                                                          const double4* __restrict__ fnrm,
-                                                          const uint8_t* __restrict__ fflag,
-                                                          double* __restrict__ part) {
-  __shared__ double sh[kThreads / 32][kTerms];
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  double v[kTerms];
-#pragma unroll
-  for (int k = 0; k < kTerms; ++k) v[k] = 0.0;
-  if (t < rp.sw * rp.sh) {
-    const int x = (t % rp.sw) * rp.stride, y = (t / rp.sw) * rp.stride;
-    const size_t c = (size_t)y * rp.W + x;
-    if (fflag[c] & 2) {
-      const Rig cur = rig_load(cur_pose);
-      const double4 fv = fvert[c];
-      const V3 vw = rig_apply(cur, v3(fv.x, fv.y, fv.z));
-      const V3 pr = rig_apply(rp.render_inv, vw);
-      if (pr.z > 0) {
-        const double u = rp.fx * pr.x / pr.z + rp.cx;
-        const double vv = rp.fy * pr.y / pr.z + rp.cy;
-        if (fabs(u) < 1e9 && fabs(vv) < 1e9) {
-          const int ui = (int)llround(u), vi = (int)llround(vv);
-          if (ui >= 0 && ui < rp.W && vi >= 0 && vi < rp.H) {
-            const int win = mm_idx[(size_t)vi * rp.W + ui];
-            if (win >= 0) {
-              const float4 lp = m.lp[win], ln = m.ln[win];
-              const V3 vm = v3(lp.x, lp.y, lp.z), nm = v3(ln.x, ln.y, ln.z);
-              const double4 fn = fnrm[c];
-              if (nrm(sub(vw, vm)) < 0.03 &&
-                  dot(rig_rotate(cur, v3(fn.x, fn.y, fn.z)), nm) > 0.7) {
-                const double r = dot(nm, sub(vw, vm));
-                const V3 cr = cross(vw, nm);
-                const double J[6] = {cr.x, cr.y, cr.z, nm.x, nm.y, nm.z};
-                int k = 0;
-#pragma unroll
-                for (int a = 0; a < 6; ++a)
-#pragma unroll
-                  for (int b = a; b < 6; ++b) v[k++] = J[a] * J[b];
-#pragma unroll
-                for (int a = 0; a < 6; ++a) v[21 + a] = J[a] * r;
-                v[27] = 1.0;
-                v[28] = fabs(r);
-              }
-            }
-          }
-        }
-      }
-    }
-  }
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < kTerms; ++k) {
-    double s = v[k];
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-    if (lane == 0) sh[wid][k] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < kTerms) {
-    double s = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) s += sh[w][threadIdx.x];
-    part[(size_t)blockIdx.x * kTerms + threadIdx.x] = s;
-  }
-}
 
 // Eigen::LDLT semantics (solver.cpp:225): diagonal pivoting, zero pivots kept,
 // pseudo-inverse of D with tolerance DBL_MIN.
@@ -166,20 +94,100 @@ __device__ void ldlt_solve6(double A[6][6], const double* b, double* x) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_rigid_finalize(const double* __restrict__ part,
-                                                         int nblocks, int level,
-                                                         double* __restrict__ cur_pose,
-                                                         DevScalars* sc) {
+struct RigidParams {
+  Rig render_inv;
+  double fx, fy, cx, cy;
+  int W, H, stride, sw, sh;
+};
+
+__global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const double* __restrict__ cur_pose,
+                                                          const int* __restrict__ mm_idx, ModelBuf m,
+                                                          const double4* __restrict__ fvert,
+                                                          const double4* __restrict__ fnrm,
+                                                          const uint8_t* __restrict__ fflag,
+                                                          double* __restrict__ part,
+                                                          unsigned* __restrict__ ticket, int level,
+                                                          double* __restrict__ pose_out,
+                                                          DevScalars* __restrict__ sc) {
+  __shared__ double sh[kThreads / 32][kTerms];
   __shared__ double tot[kTerms];
+  __shared__ bool last;
+  double v[kTerms];
+#pragma unroll
+  for (int k = 0; k < kTerms; ++k) v[k] = 0.0;
+  const int total = rp.sw * rp.sh;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int x = (t % rp.sw) * rp.stride, y = (t / rp.sw) * rp.stride;
+    const size_t c = (size_t)y * rp.W + x;
+    if (fflag[c] & 2) {
+      const Rig cur = rig_load(cur_pose);
+      const double4 fv = fvert[c];
+      const V3 vw = rig_apply(cur, v3(fv.x, fv.y, fv.z));
+      const V3 pr = rig_apply(rp.render_inv, vw);
+      if (pr.z > 0) {
+        const double u = rp.fx * pr.x / pr.z + rp.cx;
+        const double vv = rp.fy * pr.y / pr.z + rp.cy;
+        if (fabs(u) < 1e9 && fabs(vv) < 1e9) {
+          const int ui = (int)llround(u), vi = (int)llround(vv);
+          if (ui >= 0 && ui < rp.W && vi >= 0 && vi < rp.H) {
+            const int win = mm_idx[(size_t)vi * rp.W + ui];
+            if (win >= 0) {
+              const float4 lp = m.lp[win], ln = m.ln[win];
+              const V3 vm = v3(lp.x, lp.y, lp.z), nm = v3(ln.x, ln.y, ln.z);
+              const double4 fn = fnrm[c];
+              if (nrm(sub(vw, vm)) < 0.03 &&
+                  dot(rig_rotate(cur, v3(fn.x, fn.y, fn.z)), nm) > 0.7) {
+                const double r = dot(nm, sub(vw, vm));
+                const V3 cr = cross(vw, nm);
+                const double J[6] = {cr.x, cr.y, cr.z, nm.x, nm.y, nm.z};
+                int k = 0;
+#pragma unroll
+                for (int a = 0; a < 6; ++a)
+#pragma unroll
+                  for (int b = a; b < 6; ++b) v[k++] += J[a] * J[b];
+#pragma unroll
+                for (int a = 0; a < 6; ++a) v[21 + a] += J[a] * r;
+                v[27] += 1.0;
+                v[28] += fabs(r);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int term = wid; term < kTerms; term += 8) {  // fixed order per term
+#pragma unroll
+  for (int k = 0; k < kTerms; ++k) {
+    double s = v[k];
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) sh[wid][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < kTerms) {  // term-major partials: the last block reads them coalesced
     double s = 0.0;
-    for (int b = lane; b < nblocks; b += 32) s += part[(size_t)b * kTerms + term];
+    for (int w = 0; w < kThreads / 32; ++w) s += sh[w][threadIdx.x];
+    part[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = s;
+  }
+  // the last block to arrive sums the partials in block order and solves
+  // (solver.cpp:214-232) -- the whole ICP iteration is one launch
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nb = gridDim.x;
+  for (int term = wid; term < kTerms; term += kThreads / 32) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int b = lane; b < nb; b += 32) s += __ldcg(part + (size_t)term * nb + b);
     for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
     if (lane == 0) tot[term] = s;
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  *ticket = 0u;
   const int pairs = (int)tot[27];
   if (level == 0) {
     sc->rigid_pairs = pairs;
@@ -199,8 +207,8 @@ __global__ void __launch_bounds__(256) k_rigid_finalize(const double* __restrict
   ldlt_solve6(A, ng, xi);
   for (int a = 0; a < 6; ++a)
     if (!isfinite(xi[a])) return;
-  const Rig cur = rig_load(cur_pose);
-  rig_store(se3_increment(v3(xi[0], xi[1], xi[2]), v3(xi[3], xi[4], xi[5]), cur), cur_pose);
+  const Rig cur = rig_load(pose_out);
+  rig_store(se3_increment(v3(xi[0], xi[1], xi[2]), v3(xi[3], xi[4], xi[5]), cur), pose_out);
 }
 
 }  // namespace
@@ -226,12 +234,11 @@ void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int
     rp.sw = cdiv(c.W, rp.stride);
     rp.sh = cdiv(c.H, rp.stride);
     const int samples = rp.sw * rp.sh;
-    const int nb = cdiv(samples, kThreads);
+    const int nb = std::min(cdiv(samples, kThreads), 2 * c.num_sms);  // grid-stride
     for (int it = 0; it < kIters[level]; ++it) {
-      DS_LAUNCH(c, KK_RIGID, 100.0 * samples, nb, kThreads, 0, k_rigid_terms, rp, c.d_pose,
-                c.mm_idx, c.M(), c.f_vert, c.f_nrm, c.f_flag, c.red_part);
-      DS_LAUNCH(c, KK_RIGID, 8.0 * kTerms * nb, 1, 256, 0, k_rigid_finalize, c.red_part, nb,
-                level, c.d_pose, c.dsc);
+      DS_LAUNCH(c, KK_RIGID, 100.0 * samples + 16.0 * kTerms * nb, nb, kThreads, 0, k_rigid_terms,
+                rp, c.d_pose, c.mm_idx, c.M(), c.f_vert, c.f_nrm, c.f_flag, c.red_part,
+                c.tickets + 3, level, c.d_pose, c.dsc);
     }
   }
   double pose[12];

@@ -60,6 +60,28 @@ struct PairParams {
   int P;
 };
 
+// CTA-local compaction of the pixels that carry a correspondence: the CTA's
+// ~40 % valid pixels are packed to the low threads, so whole warps retire
+// early instead of idling through the fp64 blend with inactive lanes. Returns
+// this thread's pixel (or -1) in the packed order (pixel order preserved).
+__device__ __forceinline__ int pack_pairs(const int* __restrict__ pair_s, int P, int* s_list,
+                                          int* s_wcnt, int& s_out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool v = c < P && pair_s[c] >= 0;
+  const unsigned bal = __ballot_sync(0xffffffffu, v);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_wcnt[wid] = __popc(bal);
+  __syncthreads();
+  int off = 0;
+  for (int w = 0; w < wid; ++w) off += s_wcnt[w];
+  if (v) s_list[off + __popc(bal & ((1u << lane) - 1u))] = c;
+  __syncthreads();
+  int tot = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_wcnt[w];
+  s_out = tot;
+  return threadIdx.x < tot ? s_list[threadIdx.x] : -1;
+}
+
 // Per correspondence: residual, Jacobian rows (fp32), data energy partials.
 __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair_s, ModelBuf m,
                                                     const double4* __restrict__ node_dq,
@@ -68,14 +90,17 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
                                                     PairParams pp, uint8_t* __restrict__ pair_ok,
                                                     float* __restrict__ rows,
                                                     double* __restrict__ pair_r,
-                                                    int* __restrict__ pkey,
-                                                    int* __restrict__ pval, int sentinel,
+                                                    int* __restrict__ s_cnt,
+                                                    int* __restrict__ s_head,
                                                     double* __restrict__ part,
                                                     unsigned* __restrict__ ticket,
                                                     double* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ int s_list[256];
+  __shared__ int s_wcnt[8];
+  int n_valid;
+  const int c = pack_pairs(pair_s, pp.P, s_list, s_wcnt, n_valid);
   double e = 0.0;
-  int s = c < pp.P ? pair_s[c] : -1;
+  int s = c >= 0 ? pair_s[c] : -1;
   if (s >= 0) {
     const Blend b = blend_entry(m.ki[s], m.kw[s], node_dq);
     if (b.degenerate) {
@@ -148,11 +173,9 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
       }
       pair_r[c] = r;
       pair_ok[c] = 1;
+      atomicAdd(s_cnt + s, 1);  // per-surfel pair count and first (lowest) pixel
+      atomicMin(s_head + s, c);
     }
-  }
-  if (c < pp.P) {  // (surfel, pixel) sort keys of the per-surfel pair lists
-    pkey[c] = (s >= 0 && pair_ok[c]) ? s : sentinel;
-    pval[c] = c;
   }
   grid_sum<256>(e, part, ticket, out);  // data energy, fixed order
 }
@@ -168,10 +191,13 @@ __global__ void __launch_bounds__(256) k_pair_energy(const int* __restrict__ pai
                                                      int* __restrict__ count,
                                                      unsigned* __restrict__ ticket,
                                                      double* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ int s_list[256];
+  __shared__ int s_wcnt[8];
+  int n_valid;
+  const int c = pack_pairs(pair_s, pp.P, s_list, s_wcnt, n_valid);
   double e = 0.0;
   int ok = 0;
-  const int s = c < pp.P ? pair_s[c] : -1;
+  const int s = c >= 0 ? pair_s[c] : -1;
   if (s >= 0) {
     const Blend b = blend_entry(m.ki[s], m.kw[s], node_dq);
     if (!b.degenerate) {
@@ -231,31 +257,47 @@ __global__ void k_any_stable_flag(const float4* __restrict__ ln, int n, double d
 }
 
 // ---------------------------------------------------------------- pair lists
-// After the (surfel, pixel) radix sort (stable: pixel order within a surfel),
-// thread per sorted slot: run heads record (offset, count) and every slot
-// gathers its pair's Jacobian rows / residual into list order, so the block
-// assembly reads one contiguous run per surfel.
-__global__ void k_pair_runs(const int* __restrict__ key, const int* __restrict__ val, int P,
-                            int sentinel, const float* __restrict__ rows,
-                            const double* __restrict__ pair_r, int* __restrict__ s_cnt,
-                            int* __restrict__ s_off, float* __restrict__ rows_l,
-                            double* __restrict__ r_l) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= P) return;
-  const int s = key[k];
-  if (s == sentinel) return;
-  if (k == 0 || key[k - 1] != s) {
-    int cnt = 1;
-    while (k + cnt < P && key[k + cnt] == s) ++cnt;
-    s_off[s] = k;
-    s_cnt[s] = cnt;
+// A surfel's correspondence pairs in pixel order (the summation order of the
+// assembly) as a chain over the per-pixel rows: s_head[s] = lowest pixel
+// (atomicMin in k_pair_terms), p_next[pixel] = next pixel of the same surfel.
+// Most surfels own one pair (no chain). For the others: the head pixel
+// reserves a segment of cnt slots (k_pair_reserve), every pixel of the surfel
+// drops itself into the segment in arrival order (k_pair_fill), and each pixel
+// scans its segment -- independent loads, no pointer chasing -- for its
+// successor in pixel order (k_pair_next). Slot order is not observable.
+__global__ void k_pair_reserve(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
+                               int P, const int* __restrict__ s_cnt, const int* __restrict__ s_head,
+                               int* __restrict__ s_base, int* __restrict__ counter) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P || !pair_ok[c]) return;
+  const int s = pair_s[c];
+  const int cnt = s_cnt[s];
+  if (cnt > 1 && s_head[s] == c) s_base[s] = atomicAdd(counter, cnt);
+}
+__global__ void k_pair_fill(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
+                            int P, const int* __restrict__ s_cnt, const int* __restrict__ s_base,
+                            int* __restrict__ s_fill, int* __restrict__ p_list) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P || !pair_ok[c]) return;
+  const int s = pair_s[c];
+  if (s_cnt[s] > 1) p_list[s_base[s] + atomicAdd(s_fill + s, 1)] = c;
+}
+__global__ void k_pair_next(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
+                            int P, const int* __restrict__ s_cnt, const int* __restrict__ s_base,
+                            const int* __restrict__ p_list, int* __restrict__ p_next) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P || !pair_ok[c]) return;
+  const int s = pair_s[c];
+  const int cnt = s_cnt[s];
+  if (cnt < 2) return;
+  const int* seg = p_list + s_base[s];
+  int nxt = 0x7fffffff;
+#pragma unroll 8
+  for (int k = 0; k < cnt; ++k) {
+    const int q = seg[k];
+    if (q > c && q < nxt) nxt = q;
   }
-  const int pix = val[k];
-  const float4* src = reinterpret_cast<const float4*>(rows + (size_t)pix * 24);
-  float4* dst = reinterpret_cast<float4*>(rows_l + (size_t)k * 24);
-#pragma unroll
-  for (int t = 0; t < 6; ++t) dst[t] = src[t];
-  r_l[k] = pair_r[pix];
+  p_next[c] = nxt == 0x7fffffff ? -1 : nxt;
 }
 
 // ------------------------------------------------------------ block pattern
@@ -427,9 +469,10 @@ struct AsmArgs {
   const int* chunk_first;
   const int* rec_val;
   const int* s_cnt;
-  const int* s_off;
-  const float* rows_l;
-  const double* r_l;
+  const int* s_head;   // lowest pixel of the surfel's pairs
+  const int* p_next;   // next pixel of the same surfel (pixel order)
+  const float* rows;   // per-pixel Jacobian rows (4 x 6 fp32)
+  const double* pair_r;
   const double4* node_pos;
   const int* nbr;
   const double* se3;
@@ -530,17 +573,19 @@ __device__ __forceinline__ void acc_pair(const float a[6], const float b[6], boo
   }
 }
 
-// A surfel record: its pair list (list order = pixel order), the first pair's
-// rows already loaded into (a, b, r).
-__device__ __forceinline__ void acc_surfel_record(const AsmArgs& A, int v, int cnt, int off,
+// A surfel record: its pairs in pixel order (head pixel, then the p_next
+// chain), the head pair's rows already loaded into (a, b, r).
+__device__ __forceinline__ void acc_surfel_record(const AsmArgs& A, int v, int cnt, int head,
                                                   const float a[6], const float b[6], double r,
                                                   bool diag, float h[36], double gg[6]) {
   const int mr = (v >> 2) & 3, mc = v & 3;
   acc_pair(a, b, diag, r, h, gg);
+  int pix = head;
   for (int q = 1; q < cnt; ++q) {
+    pix = __ldg(A.p_next + pix);
     float a2[6], b2[6];
-    load_rows(A.rows_l + (size_t)(off + q) * 24, mr, mc, a2, b2);
-    acc_pair(a2, b2, diag, diag ? __ldg(A.r_l + off + q) : 0.0, h, gg);
+    load_rows(A.rows + (size_t)pix * 24, mr, mc, a2, b2);
+    acc_pair(a2, b2, diag, diag ? __ldg(A.pair_r + pix) : 0.0, h, gg);
   }
 }
 
@@ -574,21 +619,21 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
       const int v1 = has1 ? A.rec_val[k + kChunkLanes] : 0;
       if (v0 >= 0 && v1 >= 0) {
         // two surfel records in flight
-        const int cnt0 = A.s_cnt[v0 >> 4], off0 = A.s_off[v0 >> 4];
+        const int cnt0 = A.s_cnt[v0 >> 4], off0 = A.s_head[v0 >> 4];
         int cnt1 = 0, off1 = 0;
         if (has1) {
           cnt1 = A.s_cnt[v1 >> 4];
-          off1 = A.s_off[v1 >> 4];
+          off1 = A.s_head[v1 >> 4];
         }
         float a0[6], b0[6], a1[6], b1[6];
         double rr0 = 0.0, rr1 = 0.0;
         if (cnt0 > 0) {
-          load_rows(A.rows_l + (size_t)off0 * 24, (v0 >> 2) & 3, v0 & 3, a0, b0);
-          if (diag) rr0 = __ldg(A.r_l + off0);
+          load_rows(A.rows + (size_t)off0 * 24, (v0 >> 2) & 3, v0 & 3, a0, b0);
+          if (diag) rr0 = __ldg(A.pair_r + off0);
         }
         if (cnt1 > 0) {
-          load_rows(A.rows_l + (size_t)off1 * 24, (v1 >> 2) & 3, v1 & 3, a1, b1);
-          if (diag) rr1 = __ldg(A.r_l + off1);
+          load_rows(A.rows + (size_t)off1 * 24, (v1 >> 2) & 3, v1 & 3, a1, b1);
+          if (diag) rr1 = __ldg(A.pair_r + off1);
         }
         if (cnt0 > 0) {
           acc_surfel_record(A, v0, cnt0, off0, a0, b0, rr0, diag, h, gg);
@@ -606,11 +651,11 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
             acc_reg_record(A, v, h, gg);
             touched = 1;
           } else {
-            const int cnt = A.s_cnt[v >> 4], off = A.s_off[v >> 4];
+            const int cnt = A.s_cnt[v >> 4], off = A.s_head[v >> 4];
             if (cnt > 0) {
               float a0[6], b0[6];
-              load_rows(A.rows_l + (size_t)off * 24, (v >> 2) & 3, v & 3, a0, b0);
-              acc_surfel_record(A, v, cnt, off, a0, b0, diag ? __ldg(A.r_l + off) : 0.0, diag, h,
+              load_rows(A.rows + (size_t)off * 24, (v >> 2) & 3, v & 3, a0, b0);
+              acc_surfel_record(A, v, cnt, off, a0, b0, diag ? __ldg(A.pair_r + off) : 0.0, diag, h,
                                 gg);
               touched = 1;
             }
@@ -679,12 +724,14 @@ __global__ void k_assemble_finish(AsmArgs A, const int* __restrict__ multi, cons
   const int pm = row != colb ? A.up_mpos[ub] : -1;
   if (t < 36) {
     double acc = 0.0;
+#pragma unroll 4
     for (int c = c0; c < c1; ++c) acc += (double)A.part_h[(size_t)c * 36 + t];
     A.bsr_val[(size_t)pu * 36 + t] = (float)acc;
     if (pm >= 0) A.bsr_val[(size_t)pm * 36 + (t % 6) * 6 + t / 6] = (float)acc;
   } else if (t < 42) {
     if (pm >= 0) return;
     double acc = 0.0;
+#pragma unroll 4
     for (int c = c0; c < c1; ++c) acc += A.part_g[(size_t)c * 6 + (t - 36)];
     A.g[6 * row + (t - 36)] = acc;
   } else {
@@ -764,6 +811,7 @@ __global__ void __launch_bounds__(kStatsThreads) k_g_stats(
   if (!last || tid != 0) return;
   __threadfence();
   double m = 0, q = 0, t = 0;
+#pragma unroll 8
   for (int b = 0; b < (int)gridDim.x; ++b) {
     m = fmax(m, __ldcg(part + 3 * b));
     q += __ldcg(part + 3 * b + 1);
@@ -819,6 +867,7 @@ struct PcgArgs {
   double* vec;      // fallback scratch (kPcgVecs x 6N)
   double* items;    // fallback SpMV partials (6 nnzb)
   double* part;     // grid partials, 2 x 4 x G
+  const int* slices;  // per CTA (r0, r1, bb0, bb1), k_pcg_slices once per frame
   DevScalars* sc;
 };
 
@@ -892,6 +941,7 @@ __device__ __forceinline__ void cta_sum3(double& a, double& b, double& c, double
 __device__ __forceinline__ double4 grid_sum3(const double* part, double4* sh) {
   if (threadIdx.x < 32) {
     double va = 0.0, vb = 0.0, vc = 0.0;
+#pragma unroll 8
     for (int k = threadIdx.x; k < gridDim.x; k += 32) {
       const double2 ab = __ldcg(reinterpret_cast<const double2*>(part + 4 * k));
       va += ab.x;
@@ -971,23 +1021,36 @@ __device__ __forceinline__ void apply_minv(const double* MINV, const double* v, 
 // for a fixed iteration budget, the reference's default). kPipe = false: the
 // classic two-barrier recurrences, whose recursive residual stays close to the
 // true one -- used when PCG runs to a tolerance (attainable accuracy).
+// CTA b of the PCG owns the block rows [r0, r1) whose BSR blocks are
+// [nnzb b / G, nnzb (b+1) / G) rounded to row starts; computed once per frame
+// (the pattern is fixed for the frame), thread per CTA.
+__global__ void k_pcg_slices(const int* __restrict__ row_ptr, int N, int nnzb, int G,
+                             int* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= G) return;
+  const long long nz = nnzb;
+  const int t_lo = (int)(nz * b / G), t_hi = (int)(nz * (b + 1) / G);
+  const int r0 = b == 0 ? 0 : min(lower_bound_dev(row_ptr, N + 1, t_lo), N);
+  int r1 = b == G - 1 ? N : min(lower_bound_dev(row_ptr, N + 1, t_hi), N);
+  r1 = max(r1, r0);
+  out[4 * b + 0] = r0;
+  out[4 * b + 1] = r1;
+  out[4 * b + 2] = row_ptr[r0];
+  out[4 * b + 3] = row_ptr[r1];
+}
+
 template <bool kPipe>
 __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double4 sh[kPcgWarps + 1];
-  __shared__ int s_rng[2];
-  const int tid = threadIdx.x, G = gridDim.x, N = a.N;
-  if (tid == 0) {
-    const long long nnzb = a.nnzb;
-    const int t_lo = (int)(nnzb * blockIdx.x / G), t_hi = (int)(nnzb * (blockIdx.x + 1) / G);
-    s_rng[0] = blockIdx.x == 0 ? 0 : lower_bound_dev(a.row_ptr, N + 1, t_lo);
-    s_rng[1] = blockIdx.x == G - 1 ? N : lower_bound_dev(a.row_ptr, N + 1, t_hi);
-  }
+  __shared__ int s_rng[4];
+  const int tid = threadIdx.x, G = gridDim.x;
+  if (tid < 4) s_rng[tid] = a.slices[4 * blockIdx.x + tid];  // (r0, r1, bb0, bb1), per frame
   __syncthreads();
-  const int r0 = min(s_rng[0], N), r1 = max(min(s_rng[1], N), r0);
+  const int r0 = s_rng[0], r1 = s_rng[1];
   const int nr = r1 - r0, n6 = 6 * nr;
-  const int bb0 = a.row_ptr[r0], nb = a.row_ptr[r1] - bb0;
+  const int bb0 = s_rng[2], nb = s_rng[3] - bb0;
   const double mu = *a.mu_ptr;
   // ---- slice placement: shared memory when it fits, else global scratch
   const size_t need = (size_t)nr * (36 + 6 * kPcgVecs) * 8 + (size_t)nb * (6 * 8 + 36 * 4 + 4) +
@@ -1289,6 +1352,9 @@ __global__ void k_check_finite(const double* __restrict__ x, int n, int* __restr
 }  // namespace
 
 // ------------------------------------------------------------------ host side
+// a CTA per SM; small systems use fewer CTAs
+int pcg_ctas(const Ctx& c) { return std::min(c.pcg_grid, std::max(1, cdiv(c.n_full, 64))); }
+
 void build_pattern(Ctx& c, int t_now, int t_last) {
   const int n_all = c.n_surfels, N = c.n_nodes;
   if ((long long)N * N >= 0x7fffffffLL) fail(DS_ERR_CAPACITY, "too many nodes for block keys");
@@ -1355,6 +1421,8 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
   }
   DS_LAUNCH(c, KK_PATTERN, 16.0 * c.n_full, cdiv(N, 128), 128, 0, k_row_sort, c.row_ptr, N,
             c.bsr_col, c.bsr_tag, c.up_pos, c.up_mpos, c.diag_pos);
+  DS_LAUNCH(c, KK_PATTERN, 16.0 * pcg_ctas(c), cdiv(pcg_ctas(c), 128), 128, 0, k_pcg_slices,
+            c.row_ptr, N, c.n_full, pcg_ctas(c), c.pcg_slices);
   if (c.n_pairs_ok_est <= 0) c.n_pairs_ok_est = 0.4 * c.P;
   // fixed-size record chunks for the assembly (per frame)
   c.n_chunks = 0;
@@ -1399,18 +1467,21 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   forward_warp_list(c, c.elig, c.n_elig);
   render_model_maps_list(c, pose, t_now, t_last, pose, c.elig, c.n_elig);
   DS_CUDA(cudaMemsetAsync(c.s_cnt, 0, sizeof(int) * (n + 1), c.stream));
+  DS_CUDA(cudaMemsetAsync(c.s_head, 0x7f, sizeof(int) * (n + 1), c.stream));
+  DS_CUDA(cudaMemsetAsync(c.s_fill, 0, sizeof(int) * (n + 1), c.stream));
+  DS_CUDA(cudaMemsetAsync(&c.dsc->pair_list_n, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
   const int nbp = cdiv(P, 256);
-  const int bits = n > 0 ? 32 - __builtin_clz((unsigned)n) : 1;  // 2^bits > n
-  const int sentinel = (int)((1u << bits) - 1u);
-  // per pixel: pair id 4 B, surfel ref + skin 48 B, frame maps 64 B, rows 96 B + r 8 B + keys 8 B out
-  DS_LAUNCH(c, KK_PAIR_TERMS, 228.0 * P, nbp, 256, 0, k_pair_terms, c.pair_s, c.M(), c.node_dq,
-            c.f_vert, c.f_nrm, pair_params(c, pose), c.pair_ok, c.pair_rows, c.pair_r, c.pkey,
-            c.pval, sentinel, c.red_part, c.tickets + 0, &c.dsc->e_data_pre);
-  int *ks, *vs;
-  sort_pairs(c, c.pkey, c.pval, c.pkey2, c.pval2, P, bits, &ks, &vs, KK_PAIR_LISTS);
-  DS_LAUNCH(c, KK_PAIR_LISTS, 8.0 * P + 112.0 * c.n_pairs_ok_est, nbp, 256, 0, k_pair_runs, ks, vs,
-            P, sentinel, c.pair_rows, c.pair_r, c.s_cnt, c.s_off, c.rows_l, c.r_l);
+  // per pixel: pair id 4 B, surfel ref + skin 48 B, frame maps 64 B, rows 96 B + r 8 B out
+  DS_LAUNCH(c, KK_PAIR_TERMS, 220.0 * P, nbp, 256, 0, k_pair_terms, c.pair_s, c.M(), c.node_dq,
+            c.f_vert, c.f_nrm, pair_params(c, pose), c.pair_ok, c.pair_rows, c.pair_r, c.s_cnt,
+            c.s_head, c.red_part, c.tickets + 0, &c.dsc->e_data_pre);
+  DS_LAUNCH(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_reserve, c.pair_s, c.pair_ok, P,
+            c.s_cnt, c.s_head, c.s_base, &c.dsc->pair_list_n);
+  DS_LAUNCH(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_fill, c.pair_s, c.pair_ok, P, c.s_cnt,
+            c.s_base, c.s_fill, c.p_list);
+  DS_LAUNCH(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_pair_next, c.pair_s, c.pair_ok, P, c.s_cnt,
+            c.s_base, c.p_list, c.p_next);
   node_se3(c, c.node_dq, c.node_se3);
   const int nbe = cdiv(8 * N, 256);
   DS_LAUNCH(c, KK_ENERGY, 200.0 * N, nbe, 256, 0, k_reg_energy, c.node_pos, c.node_nbr,
@@ -1425,9 +1496,10 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   A.chunk_first = c.chunk_first;
   A.rec_val = c.rec_val;
   A.s_cnt = c.s_cnt;
-  A.s_off = c.s_off;
-  A.rows_l = c.rows_l;
-  A.r_l = c.r_l;
+  A.s_head = c.s_head;
+  A.p_next = c.p_next;
+  A.rows = c.pair_rows;
+  A.pair_r = c.pair_r;
   A.node_pos = c.node_pos;
   A.nbr = c.node_nbr;
   A.se3 = c.node_se3;
@@ -1489,9 +1561,9 @@ void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   a.vec = c.pcg_vec;
   a.items = c.pcg_items;
   a.part = c.pcg_part;
+  a.slices = c.pcg_slices;
   a.sc = c.dsc;
-  // a CTA per SM; small systems use fewer CTAs (cheaper grid barriers)
-  const int grid = std::min(c.pcg_grid, std::max(1, cdiv(c.n_full, 64)));
+  const int grid = pcg_ctas(c);
   void* args[] = {&a};
   launch_begin(c, KK_PCG);
   void* fn = a.tol2 > 0.0 ? (void*)k_pcg<false> : (void*)k_pcg<true>;

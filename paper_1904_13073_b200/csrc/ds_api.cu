@@ -4,6 +4,7 @@
 // (pipeline.cpp:42-72); all stage work is on the device.
 #include <cub/cub.cuh>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <algorithm>
@@ -239,6 +240,7 @@ void allocate(Ctx& c) {
   }
   c.pcg_part = dalloc<double>(c, 8 * (size_t)c.pcg_grid);
   c.pcg_slices = dalloc<int>(c, 4 * (size_t)c.pcg_grid + 4);
+  if (std::getenv("DS_PCG_TRACE")) c.pcg_trace = dalloc<unsigned long long>(c, 64);
   c.cand_flag = dalloc<int>(c, P + 1);
   c.cand_scan = dalloc<int>(c, P + 1);
   c.cand_pix = dalloc<int>(c, P);
@@ -1035,6 +1037,16 @@ ds_status ds_pcg_solve(ds_context* ctx, double mu, int32_t max_iters, double tol
     DS_CUDA(cudaMemcpyAsync(delta, c.pcg_x, sizeof(double) * 6 * c.n_nodes, cudaMemcpyDeviceToHost,
                             c.stream));
     ds::sync(c);
+  }
+  if (c.pcg_trace) {  // DS_PCG_TRACE: phase timestamps of CTA 0, us from kernel start
+    unsigned long long tr[64];
+    DS_CUDA(cudaMemcpy(tr, c.pcg_trace, sizeof tr, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "pcg_trace");
+    for (int k = 1; k < 64; ++k)
+      if (tr[k] >= tr[0] && tr[k] - tr[0] < 100000000ull)
+        std::fprintf(stderr, " %d:%.2f", k, (tr[k] - tr[0]) * 1e-3);
+    std::fprintf(stderr, "\n");
+    DS_CUDA(cudaMemset(c.pcg_trace, 0, sizeof tr));
   }
   API_END
 }

@@ -202,6 +202,7 @@ struct Ctx {
   double* pcg_vec = nullptr;
   double* gst_part = nullptr;
   int* pcg_slices = nullptr;  // per PCG CTA (r0, r1, bb0, bb1)
+  unsigned long long* pcg_trace = nullptr;  // DS_PCG_TRACE diagnostics
   double* reg_ab = nullptr;
   double* pcg_part = nullptr;
   int pcg_grid = 0;

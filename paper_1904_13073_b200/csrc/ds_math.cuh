@@ -36,7 +36,12 @@ DSI V3 add(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
 DSI V3 sub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
 DSI V3 neg(V3 a) { return v3(-a.x, -a.y, -a.z); }
 DSI V3 scl(double s, V3 a) { return v3(s * a.x, s * a.y, s * a.z); }
-DSI V3 dvd(V3 a, double s) { return v3(a.x / s, a.y / s, a.z / s); }
+// x / s, bit-identical to IEEE division for finite nonzero s, but a zero
+// numerator returns the signed zero directly: on sm_100 the fp64 division
+// fast path sends 0 / s to the slow subroutine (~20x slower), and zeros are
+// common here (identity nodes, zero dual parts, unit basis rows).
+DSI double ddiv(double x, double s) { return x == 0.0 ? x * s : x / s; }
+DSI V3 dvd(V3 a, double s) { return v3(ddiv(a.x, s), ddiv(a.y, s), ddiv(a.z, s)); }
 DSI double dot(V3 a, V3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
 DSI double sqn(V3 a) { return dot(a, a); }
 DSI double nrm(V3 a) { return sqrt(sqn(a)); }
@@ -49,7 +54,7 @@ DSI Q4 q4(double w, double x, double y, double z) { return Q4{w, x, y, z}; }
 DSI Q4 qadd(Q4 a, Q4 b) { return q4(a.w + b.w, a.x + b.x, a.y + b.y, a.z + b.z); }
 DSI Q4 qsub(Q4 a, Q4 b) { return q4(a.w - b.w, a.x - b.x, a.y - b.y, a.z - b.z); }
 DSI Q4 qscl(double s, Q4 a) { return q4(s * a.w, s * a.x, s * a.y, s * a.z); }
-DSI Q4 qdiv(Q4 a, double s) { return q4(a.w / s, a.x / s, a.y / s, a.z / s); }
+DSI Q4 qdiv(Q4 a, double s) { return q4(ddiv(a.w, s), ddiv(a.x, s), ddiv(a.y, s), ddiv(a.z, s)); }
 DSI Q4 qneg(Q4 a) { return q4(-a.w, -a.x, -a.y, -a.z); }
 DSI double qdot(Q4 a, Q4 b) { return ((a.w * b.w + a.x * b.x) + a.y * b.y) + a.z * b.z; }
 DSI double qnrm(Q4 a) { return sqrt(qdot(a, a)); }
@@ -198,10 +203,10 @@ DSI DQ dq_from_rig(const Rig& T) {
 // geometry.cpp:102-109
 DSI DQ dq_normalized(const DQ& q) {
   const double a = qnrm(q.r);
-  const double b = qdot(q.r, q.d) / a;
+  const double b = ddiv(qdot(q.r, q.d), a);
   DQ o;
   o.r = qdiv(q.r, a);
-  o.d = qsub(qdiv(q.d, a), qscl(b / (a * a), q.r));
+  o.d = qsub(qdiv(q.d, a), qscl(ddiv(b, a * a), q.r));
   return o;
 }
 // geometry.cpp:86-93

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
       const double a = qnrm(br);
       const double rd = qdot(br, bd);
       const Q4 nr = qdiv(br, a);
-      const Q4 ndq = qsub(qdiv(bd, a), qscl(rd / (a * a * a), br));
+      const Q4 ndq = qsub(qdiv(bd, a), qscl(ddiv(rd, a * a * a), br));
       const Q4 pq = q4(0.0, p.x, p.y, p.z);
       const Q4 q1 = qmul(pq, qconj(nr)), q2 = qmul(nr, pq);
       const Q4 cn = qconj(nr);
@@ -146,10 +146,10 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
       // dnd/dbr be = -(bd (br.be) + br (bd.be) + rd be)/a^3 + 3 rd/a^5 br (br.be)
       const double brbe = qdot(br, beq), bdbe = qdot(bd, beq);
       const Q4 t1 = qadd(qadd(qscl(brbe, bd), qscl(bdbe, br)), qscl(rd, beq));
-      const Q4 u_r2 = qadd(qscl(-1.0 / a3, t1), qscl(3.0 * rd / a5 * brbe, br));
+      const Q4 u_r2 = qadd(qscl(-1.0 / a3, t1), qscl(ddiv(3.0 * rd, a5) * brbe, br));
       const Q4 ur = qadd(u_r1, u_r2);
       // dnd/dbd be = be/a - br (br.be)/a^3
-      const Q4 ud = qsub(qdiv(beq, a), qscl(brbe / a3, br));
+      const Q4 ud = qsub(qdiv(beq, a), qscl(ddiv(brbe, a3), br));
       const double uv[8] = {ur.w, ur.x, ur.y, ur.z, ud.w, ud.x, ud.y, ud.z};
       float* out = rows + (size_t)c * 24;
 #pragma unroll
@@ -867,6 +867,7 @@ struct PcgArgs {
   double* vec;      // fallback scratch (kPcgVecs x 6N)
   double* items;    // fallback SpMV partials (6 nnzb)
   double* part;     // grid partials, 2 x 4 x G
+  unsigned long long* trace;  // optional phase timestamps (DS_PCG_TRACE), CTA 0
   const int* slices;  // per CTA (r0, r1, bb0, bb1), k_pcg_slices once per frame
   DevScalars* sc;
 };
@@ -877,7 +878,10 @@ struct PcgArgs {
 // group fall back to the inverse diagonal, like the reference's LDLT guard.
 __device__ __forceinline__ void gj_inverse6(double a[6], double b[6], int lr) {
   const int base = (threadIdx.x & 31) & ~7;
-  const double diag_lr = lr < 6 ? a[lr < 6 ? lr : 0] : 1.0;
+  double diag_lr = 1.0;  // a[lr] without a dynamic register-array index (no local memory)
+#pragma unroll
+  for (int t = 0; t < 6; ++t)
+    if (t == lr) diag_lr = a[t];
 #pragma unroll
   for (int t = 0; t < 6; ++t) b[t] = (t == lr) ? 1.0 : 0.0;
   bool ok = true;
@@ -891,14 +895,17 @@ __device__ __forceinline__ void gj_inverse6(double a[6], double b[6], int lr) {
     }
     const double piv = ap[p];
     if (!(piv > 0.0)) ok = false;
+    // one division per step (pivot > 0 normal); the rows scale by the
+    // reciprocal -- dividing the many zero entries would take the slow path
+    const double ip = ok ? 1.0 / piv : 0.0;
     if (lr == p) {
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
-        a[t] = ap[t] / piv;
-        b[t] = bp[t] / piv;
+        a[t] = ap[t] * ip;
+        b[t] = bp[t] * ip;
       }
     } else {
-      const double f = a[p] / piv;
+      const double f = a[p] * ip;
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
         a[t] = a[t] - f * ap[t];
@@ -936,28 +943,19 @@ __device__ __forceinline__ void cta_sum3(double& a, double& b, double& c, double
   c = tc;
 }
 
-// grid totals of the 3 partials at part[4 k + 0..2]: warp 0 sums the G
-// partials in a fixed order, identical in every CTA
+// grid totals of the 3 partials at part[4 k + 0..2]: thread k < G loads CTA
+// k's partials (one coalesced pass), then a fixed warp-shuffle + warp-order
+// tree -- identical bits in every CTA
 __device__ __forceinline__ double4 grid_sum3(const double* part, double4* sh) {
-  if (threadIdx.x < 32) {
-    double va = 0.0, vb = 0.0, vc = 0.0;
-#pragma unroll 8
-    for (int k = threadIdx.x; k < gridDim.x; k += 32) {
-      const double2 ab = __ldcg(reinterpret_cast<const double2*>(part + 4 * k));
-      va += ab.x;
-      vb += ab.y;
-      vc += __ldcg(part + 4 * k + 2);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      va += __shfl_xor_sync(0xffffffffu, va, off);
-      vb += __shfl_xor_sync(0xffffffffu, vb, off);
-      vc += __shfl_xor_sync(0xffffffffu, vc, off);
-    }
-    if (threadIdx.x == 0) sh[kPcgWarps] = make_double4(va, vb, vc, 0.0);
+  double va = 0.0, vb = 0.0, vc = 0.0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += kPcgThreads) {
+    const double2 ab = __ldcg(reinterpret_cast<const double2*>(part + 4 * k));
+    va += ab.x;
+    vb += ab.y;
+    vc += __ldcg(part + 4 * k + 2);
   }
-  __syncthreads();
-  return sh[kPcgWarps];
+  cta_sum3(va, vb, vc, sh);
+  return make_double4(va, vb, vc, 0.0);
 }
 
 __device__ __forceinline__ int lower_bound_dev(const int* a, int n, int v) {
@@ -1039,9 +1037,18 @@ __global__ void k_pcg_slices(const int* __restrict__ row_ptr, int N, int nnzb, i
   out[4 * b + 3] = row_ptr[r1];
 }
 
+__device__ __forceinline__ void pcg_mark(const PcgArgs& a, int slot) {
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && slot < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[slot] = t;
+  }
+}
+
 template <bool kPipe>
 __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
   cg::grid_group grid = cg::this_grid();
+  pcg_mark(a, 0);
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double4 sh[kPcgWarps + 1];
   __shared__ int s_rng[4];
@@ -1094,6 +1101,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
   double* Qv = Zv + n6;
   double* Sv = Qv + n6;
   double* Pv = Sv + n6;
+  pcg_mark(a, 1);
   // ---- prologue: block-Jacobi inverses (8-lane Gauss-Jordan per node)
   {
     const int grp = tid >> 3, lr = tid & 7;
@@ -1101,18 +1109,29 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
       const int i = i0 + grp;
       double ar[6], br[6];
       const int d = (i < nr && lr < 6) ? a.diag_pos[r0 + i] : -1;
+      if (i0 == 0) pcg_mark(a, 55 + (d >= 0 ? 0 : 4));
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
         double v = d >= 0 ? (double)a.val[(size_t)d * 36 + lr * 6 + t] : 0.0;
         if (t == lr) v += mu;
         ar[t] = lr < 6 ? v : 0.0;
       }
+      if (i0 == 0) pcg_mark(a, 56 + (ar[0] == 12345.0 ? 1 : 0));
+      if (a.trace) {  // diagnostic: a cold and a warm run of the same code
+        double a2[6], b2[6];
+#pragma unroll
+        for (int t = 0; t < 6; ++t) a2[t] = ar[t];
+        gj_inverse6(a2, b2, lr);
+        if (i0 == 0) pcg_mark(a, 50 + (b2[0] == 12345.0 ? 1 : 0));
+      }
       gj_inverse6(ar, br, lr);
+      if (i0 == 0) pcg_mark(a, 58 + (br[0] == 12345.0 ? 1 : 0));
       if (i < nr && lr < 6)
 #pragma unroll
         for (int t = 0; t < 6; ++t) MINV[36 * i + 6 * lr + t] = br[t];
     }
   }
+  pcg_mark(a, 59);
   // r0 = -g, x0 = 0, recurrence vectors 0
   for (int k = tid; k < n6; k += kPcgThreads) {
     R[k] = -a.g[6 * (size_t)r0 + k];
@@ -1123,16 +1142,22 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
     Pv[k] = 0.0;
   }
   __syncthreads();
+  pcg_mark(a, 60);
   // u0 = M^-1 r0, published (pipelined: in the odd buffer, which iteration 0's
   // m does not overwrite while slower CTAs still gather u0)
   double* u0pub = kPipe ? a.pub1 : a.pub0;
   apply_minv(MINV, R, U, nr);
+  pcg_mark(a, 61);
   for (int k = tid; k < n6; k += kPcgThreads) u0pub[6 * (size_t)r0 + k] = U[k];
+  pcg_mark(a, 62);
   double rr0 = 0.0, rr = 0.0;
   int it = 0;
+  pcg_mark(a, 2);
   if constexpr (kPipe) {
     grid.sync();
+    pcg_mark(a, 3);
     slice_spmv(V, C, RP, bb0, nb, nr, u0pub, U, mu, IT, W);  // w0 = A u0
+    pcg_mark(a, 4);
     double gamma_old = 0.0, alpha_old = 0.0;
     for (;; ++it) {
       __syncthreads();  // W (and R, U) complete
@@ -1152,6 +1177,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
         pd += W[k] * U[k];
         pr += R[k] * R[k];
       }
+      pcg_mark(a, 5 + 5 * it);
       cta_sum3(pg, pd, pr, sh);
       double* part = a.part + 4 * G * (it & 1);
       if (tid == 0) {
@@ -1159,14 +1185,18 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
         part[4 * blockIdx.x + 1] = pd;
         part[4 * blockIdx.x + 2] = pr;
       }
+      pcg_mark(a, 6 + 5 * it);
       grid.sync();
+      pcg_mark(a, 7 + 5 * it);
       const double4 tot = grid_sum3(part, sh);
+      pcg_mark(a, 8 + 5 * it);
       const double gamma = tot.x, delta = tot.y;
       rr = tot.z;
       if (it == 0) rr0 = rr;
       if (it >= a.max_iters || rr == 0.0 || (a.tol2 > 0.0 && rr <= a.tol2 * rr0)) break;
       // n = (H + mu I) m  (same k -> thread map in slice_spmv's row pass and below)
       slice_spmv(V, C, RP, bb0, nb, nr, pub, Mv, mu, IT, Nv);
+      pcg_mark(a, 9 + 5 * it);
       const double beta = it > 0 ? gamma / gamma_old : 0.0;
       const double alpha = it > 0 ? gamma / (delta - beta * gamma / alpha_old) : gamma / delta;
       for (int k = tid; k < n6; k += kPcgThreads) {
@@ -1278,6 +1308,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
     }
   }
   for (int k = tid; k < n6; k += kPcgThreads) a.x[6 * (size_t)r0 + k] = X[k];
+  pcg_mark(a, 63);
   if (blockIdx.x == 0 && tid == 0) {
     a.sc->pcg_iters = it;
     a.sc->pcg_rr = rr;
@@ -1562,6 +1593,7 @@ void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   a.items = c.pcg_items;
   a.part = c.pcg_part;
   a.slices = c.pcg_slices;
+  a.trace = c.pcg_trace;
   a.sc = c.dsc;
   const int grid = pcg_ctas(c);
   void* args[] = {&a};

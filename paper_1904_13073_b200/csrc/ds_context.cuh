@@ -295,7 +295,7 @@ int forward_warp(Ctx& c, bool count_degenerate);
 void forward_warp_list(Ctx& c, const int* list, int n);  // only the listed surfels
 void node_se3(Ctx& c, const double4* dq, double* se3);
 void node_live_positions(Ctx& c);
-void apply_increments(Ctx& c, const double* delta, double4* out);  // solver.cpp:277-286
+void apply_increments(Ctx& c, const double* delta, double4* out, double* se3 = nullptr);  // solver.cpp:277-286
 void init_warp_field(Ctx& c);
 void compute_node_edges(Ctx& c);
 int extend_warp_field(Ctx& c, const float4* positions, int n);  // returns appended
@@ -307,7 +307,8 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
 void render_index_map(Ctx& c, const double* pose, int factor);
 // model maps + association over a precomputed render-eligible surfel list
 void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
-                            const double* assoc_pose, const int* list, int n);
+                            const double* assoc_pose, const int* list, int n,
+                            const double4* warp_dq = nullptr, bool resolve = true);
 
 // ---- solver (k_solver.cu, k_rigid.cu)
 void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver_report* out);

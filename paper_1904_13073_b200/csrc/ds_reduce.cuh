@@ -7,9 +7,12 @@
 
 namespace ds {
 
+// Blocks [0, nblocks) of a sub-range of the grid (block id `bid`) reduce into
+// `out`; the plain overload uses the whole grid.
 template <int kBlock>
-__device__ __forceinline__ void grid_sum(double v, double* __restrict__ part,
-                                         unsigned* __restrict__ ticket, double* __restrict__ out) {
+__device__ __forceinline__ void grid_sum_part(double v, double* __restrict__ part,
+                                              unsigned* __restrict__ ticket,
+                                              double* __restrict__ out, int bid, int nblocks) {
   __shared__ double sh[kBlock];
   __shared__ bool last;
   const int tid = threadIdx.x;
@@ -21,16 +24,16 @@ __device__ __forceinline__ void grid_sum(double v, double* __restrict__ part,
     __syncthreads();
   }
   if (tid == 0) {
-    part[blockIdx.x] = sh[0];
+    part[bid] = sh[0];
     __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    last = atomicAdd(ticket, 1u) == (unsigned)nblocks - 1;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
   double acc = 0.0;
 #pragma unroll 8
-  for (int b = tid; b < (int)gridDim.x; b += kBlock) acc += __ldcg(part + b);
+  for (int b = tid; b < nblocks; b += kBlock) acc += __ldcg(part + b);
   sh[tid] = acc;
   __syncthreads();
 #pragma unroll
@@ -42,6 +45,12 @@ __device__ __forceinline__ void grid_sum(double v, double* __restrict__ part,
     *out = sh[0];
     *ticket = 0u;
   }
+}
+
+template <int kBlock>
+__device__ __forceinline__ void grid_sum(double v, double* __restrict__ part,
+                                         unsigned* __restrict__ ticket, double* __restrict__ out) {
+  grid_sum_part<kBlock>(v, part, ticket, out, blockIdx.x, gridDim.x);
 }
 
 }  // namespace ds

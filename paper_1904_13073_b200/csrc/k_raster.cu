@@ -10,12 +10,12 @@
 // in two atomic passes: pass 1 atomicMin on the fp64 depth bits (positive
 // doubles order like unsigned ints), pass 2 atomicMin on the index among the
 // writers whose depth equals the stored minimum.
+#include "ds_assoc.cuh"
+#include "ds_blend.cuh"
 #include "ds_context.cuh"
 
 namespace ds {
 namespace {
-
-constexpr int kEmptyIdx = 0x7f7f7f7f;
 
 struct CamParams {
   Rig w2c;
@@ -39,18 +39,39 @@ __global__ void k_any_stable(const float4* __restrict__ ln, int n, double delta_
 
 // list == nullptr: every surfel, eligibility tested here (raster.cpp:65-68);
 // list != nullptr: a precomputed render-eligible surfel list (solve loop)
-template <bool kPass2>
+// kWarp (pass 1 over a list): the surfel is first forward-warped
+// (warp_field.cpp:128-140, as k_forward_warp_list) and its live state written,
+// so the solve loop's warp + first splat pass are one launch.
+template <bool kPass2, bool kWarp = false>
 __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const int* __restrict__ list,
                                                      SplatParams sp,
                                                      const int* __restrict__ any_stable,
                                                      unsigned long long* pkey,
                                                      unsigned long long* skey, int* pidx,
-                                                     int* sidx) {
+                                                     int* sidx,
+                                                     const double4* __restrict__ warp_dq = nullptr) {
   const int k0 = blockIdx.x * blockDim.x + threadIdx.x;
   if (k0 >= n) return;
   const int i = list ? list[k0] : k0;
-  const float4 lp = m.lp[i];
-  const float4 ln = m.ln[i];
+  float4 lp, ln;
+  if (kWarp) {
+    const float4 rp = m.rp[i], rn = m.rn[i];
+    const Blend b = blend_entry(m.ki[i], m.kw[i], warp_dq);
+    lp = rp;
+    ln = rn;
+    if (!b.degenerate) {
+      const Rig T = blend_rig_fast(b);
+      const V3 p = rig_apply(T, v3(rp.x, rp.y, rp.z));
+      const V3 q = rig_rotate(T, v3(rn.x, rn.y, rn.z));
+      lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
+      ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
+    }
+    m.lp[i] = lp;
+    m.ln[i] = ln;
+  } else {
+    lp = m.lp[i];
+    ln = m.ln[i];
+  }
   if (!list) {
     const int2 t = m.t[i];
     const bool stable = (double)ln.w > sp.delta_stable;
@@ -110,20 +131,10 @@ __global__ void k_resolve_associate(const int* __restrict__ pidx, const int* __r
                                     int* __restrict__ n_pairs) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ap.P) return;
-  int win = pidx[c];
-  if (win == kEmptyIdx) win = sidx[c];
-  if (win == kEmptyIdx) win = -1;
+  const int win = resolve_winner(pidx, sidx, c);
   mm_idx[c] = win;
   if (!ap.associate) return;
-  int ps = -1;
-  if (win >= 0 && (fflag[c] & 2)) {
-    const double4 fv = fvert[c], fn = fnrm[c];
-    const V3 vd = rig_apply(ap.pose, v3(fv.x, fv.y, fv.z));
-    const V3 nd = rig_rotate(ap.pose, v3(fn.x, fn.y, fn.z));
-    const float4 lp = m.lp[win], ln = m.ln[win];
-    const V3 vm = v3(lp.x, lp.y, lp.z);
-    if (nrm(sub(vm, vd)) < 0.03 && dot(v3(ln.x, ln.y, ln.z), nd) > 0.7) ps = win;
-  }
+  const int ps = associate_pixel(c, win, m, fvert, fnrm, fflag, ap.pose);
   pair_s[c] = ps;
   const unsigned b = __ballot_sync(0xffffffffu, ps >= 0);
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(n_pairs, __popc(b));
@@ -184,10 +195,10 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
               c.cfg.delta_stable, &c.dsc->any_stable);
     DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 40.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(), n,
               (const int*)nullptr, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx,
-              c.mm_sidx);
+              c.mm_sidx, (const double4*)nullptr);
     DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 40.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
               (const int*)nullptr, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx,
-              c.mm_sidx);
+              c.mm_sidx, (const double4*)nullptr);
   }
   AssocParams ap;
   ap.pose = rig_load(associate ? assoc_pose : pose);
@@ -202,7 +213,8 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
 }
 
 void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
-                            const double* assoc_pose, const int* list, int n) {
+                            const double* assoc_pose, const int* list, int n,
+                            const double4* warp_dq, bool resolve) {
   const size_t P = c.P;
   DS_CUDA(cudaMemsetAsync(c.mm_pkey, 0xff, 8 * P, c.stream));
   DS_CUDA(cudaMemsetAsync(c.mm_skey, 0xff, 8 * P, c.stream));
@@ -216,17 +228,27 @@ void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
   sp.delta_stable = c.cfg.delta_stable;
   sp.host_bootstrap = (t_now - t_last <= c.cfg.delta_recent) ? 1 : 0;
   if (n > 0) {
-    DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(), n,
-              list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx);
+    auto k_warp_splat = k_model_splat<false, true>;
+    if (warp_dq)  // warp (96 B) + pass 1 (36 B) per listed surfel
+      DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 132.0 * n, cdiv(n, 256), 256, 0, k_warp_splat, c.M(), n,
+                list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx, warp_dq);
+    else
+      DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(),
+                n, list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
+                (const double4*)nullptr);
     DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
-              list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx);
+              list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
+              (const double4*)nullptr);
   }
-  AssocParams ap;
-  ap.pose = rig_load(assoc_pose);
-  ap.P = c.P;
-  ap.associate = 1;
-  DS_LAUNCH(c, KK_ASSOCIATE, 113.0 * c.P, cdiv(c.P, 256), 256, 0, k_resolve_associate, c.mm_pidx,
-            c.mm_sidx, c.M(), c.f_vert, c.f_nrm, c.f_flag, ap, c.mm_idx, c.pair_s, &c.dsc->n_pairs);
+  if (resolve) {
+    AssocParams ap;
+    ap.pose = rig_load(assoc_pose);
+    ap.P = c.P;
+    ap.associate = 1;
+    DS_LAUNCH(c, KK_ASSOCIATE, 113.0 * c.P, cdiv(c.P, 256), 256, 0, k_resolve_associate, c.mm_pidx,
+              c.mm_sidx, c.M(), c.f_vert, c.f_nrm, c.f_flag, ap, c.mm_idx, c.pair_s,
+              &c.dsc->n_pairs);
+  }
   std::copy(pose, pose + 12, c.mm_pose);
   c.mm_ready = true;
 }

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 
+#include "ds_assoc.cuh"
 #include "ds_blend.cuh"
 #include "ds_context.cuh"
 #include "ds_reduce.cuh"
@@ -82,25 +83,18 @@ __device__ __forceinline__ int pack_pairs(const int* __restrict__ pair_s, int P,
   return threadIdx.x < tot ? s_list[threadIdx.x] : -1;
 }
 
-// Per correspondence: residual, Jacobian rows (fp32), data energy partials.
-__global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair_s, ModelBuf m,
-                                                    const double4* __restrict__ node_dq,
-                                                    const double4* __restrict__ fvert,
-                                                    const double4* __restrict__ fnrm,
-                                                    PairParams pp, uint8_t* __restrict__ pair_ok,
-                                                    float* __restrict__ rows,
-                                                    double* __restrict__ pair_r,
-                                                    int* __restrict__ s_cnt,
-                                                    int* __restrict__ s_head,
-                                                    double* __restrict__ part,
-                                                    unsigned* __restrict__ ticket,
-                                                    double* __restrict__ out) {
-  __shared__ int s_list[256];
-  __shared__ int s_wcnt[8];
-  int n_valid;
-  const int c = pack_pairs(pair_s, pp.P, s_list, s_wcnt, n_valid);
+// Per correspondence (pixel c, surfel s): residual, Jacobian rows (fp32),
+// pair list bookkeeping; returns the data energy term r^2 (0 if degenerate).
+__device__ __forceinline__ double pair_term_one(int c, int s, const ModelBuf& m,
+                                                const double4* __restrict__ node_dq,
+                                                const double4* __restrict__ fvert,
+                                                const double4* __restrict__ fnrm,
+                                                const PairParams& pp, uint8_t* __restrict__ pair_ok,
+                                                float* __restrict__ rows,
+                                                double* __restrict__ pair_r,
+                                                int* __restrict__ s_cnt,
+                                                int* __restrict__ s_head) {
   double e = 0.0;
-  int s = c >= 0 ? pair_s[c] : -1;
   if (s >= 0) {
     const Blend b = blend_entry(m.ki[s], m.kw[s], node_dq);
     if (b.degenerate) {
@@ -177,6 +171,51 @@ __global__ void __launch_bounds__(256) k_pair_terms(const int* __restrict__ pair
       atomicMin(s_head + s, c);
     }
   }
+  return e;
+}
+
+// Fused model-map resolve + association (raster.cpp:104-119, solver.cpp:244-271)
+// + per-pair terms: the pixel's winner and correspondence are decided in
+// registers, the CTA packs its paired pixels and evaluates their terms.
+__global__ void __launch_bounds__(256) k_assoc_pair_terms(
+    const int* __restrict__ pidx, const int* __restrict__ sidx, const uint8_t* __restrict__ fflag,
+    ModelBuf m, const double4* __restrict__ node_dq, const double4* __restrict__ fvert,
+    const double4* __restrict__ fnrm, PairParams pp, int* __restrict__ mm_idx,
+    int* __restrict__ pair_s, int* __restrict__ n_pairs, uint8_t* __restrict__ pair_ok,
+    float* __restrict__ rows, double* __restrict__ pair_r, int* __restrict__ s_cnt,
+    int* __restrict__ s_head, double* __restrict__ part, unsigned* __restrict__ ticket,
+    double* __restrict__ out) {
+  __shared__ int s_pix[256], s_srf[256];
+  __shared__ int s_wcnt[8];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  int ps = -1;
+  if (c < pp.P) {
+    const int win = resolve_winner(pidx, sidx, c);
+    mm_idx[c] = win;
+    ps = associate_pixel(c, win, m, fvert, fnrm, fflag, pp.pose);
+    pair_s[c] = ps;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, ps >= 0);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_wcnt[wid] = __popc(bal);
+    if (bal) atomicAdd(n_pairs, __popc(bal));
+  }
+  __syncthreads();
+  int off = 0;
+  for (int w = 0; w < wid; ++w) off += s_wcnt[w];
+  if (ps >= 0) {
+    const int k = off + __popc(bal & ((1u << lane) - 1u));
+    s_pix[k] = c;
+    s_srf[k] = ps;
+  }
+  __syncthreads();
+  int tot = 0;
+  for (int w = 0; w < 8; ++w) tot += s_wcnt[w];
+  const int pc = threadIdx.x < tot ? s_pix[threadIdx.x] : -1;
+  const int sc = threadIdx.x < tot ? s_srf[threadIdx.x] : -1;
+  const double e = pair_term_one(pc, sc, m, node_dq, fvert, fnrm, pp, pair_ok, rows, pair_r, s_cnt,
+                                 s_head);
   grid_sum<256>(e, part, ticket, out);  // data energy, fixed order
 }
 
@@ -246,6 +285,58 @@ __global__ void __launch_bounds__(256) k_reg_energy(const double4* __restrict__ 
     }
   }
   grid_sum<256>(v, part, ticket, out);
+}
+
+// E_post of an LM attempt in one launch: blocks [0, nbp) evaluate E_data over
+// the pair set (solver.cpp:132-143), blocks [nbp, nbp + nbe) E_reg over the
+// directed edges (solver.cpp:145-155); two independent fixed-order sums.
+__global__ void __launch_bounds__(256) k_energy(const int* __restrict__ pair_s, ModelBuf m,
+                                                const double4* __restrict__ node_dq,
+                                                const double4* __restrict__ fvert,
+                                                const double4* __restrict__ fnrm, PairParams pp,
+                                                const double4* __restrict__ pos,
+                                                const int* __restrict__ nbr,
+                                                const double* __restrict__ se3, int N, int nbp,
+                                                double* __restrict__ part,
+                                                unsigned* __restrict__ tickets,
+                                                double* __restrict__ e_data,
+                                                double* __restrict__ e_reg) {
+  if ((int)blockIdx.x < nbp) {
+    __shared__ int s_list[256];
+    __shared__ int s_wcnt[8];
+    int n_valid;
+    const int c = pack_pairs(pair_s, pp.P, s_list, s_wcnt, n_valid);
+    double e = 0.0;
+    const int s = c >= 0 ? pair_s[c] : -1;
+    if (s >= 0) {
+      const Blend b = blend_entry(m.ki[s], m.kw[s], node_dq);
+      if (!b.degenerate) {
+        const float4 rp = m.rp[s];
+        const double4 fv = fvert[c], fn = fnrm[c];
+        const V3 vd = rig_apply(pp.pose, v3(fv.x, fv.y, fv.z));
+        const V3 nd = rig_rotate(pp.pose, v3(fn.x, fn.y, fn.z));
+        const V3 y = rig_apply(blend_rig_fast(b), v3(rp.x, rp.y, rp.z));
+        const double r = dot(nd, sub(y, vd));
+        e = r * r;
+      }
+    }
+    grid_sum_part<256>(e, part, tickets + 0, e_data, blockIdx.x, nbp);
+  } else {
+    const int bid = blockIdx.x - nbp, nbe = gridDim.x - nbp;
+    const int e = bid * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    if (e < 8 * N) {
+      const int i = nbr[e];
+      if (i >= 0) {
+        const int j = e >> 3;
+        const double4 pj = pos[j];
+        const V3 p = v3(pj.x, pj.y, pj.z);
+        const Rig Tj = rig_load(se3 + 12 * j), Ti = rig_load(se3 + 12 * i);
+        v = sqn(sub(rig_apply(Tj, p), rig_apply(Ti, p)));
+      }
+    }
+    grid_sum_part<256>(v, part + nbp, tickets + 1, e_reg, bid, nbe);
+  }
 }
 
 __global__ void k_any_stable_flag(const float4* __restrict__ ln, int n, double delta_stable,
@@ -1049,6 +1140,7 @@ template <bool kPipe>
 __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
   cg::grid_group grid = cg::this_grid();
   pcg_mark(a, 0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.sc->finite = 1;  // before any barrier
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double4 sh[kPcgWarps + 1];
   __shared__ int s_rng[4];
@@ -1307,7 +1399,12 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
       pnew = t;
     }
   }
-  for (int k = tid; k < n6; k += kPcgThreads) a.x[6 * (size_t)r0 + k] = X[k];
+  bool bad = false;  // non-finite increment -> LM reject (solver.cpp:387)
+  for (int k = tid; k < n6; k += kPcgThreads) {
+    a.x[6 * (size_t)r0 + k] = X[k];
+    bad |= !isfinite(X[k]);
+  }
+  if (bad) atomicExch(&a.sc->finite, 0);
   pcg_mark(a, 63);
   if (blockIdx.x == 0 && tid == 0) {
     a.sc->pcg_iters = it;
@@ -1375,10 +1472,6 @@ __global__ void __launch_bounds__(256) k_bsr_spmv_rows(const int* __restrict__ r
   if (lane < 6) y[6 * j + lane] = tot + mu * x[6 * j + lane];
 }
 
-__global__ void k_check_finite(const double* __restrict__ x, int n, int* __restrict__ finite) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && !isfinite(x[i])) atomicAnd(finite, 0);
-}
 
 }  // namespace
 
@@ -1493,20 +1586,23 @@ PairParams pair_params(Ctx& c, const double* pose) {
 // e_reg, ginf, |g|^2 (in pcg_rr slot) and tr(H) in DevScalars (no host sync).
 void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor) {
   const int n = c.n_surfels, N = c.n_nodes, P = c.P;
-  // only render-eligible surfels can be drawn / paired during the solve; the
-  // post-solve forward_warp (pipeline.cpp:108) rewrites every live surfel
-  forward_warp_list(c, c.elig, c.n_elig);
-  render_model_maps_list(c, pose, t_now, t_last, pose, c.elig, c.n_elig);
   DS_CUDA(cudaMemsetAsync(c.s_cnt, 0, sizeof(int) * (n + 1), c.stream));
   DS_CUDA(cudaMemsetAsync(c.s_head, 0x7f, sizeof(int) * (n + 1), c.stream));
   DS_CUDA(cudaMemsetAsync(c.s_fill, 0, sizeof(int) * (n + 1), c.stream));
   DS_CUDA(cudaMemsetAsync(&c.dsc->pair_list_n, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
+  // only render-eligible surfels can be drawn / paired during the solve (the
+  // post-solve forward_warp, pipeline.cpp:108, rewrites every live surfel):
+  // warp + splat pass 1 fused, splat pass 2, then resolve + associate + terms
+  render_model_maps_list(c, pose, t_now, t_last, pose, c.elig, c.n_elig, c.node_dq, false);
   const int nbp = cdiv(P, 256);
-  // per pixel: pair id 4 B, surfel ref + skin 48 B, frame maps 64 B, rows 96 B + r 8 B out
-  DS_LAUNCH(c, KK_PAIR_TERMS, 220.0 * P, nbp, 256, 0, k_pair_terms, c.pair_s, c.M(), c.node_dq,
-            c.f_vert, c.f_nrm, pair_params(c, pose), c.pair_ok, c.pair_rows, c.pair_r, c.s_cnt,
-            c.s_head, c.red_part, c.tickets + 0, &c.dsc->e_data_pre);
+  // per pixel: 2 x 4 B winner ids, frame maps 65 B, winner live 32 B, ids out 8 B; per pair:
+  // surfel ref + skin 48 B, rows 96 B + r 8 B out
+  DS_LAUNCH(c, KK_PAIR_TERMS, 113.0 * P + 152.0 * c.n_pairs_ok_est, nbp, 256, 0,
+            k_assoc_pair_terms, c.mm_pidx, c.mm_sidx, c.f_flag, c.M(), c.node_dq, c.f_vert,
+            c.f_nrm, pair_params(c, pose), c.mm_idx, c.pair_s, &c.dsc->n_pairs, c.pair_ok,
+            c.pair_rows, c.pair_r, c.s_cnt, c.s_head, c.red_part, c.tickets + 0,
+            &c.dsc->e_data_pre);
   DS_LAUNCH(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_reserve, c.pair_s, c.pair_ok, P,
             c.s_cnt, c.s_head, c.s_base, &c.dsc->pair_list_n);
   DS_LAUNCH(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_fill, c.pair_s, c.pair_ok, P, c.s_cnt,
@@ -1602,9 +1698,7 @@ void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   DS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPcgThreads), args, kPcgSmem, c.stream));
   // algorithmic bytes per PCG: per iteration one BSR SpMV (148 B/block + vectors)
   launch_end(c, KK_PCG, std::max(1, max_iters) * (148.0 * c.n_full + 6.0 * 8 * 8 * N));
-  DS_CUDA(cudaMemsetAsync(&c.dsc->finite, 0xff, sizeof(int), c.stream));
-  DS_LAUNCH(c, KK_MISC, 48.0 * N, cdiv(6 * N, 256), 256, 0, k_check_finite, c.pcg_x, 6 * N,
-            &c.dsc->finite);
+
 }
 
 void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double* rel_res) {
@@ -1623,12 +1717,10 @@ namespace {
 void energy_async(Ctx& c, const double* pose, const double4* dq, double* se3) {
   const int N = c.n_nodes, P = c.P;
   const int nbp = cdiv(P, 256), nbe = cdiv(8 * N, 256);
-  DS_LAUNCH(c, KK_ENERGY, 120.0 * P * 0.5, nbp, 256, 0, k_pair_energy, c.pair_s, c.M(), dq,
-            c.f_vert, c.f_nrm, pair_params(c, pose), 0, c.red_part, (int*)nullptr, c.tickets + 0,
-            &c.dsc->e_data);
-  node_se3(c, dq, se3);
-  DS_LAUNCH(c, KK_ENERGY, 200.0 * N, nbe, 256, 0, k_reg_energy, c.node_pos, c.node_nbr, se3, N,
-            c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg, (double*)nullptr);
+  // the node transforms `se3` of `dq` are written by apply_increments (fused)
+  DS_LAUNCH(c, KK_ENERGY, 120.0 * c.n_pairs_ok_est + 200.0 * N, nbp + nbe, 256, 0, k_energy,
+            c.pair_s, c.M(), dq, c.f_vert, c.f_nrm, pair_params(c, pose), c.node_pos, c.node_nbr,
+            se3, N, nbp, c.red_part, c.tickets, &c.dsc->e_data, &c.dsc->e_reg);
 }
 }  // namespace
 
@@ -1637,12 +1729,12 @@ namespace {
 void gn_step_async(Ctx& c, const double* pose, int t_now, int t_last, int max_pcg, double tol) {
   gn_linearize_async(c, pose, t_now, t_last, true);  // + LM floor on mu
   pcg_solve_async(c, max_pcg, tol);
-  apply_increments(c, c.pcg_x, c.node_dq_cand);
+  apply_increments(c, c.pcg_x, c.node_dq_cand, c.node_se3_cand);
   energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
 }
 void attempt_async(Ctx& c, const double* pose, int max_pcg, double tol) {
   pcg_solve_async(c, max_pcg, tol);
-  apply_increments(c, c.pcg_x, c.node_dq_cand);
+  apply_increments(c, c.pcg_x, c.node_dq_cand, c.node_se3_cand);
   energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
 }
 

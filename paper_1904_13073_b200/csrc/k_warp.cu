@@ -85,8 +85,10 @@ __global__ void k_node_live(const double4* __restrict__ pos, const double4* __re
   atomicMax(rmax_bits, __float_as_int(__double2float_ru(m)));
 }
 
+// se3 (optional): the new transforms' to_se3 cache (geometry.cpp:86-93) for
+// the energy evaluation, fused here instead of a separate k_node_se3 launch
 __global__ void k_apply_increments(const double4* __restrict__ dq, const double* __restrict__ delta,
-                                   int n, double4* __restrict__ out) {
+                                   int n, double4* __restrict__ out, double* __restrict__ se3) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const double* d = delta + 6 * j;
@@ -97,14 +99,15 @@ __global__ void k_apply_increments(const double4* __restrict__ dq, const double*
   const DQ o = dq_normalized(dq_mul(inc, q));
   out[2 * j] = make_double4(o.r.w, o.r.x, o.r.y, o.r.z);
   out[2 * j + 1] = make_double4(o.d.w, o.d.x, o.d.y, o.d.z);
+  if (se3) rig_store(dq_to_rig(o), se3 + 12 * j);
 }
 
 }  // namespace
 
-void apply_increments(Ctx& c, const double* delta, double4* out) {
+void apply_increments(Ctx& c, const double* delta, double4* out, double* se3) {
   if (c.n_nodes == 0) return;
-  DS_LAUNCH(c, KK_NODE_UPDATE, 112.0 * c.n_nodes, cdiv(c.n_nodes, 128), 128, 0,
-            k_apply_increments, c.node_dq, delta, c.n_nodes, out);
+  DS_LAUNCH(c, KK_NODE_UPDATE, (se3 ? 208.0 : 112.0) * c.n_nodes, cdiv(c.n_nodes, 128), 128, 0,
+            k_apply_increments, c.node_dq, delta, c.n_nodes, out, se3);
 }
 
 int forward_warp(Ctx& c, bool count_degenerate) {

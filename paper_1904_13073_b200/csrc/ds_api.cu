@@ -270,6 +270,8 @@ void allocate(Ctx& c) {
   DS_CUDA(cudaMallocHost(&c.h_mu, sizeof(double)));
   DS_CUDA(cudaMallocHost(&c.h_int, 4 * sizeof(int)));
   if (const char* e = std::getenv("DS_NO_GRAPHS")) c.use_graphs = e[0] == '0';
+  if (const char* e = std::getenv("DS_HOST_LM")) c.device_lm = e[0] == '0';
+  c.trace_host = std::getenv("DS_TRACE_HOST") != nullptr;
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));
   DS_CUDA(cudaMemsetAsync(c.node_nbr, 0xff, sizeof(int) * 8 * N, c.stream));
 }
@@ -287,6 +289,7 @@ void release(Ctx& c) {
   if (c.h_int) cudaFreeHost(c.h_int);
   if (c.g_step.exec) cudaGraphExecDestroy(c.g_step.exec);
   if (c.g_attempt.exec) cudaGraphExecDestroy(c.g_attempt.exec);
+  if (c.g_solve.exec) cudaGraphExecDestroy(c.g_solve.exec);
   if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
 }
 

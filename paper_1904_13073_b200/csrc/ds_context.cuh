@@ -86,6 +86,11 @@ struct DevScalars {
   double e_data, e_reg, ginf, htrace;
   double e_data_pre, e_reg_pre, g_sq, mu, mu_floor;
   double pcg_rr, pcg_rr0, mean_abs_r, rigid_abs;
+  // device-resident LM loop (solver.cpp:296-406 state, k_lm_decide)
+  int lm_iter, lm_attempt, lm_relin, lm_done;
+  int lm_accepted, lm_attempts_total, pcg_iter_total, lm_rounds;
+  int lm_relins, lm_pairs, _pad_lm0, _pad_lm1;
+  double lm_e_pre, lm_gnorm, lm_initial, lm_final;
   double rigid_pose[12];
 };
 
@@ -94,6 +99,7 @@ enum DevErr { DERR_NODE_CAP = 1, DERR_HASH_CELL = 2, DERR_HASH_FULL = 4, DERR_BL
 struct GraphSlot {
   cudaGraphExec_t exec = nullptr;
   int64_t kernels = 0;  // kernel launches per replay (accounting)
+  int64_t kernels_lin = 0;  // device LM loop: kernels per linearisation round
 };
 
 struct ProfRec {
@@ -254,7 +260,9 @@ struct Ctx {
   int lm_attempts = 0, pcg_iterations = 0;
   // CUDA graphs of the GN step / LM attempt (re-captured per frame, updated in place)
   bool use_graphs = true;
-  GraphSlot g_step, g_attempt;
+  bool trace_host = false;  // DS_TRACE_HOST: host-side timing prints
+  bool device_lm = true;  // LM loop as a device-side WHILE graph (DS_HOST_LM=1: host loop)
+  GraphSlot g_step, g_attempt, g_solve;
   double* h_mu = nullptr;  // pinned staging for mu
   int* h_int = nullptr;    // pinned staging for small ints
 

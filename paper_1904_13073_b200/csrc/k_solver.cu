@@ -23,6 +23,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 
 #include "ds_assoc.cuh"
 #include "ds_blend.cuh"
@@ -1738,6 +1740,186 @@ void attempt_async(Ctx& c, const double* pose, int max_pcg, double tol) {
   energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
 }
 
+// ------------------------------------------------------ device-resident LM
+// The LM loop of solver.cpp:296-406 as device state, one decision per attempt
+// (same arithmetic as the host loop below): a WHILE graph node repeats
+// [IF(relinearise) {linearise + mu floor}; PCG; candidate; E_post; decide].
+struct LmParams {
+  double lambda, tol;
+  int max_gn_iters, N;
+  cudaGraphConditionalHandle h_loop, h_relin;
+};
+
+__global__ void k_lm_init(DevScalars* sc) {
+  sc->mu = 0.0;  // solver.cpp:313
+  sc->lm_iter = 0;
+  sc->lm_attempt = 0;
+  sc->lm_relin = 1;
+  sc->lm_done = 0;
+  sc->lm_accepted = 0;
+  sc->lm_attempts_total = 0;
+  sc->pcg_iter_total = 0;
+  sc->lm_rounds = 0;
+  sc->lm_relins = 0;
+  sc->lm_pairs = 0;
+  sc->lm_initial = 0.0;
+  sc->lm_final = 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_lm_decide(DevScalars* sc, LmParams lp,
+                                                   double4* __restrict__ node_dq,
+                                                   const double4* __restrict__ node_dq_cand) {
+  __shared__ int s_acc;
+  if (threadIdx.x == 0) {
+    ++sc->lm_rounds;
+    bool done = false, accepted = false;
+    double mu = sc->mu;
+    const double floor_ = sc->mu_floor;
+    if (sc->lm_relin) {  // a GN iteration started this round (solver.cpp:316-379)
+      ++sc->lm_relins;
+      const double e_pre = sc->e_data_pre + lp.lambda * sc->e_reg_pre;
+      sc->lm_e_pre = e_pre;
+      sc->lm_pairs = sc->n_pairs;
+      if (sc->lm_iter == 0) {
+        sc->lm_initial = e_pre;
+        sc->lm_final = e_pre;
+      }
+      sc->lm_gnorm = sqrt(sc->g_sq);
+      sc->lm_attempt = 0;
+      if (sc->ginf < 1e-14) done = true;  // stationary: the attempt is discarded
+    }
+    if (!done) {
+      ++sc->lm_attempts_total;
+      sc->pcg_iter_total += sc->pcg_iters;
+      const bool finite = sc->finite != 0;
+      const double rr = sqrt(sc->pcg_rr), rr0 = sqrt(sc->pcg_rr0);
+      const bool guard_fail = lp.tol > 0 && rr > 1e-6 * (sc->lm_gnorm + 1.0) && rr > lp.tol * rr0;
+      double e_post = 0.0;
+      if (!finite || guard_fail) {
+        mu = fmax(floor_, mu * 10.0);
+      } else {
+        e_post = sc->e_data + lp.lambda * sc->e_reg;
+        if (e_post <= sc->lm_e_pre) accepted = true;
+        else mu = fmax(floor_, mu * 10.0);
+      }
+      ++sc->lm_attempt;
+      if (accepted) {
+        mu = fmax(floor_, mu * 0.1);
+        ++sc->lm_accepted;
+        sc->lm_final = e_post;
+        ++sc->lm_iter;
+        const double e_pre = sc->lm_e_pre;
+        done = (e_pre - e_post < 1e-4 * fmax(e_pre, 1e-300)) || sc->lm_iter >= lp.max_gn_iters;
+      } else if (sc->lm_attempt >= 8) {
+        done = true;  // no acceptable step (solver.cpp:403)
+      }
+    }
+    sc->mu = mu;
+    sc->lm_relin = accepted ? 1 : 0;
+    sc->lm_done = done ? 1 : 0;
+    cudaGraphSetConditional(lp.h_loop, done ? 0u : 1u);
+    cudaGraphSetConditional(lp.h_relin, accepted ? 1u : 0u);
+    s_acc = accepted ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_acc)  // T <- T_cand (solver.cpp:399)
+    for (int k = threadIdx.x; k < 2 * lp.N; k += blockDim.x) node_dq[k] = node_dq_cand[k];
+}
+
+// Build the per-frame solve graph: WHILE(loop) { IF(relin) {linearise}; attempt; decide }.
+bool build_solve_graph(Ctx& c, const double* pose, int t_now, int t_last, int max_pcg,
+                       double tol) {
+  cudaGraph_t g = nullptr;
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return false;
+  bool ok = true;
+  const int64_t l0 = c.total_launches;
+  auto fail_ = [&]() {
+    cudaGetLastError();
+    c.total_launches = l0;
+    if (g) cudaGraphDestroy(g);
+    return false;
+  };
+  cudaGraphConditionalHandle h_loop, h_relin;
+  if (cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+    return fail_();
+  cudaGraphNodeParams pw = {};
+  pw.type = cudaGraphNodeTypeConditional;
+  pw.conditional.handle = h_loop;
+  pw.conditional.type = cudaGraphCondTypeWhile;
+  pw.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  if (cudaGraphAddNode(&wnode, g, nullptr, 0, &pw) != cudaSuccess) return fail_();
+  cudaGraph_t body = pw.conditional.phGraph_out[0];
+  if (cudaGraphConditionalHandleCreate(&h_relin, body, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+    return fail_();
+  cudaGraphNodeParams pi = {};
+  pi.type = cudaGraphNodeTypeConditional;
+  pi.conditional.handle = h_relin;
+  pi.conditional.type = cudaGraphCondTypeIf;
+  pi.conditional.size = 1;
+  cudaGraphNode_t inode;
+  if (cudaGraphAddNode(&inode, body, nullptr, 0, &pi) != cudaSuccess) return fail_();
+  cudaGraph_t lin = pi.conditional.phGraph_out[0];
+  cudaGraph_t tmp = nullptr;
+  // linearisation round
+  if (cudaStreamBeginCaptureToGraph(c.stream, lin, nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return fail_();
+  try {
+    gn_linearize_async(c, pose, t_now, t_last, true);
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &tmp);
+    fail_();
+    throw;
+  }
+  ok = cudaStreamEndCapture(c.stream, &tmp) == cudaSuccess;
+  const int64_t k_lin = c.total_launches - l0;
+  if (!ok) return fail_();
+  // attempt + decision
+  if (cudaStreamBeginCaptureToGraph(c.stream, body, &inode, nullptr, 1,
+                                    cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return fail_();
+  LmParams lp;
+  lp.lambda = c.cfg.lambda;
+  lp.tol = tol;
+  lp.max_gn_iters = c.cfg.max_gn_iters;
+  lp.N = c.n_nodes;
+  lp.h_loop = h_loop;
+  lp.h_relin = h_relin;
+  try {
+    pcg_solve_async(c, max_pcg, tol);
+    apply_increments(c, c.pcg_x, c.node_dq_cand, c.node_se3_cand);
+    energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
+    DS_LAUNCH(c, KK_MISC, 64.0 * 2 * c.n_nodes, 1, 256, 0, k_lm_decide, c.dsc, lp, c.node_dq,
+              c.node_dq_cand);
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &tmp);
+    fail_();
+    throw;
+  }
+  ok = cudaStreamEndCapture(c.stream, &tmp) == cudaSuccess;
+  if (!ok) return fail_();
+  c.g_solve.kernels_lin = k_lin;
+  c.g_solve.kernels = c.total_launches - l0 - k_lin;
+  c.total_launches = l0;
+  if (c.g_solve.exec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(c.g_solve.exec, g, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(c.g_solve.exec);
+      c.g_solve.exec = nullptr;
+    }
+  }
+  if (!c.g_solve.exec && cudaGraphInstantiate(&c.g_solve.exec, g, 0) != cudaSuccess) {
+    cudaGetLastError();
+    c.g_solve.exec = nullptr;
+    cudaGraphDestroy(g);
+    return false;
+  }
+  cudaGraphDestroy(g);
+  return true;
+}
+
 // Capture `enqueue` into `slot` (update the executable graph in place when the
 // topology is unchanged; re-instantiate otherwise). Returns false if the stream
 // cannot be captured (the caller then launches directly).
@@ -1810,10 +1992,35 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
   const int max_pcg = c.cfg.pcg_max_iters > 0 ? c.cfg.pcg_max_iters : 10;
   const double tol = c.cfg.pcg_tol;
   const bool graphs = c.use_graphs && !c.cfg.profile;
+  int n_pairs = 0;
+  if (graphs && c.device_lm && c.cfg.max_gn_iters > 0) {
+    // the whole LM loop on the device: one graph launch, one host sync
+    DS_LAUNCH(c, KK_MISC, 64.0, 1, 1, 0, k_lm_init, c.dsc);
+    const auto tb0 = std::chrono::steady_clock::now();
+    const bool built = build_solve_graph(c, pose, t_now, t_last, max_pcg, tol);
+    if (c.trace_host)
+      std::fprintf(stderr, "solve graph build %.1f us\n",
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tb0)
+                       .count());
+    if (built) {
+      DS_CUDA(cudaGraphLaunch(c.g_solve.exec, c.stream));
+      fetch_scalars(c);
+      const DevScalars& h = *c.hsc;
+      c.total_launches += c.g_solve.kernels_lin * h.lm_relins + c.g_solve.kernels * h.lm_rounds;
+      c.lm_attempts = h.lm_attempts_total;
+      c.pcg_iterations = h.pcg_iter_total;
+      rep.iterations = h.lm_accepted;
+      rep.initial_energy = h.lm_initial;
+      rep.final_energy = h.lm_final;
+      n_pairs = h.lm_pairs;
+      c.n_pairs_ok_est = n_pairs;
+      goto report;
+    }
+  }
+  {
   bool have_step = false, have_attempt = false;
   double mu = 0.0;
   set_mu(c, 0.0);
-  int n_pairs = 0;
   for (int iter = 0; iter < c.cfg.max_gn_iters; ++iter) {
     if (graphs && !have_step)
       have_step = capture(c, c.g_step, [&] { gn_step_async(c, pose, t_now, t_last, max_pcg, tol); });
@@ -1865,6 +2072,8 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
     rep.final_energy = e_post;
     if (e_pre - e_post < 1e-4 * std::max(e_pre, 1e-300)) break;
   }
+  }
+report:
   rep.correspondences = n_pairs;
   // mean |r| at the final nodes over the last pair set (solver.cpp:409-420)
   const int nbp = cdiv(c.P, 256);

@@ -253,6 +253,17 @@ void allocate(Ctx& c) {
   c.keep = dalloc<int>(c, S + P + 1);
   c.keep_scan = dalloc<int>(c, S + P + 1);
   c.ext_pos = dalloc<float4>(c, P);
+  for (KnnGrid* g : {&c.grid_ref, &c.grid_live}) {
+    int slots = 1;
+    while (slots < 2 * std::min(c.N_cap, kKnnMaxPoints)) slots <<= 1;
+    g->key = dalloc<long long>(c, slots);
+    g->range = dalloc<int2>(c, slots);
+    g->ids = dalloc<int>(c, std::min(c.N_cap, kKnnMaxPoints));
+    g->prm = dalloc<double>(c, 8);
+    g->pslot = dalloc<int>(c, std::min(c.N_cap, kKnnMaxPoints));
+    g->fill = dalloc<int>(c, slots);
+    g->mask = slots - 1;
+  }
   c.ht_key = dalloc<long long>(c, c.HT);
   c.ht_cnt = dalloc<int>(c, c.HT);
   c.ht_ids = dalloc<int>(c, 8 * (size_t)c.HT);

@@ -107,6 +107,19 @@ struct ProfRec {
   cudaEvent_t a, b;
 };
 
+// Uniform-grid index over a node set (ds_knn.cuh / k_knn.cu).
+constexpr int kKnnMaxPoints = 1 << 20;  // grid index capacity (points)
+struct KnnGrid {
+  long long* key = nullptr;
+  int2* range = nullptr;
+  int* ids = nullptr;
+  double* prm = nullptr;
+  int* pslot = nullptr;  // build scratch: slot of every point
+  int* fill = nullptr;   // build scratch: per-slot scatter counters
+  int mask = 0;
+  bool valid = false;
+};
+
 struct Ctx {
   ds_config cfg{};
   int device = 0;
@@ -226,6 +239,7 @@ struct Ctx {
   int* keep_scan = nullptr;
   float4* ext_pos = nullptr;  // uncovered extension candidates (ordered)
   // greedy node hash
+  KnnGrid grid_ref, grid_live;  // reference / live node positions
   long long* ht_key = nullptr;
   int* ht_cnt = nullptr;
   int* ht_ids = nullptr;
@@ -305,7 +319,8 @@ void node_se3(Ctx& c, const double4* dq, double* se3);
 void node_live_positions(Ctx& c);
 void apply_increments(Ctx& c, const double* delta, double4* out, double* se3 = nullptr);  // solver.cpp:277-286
 void init_warp_field(Ctx& c);
-void compute_node_edges(Ctx& c);
+void compute_node_edges(Ctx& c, bool build_grid = true);
+bool build_knn_grid(Ctx& c, KnnGrid& g, const double4* pos, int n, double h);
 int extend_warp_field(Ctx& c, const float4* positions, int n);  // returns appended
 void update_skinning_incremental(Ctx& c, int first_new);
 

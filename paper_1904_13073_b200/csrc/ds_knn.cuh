@@ -1,0 +1,148 @@
+// ds_knn.cuh — exact K-nearest-node queries on a uniform grid (the device
+// counterpart of VoxelGrid, spatial_grid.hpp:16-136).
+//
+// The grid is rebuilt whenever the point set changes (k_knn_build, one CTA):
+// cell size h, cells keyed by packed integer coordinates, node ids sorted by
+// cell, an open-addressing table cell -> (start, count). A query walks
+// Chebyshev shells r = 0, 1, 2, ... around its cell; every point outside the
+// shells walked so far lies in a cell at Chebyshev distance >= r + 1, hence at
+// Euclidean distance >= r h from the query (the query lies inside its own
+// cell). Once the K-th best squared distance is below (r h)^2 (with a rounding
+// margin) no unvisited point can enter the top K, so the result is the exact
+// (d^2, index) top K of the brute-force scan -- same fp64 distances, same total
+// order (spatial_grid.hpp:21-23).
+#pragma once
+#include "ds_context.cuh"
+#include "ds_math.cuh"
+
+namespace ds {
+
+constexpr long long kKnnEmpty = -1LL;
+constexpr int kKnnOff = 1 << 20;  // coordinate offset (queries may lie outside the box)
+
+struct KnnGridView {
+  const long long* key;  // slot -> packed cell key, kKnnEmpty if free
+  const int2* range;     // slot -> (start, count) into ids
+  const int* ids;        // point ids sorted by cell
+  const double* prm;     // lo.x, lo.y, lo.z, h, 1/h
+  int mask;              // slots - 1
+  int max_ring;          // shells walked before giving up (then brute force)
+};
+
+inline KnnGridView knn_view(const KnnGrid& g, int max_ring) {
+  KnnGridView v;
+  v.key = g.key;
+  v.range = g.range;
+  v.ids = g.ids;
+  v.prm = g.prm;
+  v.mask = g.mask;
+  v.max_ring = max_ring;
+  return v;
+}
+
+__device__ __forceinline__ long long knn_pack(int cx, int cy, int cz) {
+  return ((long long)(cx + kKnnOff) << 42) | ((long long)(cy + kKnnOff) << 21) |
+         (long long)(cz + kKnnOff);
+}
+__device__ __forceinline__ unsigned knn_hash(long long k) {
+  unsigned long long x = (unsigned long long)k * 0x9E3779B97F4A7C15ull;
+  return (unsigned)(x >> 32);
+}
+__device__ __forceinline__ int2 knn_find(const KnnGridView& g, long long k) {
+  unsigned s = knn_hash(k) & g.mask;
+  for (int probe = 0; probe <= g.mask; ++probe) {
+    const long long v = __ldg(g.key + s);
+    if (v == k) return __ldg(g.range + s);
+    if (v == kKnnEmpty) return make_int2(0, 0);
+    s = (s + 1) & g.mask;
+  }
+  return make_int2(0, 0);
+}
+
+// sorted (d2, index) insertion into a top-K list
+template <int K>
+__device__ __forceinline__ void knnk_insert(double d2, int j, double bd[K], int bi[K]) {
+  if (!nb_less(d2, j, bd[K - 1], bi[K - 1])) return;
+  double cd = d2;
+  int ci = j;
+#pragma unroll
+  for (int s = 0; s < K; ++s)
+    if (nb_less(cd, ci, bd[s], bi[s])) {
+      const double td = bd[s];
+      const int ti = bi[s];
+      bd[s] = cd;
+      bi[s] = ci;
+      cd = td;
+      ci = ti;
+    }
+}
+
+// top-K of the union of the per-lane lists of an aligned LANES group (disjoint
+// point subsets), written to (md, mi) in every lane; the per-lane lists stay.
+template <int K, int LANES>
+__device__ __forceinline__ void knnk_merged(const double bd[K], const int bi[K], double md[K],
+                                            int mi[K]) {
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    md[s] = bd[s];
+    mi[s] = bi[s];
+  }
+  // only the group's lanes take part: groups of a warp may be at different
+  // shells of their own queries
+  const unsigned gmask =
+      LANES >= 32 ? 0xffffffffu
+                  : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(unsigned)(LANES - 1)));
+#pragma unroll
+  for (int off = LANES / 2; off > 0; off >>= 1) {
+    double od[K];
+    int oi[K];
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      od[s] = __shfl_xor_sync(gmask, md[s], off);
+      oi[s] = __shfl_xor_sync(gmask, mi[s], off);
+    }
+#pragma unroll
+    for (int s = 0; s < K; ++s) knnk_insert<K>(od[s], oi[s], md, mi);
+  }
+}
+
+// Exact top-K of the points `pos` (x, y, z in double4) around x by (d2, id),
+// ids accepted by `keep(id)`; LANES lanes of an aligned group cooperate (every
+// lane of the group must call it). Returns false if the shell limit was hit
+// before the result was certain (caller falls back to brute force).
+template <int K, int LANES, class Keep>
+__device__ bool knn_grid_query(const KnnGridView& g, const double4* __restrict__ pos, V3 x,
+                               Keep keep, double md[K], int mi[K]) {
+  const int lane = threadIdx.x & (LANES - 1);
+  const double lox = g.prm[0], loy = g.prm[1], loz = g.prm[2], h = g.prm[3], ih = g.prm[4];
+  const int cx = (int)floor((x.x - lox) * ih), cy = (int)floor((x.y - loy) * ih),
+            cz = (int)floor((x.z - loz) * ih);
+  double bd[K];
+  int bi[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    bd[s] = INFINITY;
+    bi[s] = 0x7fffffff;
+  }
+  for (int r = 0; r <= g.max_ring; ++r) {
+    const int side = 2 * r + 1, ncell = side * side * side;
+    for (int q = lane; q < ncell; q += LANES) {
+      const int dx = q % side - r, dy = (q / side) % side - r, dz = q / (side * side) - r;
+      if (max(abs(dx), max(abs(dy), abs(dz))) != r) continue;  // interior: done before
+      const int2 rg = knn_find(g, knn_pack(cx + dx, cy + dy, cz + dz));
+      for (int k = rg.x; k < rg.x + rg.y; ++k) {
+        const int id = __ldg(g.ids + k);
+        if (!keep(id)) continue;
+        const double4 p = pos[id];
+        knnk_insert<K>(sqn(sub(v3(p.x, p.y, p.z), x)), id, bd, bi);
+      }
+    }
+    knnk_merged<K, LANES>(bd, bi, md, mi);
+    // unvisited points are >= r h away; margin for the cell rounding of x
+    const double lim = (double)r * h * (1.0 - 1e-9);
+    if (r >= 1 && md[K - 1] < lim * lim) return true;
+  }
+  return false;
+}
+
+}  // namespace ds

@@ -17,6 +17,7 @@
 //   clean_and_reset    reinit.cpp:28-89
 #include "ds_blend.cuh"
 #include "ds_context.cuh"
+#include "ds_knn.cuh"
 
 namespace ds {
 
@@ -100,29 +101,38 @@ __global__ void k_write_cands(const int* __restrict__ flag, const int* __restric
   cn[k] = make_float4((float)nd.x, (float)nd.y, (float)nd.z, (float)fn.w);
 }
 
-// 3x3 symmetric eigenvalues by cyclic Jacobi; returns sqrt(max eig of S^T S)
+// 3x3 symmetric eigenvalues by cyclic Jacobi; returns sqrt(max eig of S^T S).
+// Fully unrolled over the (p, q) pairs so the matrix stays in registers; the
+// arithmetic (and its order) is the oracle's.
 __device__ double sigma_max3(const double S[3][3]) {
   double a[3][3];
+#pragma unroll
   for (int i = 0; i < 3; ++i)
+#pragma unroll
     for (int j = 0; j < 3; ++j) {
       double acc = 0;
+#pragma unroll
       for (int k = 0; k < 3; ++k) acc += S[k][i] * S[k][j];
       a[i][j] = acc;
     }
   for (int sweep = 0; sweep < 30; ++sweep) {
     const double off = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
     if (off < 1e-300) break;
+#pragma unroll
     for (int p = 0; p < 2; ++p)
+#pragma unroll
       for (int q = p + 1; q < 3; ++q) {
         if (a[p][q] == 0.0) continue;
-        const double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double theta = ddiv(a[q][q] - a[p][p], 2.0 * a[p][q]);
         const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
         const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+#pragma unroll
         for (int k = 0; k < 3; ++k) {
           const double akp = a[k][p], akq = a[k][q];
           a[k][p] = cs * akp - sn * akq;
           a[k][q] = sn * akp + cs * akq;
         }
+#pragma unroll
         for (int k = 0; k < 3; ++k) {
           const double apk = a[p][k], aqk = a[q][k];
           a[p][k] = cs * apk - sn * aqk;
@@ -216,6 +226,73 @@ __device__ int screen_one(V3 x, const double bd[4], const int bi[4],
   return 2;
 }
 
+// screen_one for an aligned 8-lane group (all lanes call it): the Eq. 6 entry
+// is built redundantly, the four inverse warps of the compressive check
+// (x and the three 1 mm probes, fusion.cpp:151-176) run on lanes 0-3 and
+// meet in lane 0 for the strain's sigma_max. Same arithmetic as screen_one.
+__device__ int screen_group(V3 x, const double bd[4], const int bi[4],
+                            const double4* __restrict__ node_pos,
+                            const double4* __restrict__ node_live,
+                            const double4* __restrict__ node_dq, const ScreenParams& sp, int ids[4],
+                            float ws[4], int& cnt, int lane_k) {
+  (void)bd;
+  const unsigned gmask = 0xffu << ((threadIdx.x & 31) & ~7u);
+  const int k = min(sp.K, sp.N);
+  const int n0 = bi[0];
+  const double4 l0 = node_live[n0], p0 = node_pos[n0];
+  double w[4];
+  cnt = 0;
+  ids[cnt] = n0;
+  w[cnt] = skin_weight(x, v3(l0.x, l0.y, l0.z), l0.w);
+  ++cnt;
+  for (int m = 1; m < k; ++m) {
+    const int j = bi[m];
+    const double4 lj = node_live[j], pj = node_pos[j];
+    const double lpair = nrm(sub(v3(lj.x, lj.y, lj.z), v3(l0.x, l0.y, l0.z)));
+    const double rpair = nrm(sub(v3(pj.x, pj.y, pj.z), v3(p0.x, p0.y, p0.z)));
+    if (rpair <= 0) continue;
+    const double ratio = lpair / rpair;
+    if (ratio <= 1.0 - sp.eps || ratio >= 1.0 + sp.eps) continue;
+    ids[cnt] = j;
+    w[cnt] = skin_weight(x, v3(lj.x, lj.y, lj.z), lj.w);
+    ++cnt;
+  }
+  double wsum = 0;
+  for (int m = 0; m < cnt; ++m) wsum += w[m];
+  for (int m = 0; m < 4; ++m) ws[m] = m < cnt ? (float)w[m] : 0.f;
+  for (int m = cnt; m < 4; ++m) ids[m] = -1;
+  if (wsum < sp.delta_nn) return 0;  // uniform across the group
+  if (!sp.compressive) return 2;
+  V3 pr = x, r = v3(0, 0, 0);
+  if (lane_k == 1) pr.x += 1e-3;
+  else if (lane_k == 2) pr.y += 1e-3;
+  else if (lane_k == 3) pr.z += 1e-3;
+  int okw = 1;
+  if (lane_k < 4) okw = inv_warp_reweighted(pr, ids, cnt, node_dq, node_live, r) ? 1 : 0;
+  double rx[4], ry[4], rz[4];
+  int oks = 1;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int src = ((threadIdx.x & 31) & ~7) + a;
+    rx[a] = __shfl_sync(gmask, r.x, src);
+    ry[a] = __shfl_sync(gmask, r.y, src);
+    rz[a] = __shfl_sync(gmask, r.z, src);
+    oks &= __shfl_sync(gmask, okw, src);
+  }
+  if (!oks) return 1;  // a degenerate probe blend (fusion.cpp:174)
+  const V3 c0 = v3(rx[0], ry[0], rz[0]);
+  double S[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const V3 col = dvd(sub(v3(rx[a + 1], ry[a + 1], rz[a + 1]), c0), 1e-3);
+    S[0][a] = col.x;
+    S[1][a] = col.y;
+    S[2][a] = col.z;
+  }
+  if (lane_k != 0) return 2;  // only lane 0's verdict is used
+  return sigma_max3(S) <= 1.0 + sp.eps ? 2 : 1;
+}
+
 // kScreenLanes lanes per candidate, each scanning a strided subset of the
 // node tiles; the per-lane top-4 lists are merged by a shuffle butterfly.
 constexpr int kScreenLanes = 8;
@@ -227,13 +304,41 @@ __global__ void __launch_bounds__(kScreenThreads, 2) k_screen(
     const float4* __restrict__ node_live_f, const int* __restrict__ rmax_bits,
     const double4* __restrict__ node_dq, ScreenParams sp, int4* __restrict__ cki,
     float4* __restrict__ ckw, int* __restrict__ ok, int* __restrict__ res_out,
-    int* __restrict__ low, int* __restrict__ comp) {
+    int* __restrict__ low, int* __restrict__ comp, KnnGridView grid, int use_grid) {
   __shared__ float4 tile[kScreenThreads];
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = gt / kScreenLanes, lane_k = gt % kScreenLanes;
   const int n = *n_cand_dev;
   if (blockIdx.x * (kScreenThreads / kScreenLanes) >= n) return;  // whole block idle
   const bool active = k < n;
+  double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+  if (use_grid) {  // exact 4-NN on the live-node grid (ds_knn.cuh), group of 8 lanes
+    if (!active) return;  // whole 8-lane group
+    const float4 p = cp[k];
+    const V3 x = v3(p.x, p.y, p.z);
+    double md[4];
+    int mi[4];
+    if (!knn_grid_query<4, kScreenLanes>(grid, node_live, x, [](int) { return true; }, md, mi)) {
+      for (int t = lane_k; t < sp.N; t += kScreenLanes) {
+        const double4 nl = node_live[t];
+        knnk_insert<4>(sqn(sub(v3(nl.x, nl.y, nl.z), x)), t, bd, bi);
+      }
+      knnk_merged<4, kScreenLanes>(bd, bi, md, mi);
+    }
+    int ids[4];
+    float ws[4];
+    int cnt = 0;
+    const int res = screen_group(x, md, mi, node_pos, node_live, node_dq, sp, ids, ws, cnt, lane_k);
+    if (lane_k != 0) return;
+    ok[k] = res == 2 ? 1 : 0;
+    res_out[k] = res;
+    if (res == 0) atomicAdd(low, 1);
+    if (res == 1) atomicAdd(comp, 1);
+    cki[k] = make_int4(ids[0], ids[1], ids[2], ids[3]);
+    ckw[k] = make_float4(ws[0], ws[1], ws[2], ws[3]);
+    return;
+  }
   V3 x = v3(0, 0, 0);
   float xf = 0.f, yf = 0.f, zf = 0.f;
   if (active) {
@@ -290,8 +395,6 @@ __global__ void __launch_bounds__(kScreenThreads, 2) k_screen(
     const double tp = B + delta;
     thr = (float)(tp * tp * (1.0 + 2e-5)) + 1e-37f;
   }
-  double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-  int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
   for (int base = 0; base < sp.N; base += kScreenThreads) {
     __syncthreads();
     if (base + threadIdx.x < sp.N) tile[threadIdx.x] = node_live_f[base + threadIdx.x];
@@ -545,11 +648,13 @@ void screen_candidates_async(Ctx& c) {
   DS_CUDA(cudaMemsetAsync(&c.dsc->comp_rejected, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(c.cand_ok, 0, sizeof(int) * c.P, c.stream));
   node_live_positions(c);
+  const bool grid = build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
   DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02, cdiv((long long)c.P * kScreenLanes, kScreenThreads),
             kScreenThreads, 0, k_screen, c.cand_p,
             &c.dsc->n_cand, c.node_pos, c.node_live, c.node_live_f, &c.dsc->rmax_bits, c.node_dq,
             screen_params(c), c.cand_ki,
-            c.cand_kw, c.cand_ok, c.cand_flag, &c.dsc->low_support, &c.dsc->comp_rejected);
+            c.cand_kw, c.cand_ok, c.cand_flag, &c.dsc->low_support, &c.dsc->comp_rejected,
+            knn_view(c.grid_live, 3), grid ? 1 : 0);
 }
 
 void screen_candidates(Ctx& c, int n_cand, int* low_support, int* comp_rejected, int* accepted) {

@@ -12,6 +12,7 @@
 //   incremental skinning    warp_field.cpp:186-236
 #include "ds_blend.cuh"
 #include "ds_context.cuh"
+#include "ds_knn.cuh"
 
 namespace ds {
 namespace {
@@ -233,11 +234,11 @@ __global__ void k_node_edges(const double4* __restrict__ pos, int n, int k, int*
     bd[t] = INFINITY;
     bi[t] = 0x7fffffff;
   }
+#pragma unroll 4
   for (int i = lane; i < n; i += 32) {
-    if (i == j) continue;
     const double4 pi = pos[i];
     const double d2 = sqn(sub(v3(pi.x, pi.y, pi.z), v3(pj.x, pj.y, pj.z)));
-    if (!nb_less(d2, i, bd[7], bi[7])) continue;
+    if (i == j || !nb_less(d2, i, bd[7], bi[7])) continue;
     // insert keeping ascending (d2, idx) order
     double cd = d2;
     int ci = i;
@@ -275,6 +276,41 @@ __global__ void k_node_edges(const double4* __restrict__ pos, int n, int k, int*
       bi[7] = 0x7fffffff;
     }
   }
+}
+
+// Grid versions (ds_knn.cuh): same exact (d2, index) results as the brute-force
+// kernels, visiting only the Chebyshev shells the distance bound requires;
+// queries that exhaust the shell limit fall back to the full scan.
+constexpr int kKnnRing = 3;
+constexpr int kKnnEdgesGrid = 8192;  // node count above which edges / seeds use the grid
+
+__global__ void k_node_edges_grid(const double4* __restrict__ pos, int n, int k, KnnGridView g,
+                                  int* __restrict__ nbr) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;  // warp-uniform
+  const double4 pj = pos[j];
+  const V3 x = v3(pj.x, pj.y, pj.z);
+  double md[8];
+  int mi[8];
+  if (!knn_grid_query<8, 32>(g, pos, x, [j](int id) { return id != j; }, md, mi)) {
+    double bd[8];
+    int bi[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      bd[t] = INFINITY;
+      bi[t] = 0x7fffffff;
+    }
+    for (int i = lane; i < n; i += 32) {
+      if (i == j) continue;
+      const double4 pi = pos[i];
+      knnk_insert<8>(sqn(sub(v3(pi.x, pi.y, pi.z), x)), i, bd, bi);
+    }
+    knnk_merged<8, 32>(bd, bi, md, mi);
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) nbr[8 * j + r] = (r < k && mi[r] != 0x7fffffff) ? mi[r] : -1;
 }
 
 constexpr int kTile = 256;
@@ -340,10 +376,56 @@ __global__ void __launch_bounds__(kTile) k_skin_knn(ModelBuf m, int n, const dou
   m.kw[i] = make_float4(w[0], w[1], w[2], w[3]);
 }
 
+// Thread per surfel on the node grid (init_warp_field's skin_positions_bulk,
+// warp_field.cpp:60-79): exact 4-NN by (d2, idx), Gaussian weights.
+__global__ void __launch_bounds__(256) k_skin_knn_grid(ModelBuf m, int n,
+                                                       const double4* __restrict__ pos, int N,
+                                                       int K, KnnGridView g) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 rp = m.rp[i];
+  const V3 p = v3(rp.x, rp.y, rp.z);
+  double bd[4], md[4];
+  int bi[4], mi[4];
+  if (!knn_grid_query<4, 1>(g, pos, p, [](int) { return true; }, md, mi)) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      bd[s] = INFINITY;
+      bi[s] = 0x7fffffff;
+    }
+    for (int j = 0; j < N; ++j) {
+      const double4 q = pos[j];
+      knn4_insert(sqn(sub(v3(q.x, q.y, q.z), p)), j, bd, bi);
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      bd[s] = md[s];
+      bi[s] = mi[s];
+    }
+  }
+  int ids[4];
+  float w[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const bool ok = s < K && bi[s] != 0x7fffffff;
+    ids[s] = ok ? bi[s] : -1;
+    if (ok) {
+      const double4 q = pos[bi[s]];
+      w[s] = (float)skin_weight(p, v3(q.x, q.y, q.z), q.w);
+    } else {
+      w[s] = 0.f;
+    }
+  }
+  m.ki[i] = make_int4(ids[0], ids[1], ids[2], ids[3]);
+  m.kw[i] = make_float4(w[0], w[1], w[2], w[3]);
+}
+
 // Seeds of appended nodes from their K nearest pre-existing nodes.
 // Warp per new node: exact 4-NN among the N0 pre-existing nodes (lanes scan
 // strided subsets, shuffle merge), then lane 0 blends their DQs.
-__global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, int N, int K) {
+__global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, int N, int K,
+                          KnnGridView g, int use_grid) {
   const int jn = N0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (jn >= N) return;  // warp-uniform
@@ -353,11 +435,22 @@ __global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, 
     const V3 p = v3(pn.x, pn.y, pn.z);
     double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-    for (int i = lane; i < N0; i += 32) {
-      const double4 q = pos[i];
-      knn4_insert(sqn(sub(v3(q.x, q.y, q.z), p)), i, bd, bi);
+    double md[4];
+    int mi[4];
+    if (!(use_grid && knn_grid_query<4, 32>(g, pos, p, [N0](int id) { return id < N0; }, md, mi))) {
+#pragma unroll 4
+      for (int i = lane; i < N0; i += 32) {
+        const double4 q = pos[i];
+        knn4_insert(sqn(sub(v3(q.x, q.y, q.z), p)), i, bd, bi);
+      }
+      knn4_merge_lanes<32>(bd, bi);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        bd[t] = md[t];
+        bi[t] = mi[t];
+      }
     }
-    knn4_merge_lanes<32>(bd, bi);
     if (lane != 0) return;
     Q4 rs = q4(0, 0, 0, 0), ds_ = q4(0, 0, 0, 0);
     const int cnt = min(K, N0);
@@ -504,12 +597,26 @@ int greedy(Ctx& c, const float4* cand, int M, int n0, int list_mode) {
 
 }  // namespace
 
-void compute_node_edges(Ctx& c) {
+// grid over the reference node positions, cell 2 sigma (nodes are >= sigma apart)
+bool build_ref_grid(Ctx& c) {
+  return build_knn_grid(c, c.grid_ref, c.node_pos, c.n_nodes, 2.0 * c.cfg.node_sigma);
+}
+
+// Node edges stay a brute-force warp-per-node scan up to the grid capacity: at
+// a few thousand nodes 32 lanes x ~100 distances beat 2-3 grid shells of a
+// top-8 query (measured); the grid takes over beyond kKnnEdgesGrid nodes.
+void compute_node_edges(Ctx& c, bool build_grid) {
   const int n = c.n_nodes;
   if (n == 0) return;
   const int k = std::min(8, std::max(0, c.cfg.node_neighbor_k));
-  DS_LAUNCH(c, KK_NODE_EDGES, 32.0 * n + 32.0 * n, cdiv((long long)n * 32, 256), 256, 0,
-            k_node_edges, c.node_pos, n, k, c.node_nbr);
+  const bool big = n > kKnnEdgesGrid;
+  const bool grid = big && (build_grid ? build_ref_grid(c) : c.grid_ref.valid);
+  if (grid)
+    DS_LAUNCH(c, KK_NODE_EDGES, 32.0 * n + 32.0 * n, cdiv((long long)n * 32, 256), 256, 0,
+              k_node_edges_grid, c.node_pos, n, k, knn_view(c.grid_ref, kKnnRing), c.node_nbr);
+  else
+    DS_LAUNCH(c, KK_NODE_EDGES, 32.0 * n + 32.0 * n, cdiv((long long)n * 32, 256), 256, 0,
+              k_node_edges, c.node_pos, n, k, c.node_nbr);
 }
 
 void init_warp_field(Ctx& c) {
@@ -518,9 +625,15 @@ void init_warp_field(Ctx& c) {
   const int n = greedy(c, c.M().rp, c.n_surfels, 0, 0);
   c.n_nodes = n;
   DS_LAUNCH(c, KK_MISC, 64.0 * n, cdiv(n, 128), 128, 0, k_identity_dq, c.node_dq, 0, n);
-  compute_node_edges(c);
-  DS_LAUNCH(c, KK_SKIN_KNN, 48.0 * c.n_surfels, cdiv(c.n_surfels, kTile), kTile, 0, k_skin_knn,
-            c.M(), c.n_surfels, c.node_pos, n, std::min(4, c.cfg.knn_k));
+  const bool grid = build_ref_grid(c);  // current node set (also used by the edges if large)
+  compute_node_edges(c, false);
+  if (grid)
+    DS_LAUNCH(c, KK_SKIN_KNN, 48.0 * c.n_surfels, cdiv(c.n_surfels, 256), 256, 0, k_skin_knn_grid,
+              c.M(), c.n_surfels, c.node_pos, n, std::min(4, c.cfg.knn_k),
+              knn_view(c.grid_ref, kKnnRing));
+  else
+    DS_LAUNCH(c, KK_SKIN_KNN, 48.0 * c.n_surfels, cdiv(c.n_surfels, kTile), kTile, 0, k_skin_knn,
+              c.M(), c.n_surfels, c.node_pos, n, std::min(4, c.cfg.knn_k));
 }
 
 int extend_warp_field(Ctx& c, const float4* positions, int n) {
@@ -547,9 +660,11 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
   const int added = total - n0;
   c.n_nodes = total;
   if (added > 0) {
-    DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, cdiv((long long)added * 32, 128), 128, 0, k_seed_dq, c.node_pos,
-              c.node_dq, n0, total, std::min(4, c.cfg.knn_k));
-    compute_node_edges(c);
+    const bool grid = total > kKnnEdgesGrid && build_ref_grid(c);
+    DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, cdiv((long long)added * 32, 128), 128, 0,
+              k_seed_dq, c.node_pos, c.node_dq, n0, total, std::min(4, c.cfg.knn_k),
+              knn_view(c.grid_ref, kKnnRing), grid ? 1 : 0);
+    compute_node_edges(c, false);
   }
   return added;
 }

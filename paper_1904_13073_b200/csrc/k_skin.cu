@@ -282,7 +282,6 @@ __global__ void k_node_edges(const double4* __restrict__ pos, int n, int k, int*
 // kernels, visiting only the Chebyshev shells the distance bound requires;
 // queries that exhaust the shell limit fall back to the full scan.
 constexpr int kKnnRing = 3;
-constexpr int kKnnEdgesGrid = 8192;  // node count above which edges / seeds use the grid
 
 __global__ void k_node_edges_grid(const double4* __restrict__ pos, int n, int k, KnnGridView g,
                                   int* __restrict__ nbr) {
@@ -604,12 +603,13 @@ bool build_ref_grid(Ctx& c) {
 
 // Node edges stay a brute-force warp-per-node scan up to the grid capacity: at
 // a few thousand nodes 32 lanes x ~100 distances beat 2-3 grid shells of a
-// top-8 query (measured); the grid takes over beyond kKnnEdgesGrid nodes.
+// top-8 query (measured); the grid takes over beyond c.knn_edges_grid nodes
+// (8192; DS_KNN_EDGES_GRID overrides, used by the parity test).
 void compute_node_edges(Ctx& c, bool build_grid) {
   const int n = c.n_nodes;
   if (n == 0) return;
   const int k = std::min(8, std::max(0, c.cfg.node_neighbor_k));
-  const bool big = n > kKnnEdgesGrid;
+  const bool big = n > c.knn_edges_grid;
   const bool grid = big && (build_grid ? build_ref_grid(c) : c.grid_ref.valid);
   if (grid)
     DS_LAUNCH(c, KK_NODE_EDGES, 32.0 * n + 32.0 * n, cdiv((long long)n * 32, 256), 256, 0,
@@ -660,7 +660,7 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
   const int added = total - n0;
   c.n_nodes = total;
   if (added > 0) {
-    const bool grid = total > kKnnEdgesGrid && build_ref_grid(c);
+    const bool grid = total > c.knn_edges_grid && build_ref_grid(c);
     DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, cdiv((long long)added * 32, 128), 128, 0,
               k_seed_dq, c.node_pos, c.node_dq, n0, total, std::min(4, c.cfg.knn_k),
               knn_view(c.grid_ref, kKnnRing), grid ? 1 : 0);

@@ -246,6 +246,13 @@ def test_extend_and_incremental_skinning_match_oracle():
     assert np.array_equal(gm["skin_count"], om["skin_count"])
 
 
+def test_grid_knn_paths_match_oracle(monkeypatch):
+    """Node edges and new-node seeds through the exact grid K-NN (ds_knn.cuh)
+    instead of the brute-force scans: identical indices and DQs."""
+    monkeypatch.setenv("DS_KNN_EDGES_GRID", "0")  # read at context creation
+    test_extend_and_incremental_skinning_match_oracle()
+
+
 def test_clean_and_reset_matches_oracle():
     """reinit.cpp:28-89; test_reinit.cpp:97-132 phantom removed, occluded kept."""
     cfg = pkg.make_config(**SMALL)

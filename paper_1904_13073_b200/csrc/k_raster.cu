@@ -17,6 +17,12 @@
 namespace ds {
 namespace {
 
+// z-buffer updates are fire-and-forget reductions (RED.MIN: the result is not
+// read, nothing waits). A load-then-atomic pre-test measured 2.5x slower: the
+// load blocks the thread for an L2 round trip, the RED does not.
+__device__ __forceinline__ void zmin(unsigned long long* p, unsigned long long v) { atomicMin(p, v); }
+__device__ __forceinline__ void imin(int* p, int v) { atomicMin(p, v); }
+
 struct CamParams {
   Rig w2c;
   double fx, fy, cx, cy, focal;
@@ -92,8 +98,8 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
   const bool cin = ccx >= 0 && ccx < k.W && ccy >= 0 && ccy < k.H;
   if (cin) {
     const size_t c = (size_t)ccy * k.W + ccx;
-    if (!kPass2) atomicMin(pkey + c, zb);
-    else if (pkey[c] == zb) atomicMin(pidx + c, i);
+    if (!kPass2) zmin(pkey + c, zb);
+    else if (pkey[c] == zb) imin(pidx + c, i);
   }
   const double rpx = (double)lp.w * k.focal / pc.z;
   const double r2 = rpx * rpx;
@@ -105,15 +111,15 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
         const double dx = x - u, dy = y - v;
         if (dx * dx + dy * dy <= r2) {
           const size_t c = (size_t)y * k.W + x;
-          if (!kPass2) atomicMin(skey + c, zb);
-          else if (skey[c] == zb) atomicMin(sidx + c, i);
+          if (!kPass2) zmin(skey + c, zb);
+          else if (skey[c] == zb) imin(sidx + c, i);
         }
       }
   }
   if (cin) {  // sub-pixel splats keep their own pixel (raster.cpp:101)
     const size_t c = (size_t)ccy * k.W + ccx;
-    if (!kPass2) atomicMin(skey + c, zb);
-    else if (skey[c] == zb) atomicMin(sidx + c, i);
+    if (!kPass2) zmin(skey + c, zb);
+    else if (skey[c] == zb) imin(sidx + c, i);
   }
 }
 
@@ -155,8 +161,8 @@ __global__ void __launch_bounds__(256) k_index_splat(ModelBuf m, int n, CamParam
   if (!(fu >= 0 && fu < Wf && fv >= 0 && fv < Hf)) return;
   const size_t c = (size_t)fv * Wf + (size_t)fu;
   const unsigned long long zb = (unsigned long long)__double_as_longlong(pc.z);
-  if (!kPass2) atomicMin(key + c, zb);
-  else if (key[c] == zb) atomicMin(idx + c, i);
+  if (!kPass2) zmin(key + c, zb);
+  else if (key[c] == zb) imin(idx + c, i);
 }
 
 CamParams cam_params(Ctx& c, const double* pose) {

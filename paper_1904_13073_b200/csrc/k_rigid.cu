@@ -6,6 +6,8 @@
 //   of the 21 + 6 + 2 normal-equation terms, and the last block to arrive
 //   (ticket) sums the partials in a fixed order and solves on the device, so
 //   the whole pyramid runs without a host round trip.
+#include <cstdio>
+
 #include "ds_context.cuh"
 
 namespace ds {
@@ -15,14 +17,19 @@ constexpr int kTerms = 29;  // 21 upper H, 6 g, count, sum |r|
 constexpr int kThreads = 256;
 
 // Eigen::LDLT semantics (solver.cpp:225): diagonal pivoting, zero pivots kept,
-// pseudo-inverse of D with tolerance DBL_MIN.
-__device__ void ldlt_solve6(double A[6][6], const double* b, double* x) {
+// pseudo-inverse of D with tolerance DBL_MIN. Register-resident: every index
+// is a compile-time constant (unrolled loops); the pivot row/column swaps are
+// predicated on the runtime pivot instead of indexing with it. Same operations
+// in the same order as the oracle's ldlt_solve.
+__device__ __forceinline__ void ldlt_solve6(double A[6][6], const double* b, double* x) {
   int perm[6];
-  double temp[6];
   bool zero_all = false;
+#pragma unroll
   for (int k = 0; k < 6; ++k) {
+    if (zero_all) break;
     int big = k;
     double bv = fabs(A[k][k]);
+#pragma unroll
     for (int i = k + 1; i < 6; ++i)
       if (fabs(A[i][i]) > bv) {
         bv = fabs(A[i][i]);
@@ -30,32 +37,66 @@ __device__ void ldlt_solve6(double A[6][6], const double* b, double* x) {
       }
     perm[k] = big;
     if (big != k) {
-      for (int c = 0; c < k; ++c) {
-        const double t = A[k][c];
-        A[k][c] = A[big][c];
-        A[big][c] = t;
+#pragma unroll
+      for (int c = 0; c < k; ++c) {  // swap A[k][c] <-> A[big][c]
+        double vb = A[k][c];
+#pragma unroll
+        for (int i = k + 1; i < 6; ++i)
+          if (i == big) vb = A[i][c];
+#pragma unroll
+        for (int i = k + 1; i < 6; ++i)
+          if (i == big) A[i][c] = A[k][c];
+        A[k][c] = vb;
       }
-      for (int r = big + 1; r < 6; ++r) {
-        const double t = A[r][k];
-        A[r][k] = A[r][big];
-        A[r][big] = t;
+#pragma unroll
+      for (int r = k + 1; r < 6; ++r) {  // swap A[r][k] <-> A[r][big] for r > big
+        double vb = A[r][k];
+#pragma unroll
+        for (int i = k + 1; i < r; ++i)
+          if (i == big) vb = A[r][i];
+        if (r > big) {
+#pragma unroll
+          for (int i = k + 1; i < r; ++i)
+            if (i == big) A[r][i] = A[r][k];
+          A[r][k] = vb;
+        }
       }
-      const double t = A[k][k];
-      A[k][k] = A[big][big];
-      A[big][big] = t;
-      for (int i = k + 1; i < big; ++i) {
-        const double tmp = A[i][k];
-        A[i][k] = A[big][i];
-        A[big][i] = tmp;
+      {  // swap diagonal A[k][k] <-> A[big][big]
+        double vb = A[k][k];
+#pragma unroll
+        for (int i = k + 1; i < 6; ++i)
+          if (i == big) vb = A[i][i];
+#pragma unroll
+        for (int i = k + 1; i < 6; ++i)
+          if (i == big) A[i][i] = A[k][k];
+        A[k][k] = vb;
+      }
+#pragma unroll
+      for (int i = k + 1; i < 6; ++i) {  // swap A[i][k] <-> A[big][i] for k < i < big
+        if (i < big) {
+          double vb = A[i][k];
+#pragma unroll
+          for (int j = i + 1; j < 6; ++j)
+            if (j == big) vb = A[j][i];
+#pragma unroll
+          for (int j = i + 1; j < 6; ++j)
+            if (j == big) A[j][i] = A[i][k];
+          A[i][k] = vb;
+        }
       }
     }
     if (k > 0) {
+      double temp[6];
+#pragma unroll
       for (int c = 0; c < k; ++c) temp[c] = A[c][c] * A[k][c];
-      double s = 0;
-      for (int c = 0; c < k; ++c) s += A[k][c] * temp[c];
-      A[k][k] -= s;
+      double sacc = 0;
+#pragma unroll
+      for (int c = 0; c < k; ++c) sacc += A[k][c] * temp[c];
+      A[k][k] -= sacc;
+#pragma unroll
       for (int r = k + 1; r < 6; ++r) {
         double acc = 0;
+#pragma unroll
         for (int c = 0; c < k; ++c) acc += A[r][c] * temp[c];
         A[r][k] -= acc;
       }
@@ -67,30 +108,49 @@ __device__ void ldlt_solve6(double A[6][6], const double* b, double* x) {
       break;
     }
     if (valid)
-      for (int r = k + 1; r < 6; ++r) A[r][k] /= akk;
+#pragma unroll
+      for (int r = k + 1; r < 6; ++r) A[r][k] = ddiv(A[r][k], akk);
   }
+#pragma unroll
   for (int i = 0; i < 6; ++i) x[i] = zero_all ? 0.0 : b[i];
   if (zero_all) return;
-  for (int k = 0; k < 6; ++k) {
-    const double t = x[k];
-    x[k] = x[perm[k]];
-    x[perm[k]] = t;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {  // x[k] <-> x[perm[k]]
+    double vp = x[k];
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (i == perm[k]) vp = x[i];
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (i == perm[k]) x[i] = x[k];
+    x[k] = vp;
   }
+#pragma unroll
   for (int r = 0; r < 6; ++r) {
-    double s = x[r];
-    for (int c = 0; c < r; ++c) s -= A[r][c] * x[c];
-    x[r] = s;
+    double sacc = x[r];
+#pragma unroll
+    for (int c = 0; c < r; ++c) sacc -= A[r][c] * x[c];
+    x[r] = sacc;
   }
-  for (int i = 0; i < 6; ++i) x[i] = fabs(A[i][i]) > 2.2250738585072014e-308 ? x[i] / A[i][i] : 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) x[i] = fabs(A[i][i]) > 2.2250738585072014e-308 ? ddiv(x[i], A[i][i]) : 0.0;
+#pragma unroll
   for (int r = 5; r >= 0; --r) {
-    double s = x[r];
-    for (int c = r + 1; c < 6; ++c) s -= A[c][r] * x[c];
-    x[r] = s;
+    double sacc = x[r];
+#pragma unroll
+    for (int c = r + 1; c < 6; ++c) sacc -= A[c][r] * x[c];
+    x[r] = sacc;
   }
-  for (int k = 5; k >= 0; --k) {
-    const double t = x[k];
-    x[k] = x[perm[k]];
-    x[perm[k]] = t;
+#pragma unroll
+  for (int k = 5; k >= 0; --k) {  // x[k] <-> x[perm[k]]
+    double vp = x[k];
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (i == perm[k]) vp = x[i];
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i)
+      if (i == perm[k]) x[i] = x[k];
+    x[k] = vp;
   }
 }
 
@@ -108,10 +168,16 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
                                                           double* __restrict__ part,
                                                           unsigned* __restrict__ ticket, int level,
                                                           double* __restrict__ pose_out,
-                                                          DevScalars* __restrict__ sc) {
+                                                          DevScalars* __restrict__ sc,
+                                                          unsigned long long* __restrict__ trace) {
   __shared__ double sh[kThreads / 32][kTerms];
   __shared__ double tot[kTerms];
   __shared__ bool last;
+  if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    trace[0] = t_;
+  }
   double v[kTerms];
 #pragma unroll
   for (int k = 0; k < kTerms; ++k) v[k] = 0.0;
@@ -176,6 +242,11 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
   if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
+  if (trace && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    trace[1] = t_;
+  }
   __threadfence();
   const int nb = gridDim.x;
   for (int term = wid; term < kTerms; term += kThreads / 32) {
@@ -186,6 +257,11 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
     if (lane == 0) tot[term] = s;
   }
   __syncthreads();
+  if (trace && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    trace[2] = t_;
+  }
   if (threadIdx.x != 0) return;
   *ticket = 0u;
   const int pairs = (int)tot[27];
@@ -205,10 +281,20 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
   double ng[6], xi[6];
   for (int a = 0; a < 6; ++a) ng[a] = -tot[21 + a];
   ldlt_solve6(A, ng, xi);
+  if (trace && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    trace[3] = t_;
+  }
   for (int a = 0; a < 6; ++a)
     if (!isfinite(xi[a])) return;
   const Rig cur = rig_load(pose_out);
   rig_store(se3_increment(v3(xi[0], xi[1], xi[2]), v3(xi[3], xi[4], xi[5]), cur), pose_out);
+  if (trace && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    trace[4] = t_;
+  }
 }
 
 }  // namespace
@@ -238,12 +324,19 @@ void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int
     for (int it = 0; it < kIters[level]; ++it) {
       DS_LAUNCH(c, KK_RIGID, 100.0 * samples + 16.0 * kTerms * nb, nb, kThreads, 0, k_rigid_terms,
                 rp, c.d_pose, c.mm_idx, c.M(), c.f_vert, c.f_nrm, c.f_flag, c.red_part,
-                c.tickets + 3, level, c.d_pose, c.dsc);
+                c.tickets + 3, level, c.d_pose, c.dsc, c.pcg_trace ? c.pcg_trace + 32 : nullptr);
     }
   }
   double pose[12];
   DS_CUDA(cudaMemcpyAsync(pose, c.d_pose, sizeof pose, cudaMemcpyDeviceToHost, c.stream));
   fetch_scalars(c);  // syncs
+  if (c.pcg_trace) {  // last ICP launch: block-0 start -> last block phases (us)
+    unsigned long long tr[5];
+    DS_CUDA(cudaMemcpy(tr, c.pcg_trace + 32, sizeof tr, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "rigid_trace last:%.2f reduce:%.2f ldlt:%.2f se3:%.2f\n",
+                 (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3, (tr[3] - tr[2]) * 1e-3,
+                 (tr[4] - tr[3]) * 1e-3);
+  }
   const int pairs = c.hsc->rigid_pairs;
   const double abs_r = c.hsc->rigid_abs;
   ds_rigid_result r{};

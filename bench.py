@@ -43,6 +43,11 @@ sys.path.insert(0, REPO)
 
 CFG2 = dict(width=640, height=480, focal=560.0, scene="articulated_body", seq_frames=100)
 CFG1 = dict(width=320, height=240, focal=280.0, scene="deforming_sphere", seq_frames=10)
+# BASELINE config 3: large scene with a panning camera (node append + reskinning
+# every frame) and an open-to-close contact, 1280x960
+CFG3 = dict(width=1280, height=960, focal=1120.0, scene="large_scene", seq_frames=60,
+            max_nodes=16384)
+CONFIGS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3}
 
 
 def peaks():
@@ -110,6 +115,8 @@ class ClockSampler:
 def make_cfg(spec, **kw):
     import paper_1904_13073_b200 as pkg
 
+    if "max_nodes" in spec:
+        kw.setdefault("max_nodes", spec["max_nodes"])
     return pkg.camera_config(spec["width"], spec["height"], spec["focal"], max_gn_iters=10,
                              pcg_max_iters=10, **kw)
 
@@ -126,7 +133,7 @@ def run_b200(args, rank, world, local_rank):
     import paper_1904_13073_b200 as pkg
 
     torch.cuda.set_device(local_rank)
-    spec = CFG2 if args.config == "cfg2" else CFG1
+    spec = CONFIGS[args.config]
     cfg = make_cfg(spec)
     K, W = args.steps, args.warmup
     frames = render_frames(spec, cfg, 1 + W + K, phase=3 * rank)
@@ -389,7 +396,7 @@ def main():
     ap.add_argument("--steps", type=int, default=94)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg1"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg1", "cfg3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sequences", type=int, default=1,
                     help="independent cfg2 sequences per GPU (BASELINE config 5)")
@@ -472,7 +479,11 @@ def main():
         "ms_per_gn_iter": round(solve_ms / max(gn_iters, 1e-9), 3),
         "roofline": roof, "kernels": per, "clocks": r["clocks"],
     }
-    if not args.no_cpu_baseline:
+    if args.config == "cfg3":
+        line["cpu_baseline"] = {"value": None, "unit": "frames/s", "cores": 1, "kind": "port",
+                                "sample": "n/a: the reference's dense 6N x 6N system at ~8k nodes "
+                                          "needs ~18 GB (SURVEY 8(d))"}
+    elif not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_entry(cpu_sample(r["spec"], r["cfg"], gn_iters))
         except Exception as e:  # never fail the GPU line on the CPU sample

@@ -274,12 +274,13 @@ enum Kind {
   kDeformingSphere,
   kArticulatedBody,
   kSineSheet,
+  kLargeScene,
   kNumKinds
 };
 const char* kNames[kNumKinds] = {"static_plane",     "rigid_orbit",    "bending_sheet",
                                  "articulated_two_part", "open_to_close", "tangential_slide",
                                  "turntable",        "deforming_sphere", "articulated_body",
-                                 "sine_sheet"};
+                                 "sine_sheet",       "large_scene"};
 int default_frames(int kind) {  // synth.cpp:213-224 (+ new scenes)
   switch (kind) {
     case kStaticPlane: return 10;
@@ -292,6 +293,7 @@ int default_frames(int kind) {  // synth.cpp:213-224 (+ new scenes)
     case kDeformingSphere: return 10;
     case kArticulatedBody: return 100;
     case kSineSheet: return 10;
+    case kLargeScene: return 60;
   }
   return 60;
 }
@@ -319,16 +321,16 @@ double swing(double u, double phase) { return 0.5 - 0.5 * std::cos(2.0 * kPi * (
 
 // Config 2 body: torso + head + two-link arms + legs, joint rotations in the
 // image plane and a breathing torso; ~0.9 m^2 visible at ~1.2 m.
-void articulated_body(Scene& s, double u) {
+void articulated_body(Scene& s, double u, P3 o = P3()) {
   const double breathe = 1.0 + 0.015 * std::sin(2.0 * kPi * u);
-  const P3 torso_c = p3(0.0, 0.12, 1.22);
+  const P3 torso_c = o + p3(0.0, 0.12, 1.22);
   s.ellipsoids.push_back({torso_c, rot_z(0.04 * std::sin(2.0 * kPi * u)),
                           p3(0.35 * breathe, 0.46, 0.17 * breathe)});
-  const P3 neck = p3(0.0, -0.29, 1.22);
+  const P3 neck = o + p3(0.0, -0.29, 1.22);
   const R3 nod = rot_x(0.12 * std::sin(2.0 * kPi * u));
   s.spheres.push_back({neck + nod * p3(0.0, -0.16, 0.0), 0.15});
   for (int side = -1; side <= 1; side += 2) {
-    const P3 shoulder = p3(0.36 * side, -0.18, 1.22);
+    const P3 shoulder = o + p3(0.36 * side, -0.18, 1.22);
     const double raise = (22.0 + 40.0 * swing(u, side > 0 ? 0.0 : 0.25)) * kPi / 180.0;
     const R3 r_up = rot_z(-side * raise);
     const P3 elbow = shoulder + r_up * p3(0.0, 0.40, 0.0);
@@ -337,7 +339,7 @@ void articulated_body(Scene& s, double u) {
     const P3 wrist = elbow + r_lo * p3(0.0, 0.36, 0.0);
     s.capsules.push_back({shoulder, elbow, 0.10});
     s.capsules.push_back({elbow, wrist, 0.085});
-    const P3 hip = p3(0.15 * side, 0.46, 1.22);
+    const P3 hip = o + p3(0.15 * side, 0.46, 1.22);
     const R3 r_leg = rot_z(side * (6.0 + 10.0 * swing(u, side > 0 ? 0.5 : 0.0)) * kPi / 180.0);
     s.capsules.push_back({hip, hip + r_leg * p3(0.0, 0.55, 0.0), 0.12});
   }
@@ -403,6 +405,17 @@ Scene scene_at(int kind, double u) {  // synth.cpp:275-334 (+ new scenes)
     case kSineSheet:  // 2 cm waves travelling ~1.3 mm per frame over 10 frames
       s.sines.push_back({1.2, 0.02, 2.0 * kPi / 0.4, 2.0 * kPi / 0.3, 0.2 * kPi * u});
       break;
+    case kLargeScene: {
+      // Config 3: a wide back wall band (revealed by the panning camera every
+      // frame), an articulated body at ~2.3 m and two spheres closing into
+      // contact (open-to-close topology change): ~5 m^2 visible at 1280x960.
+      s.rects.push_back({3.3, -2.4, 2.4, -0.55, 0.55});
+      articulated_body(s, u, p3(-0.45, 0.0, 1.1));
+      const double xc = 0.16 + 0.5 * open_close_gap(u) * 2.0;
+      s.spheres.push_back({p3(0.75 - xc, 0.05, 2.0), 0.16});
+      s.spheres.push_back({p3(0.75 + xc, 0.05, 2.0), 0.16});
+      break;
+    }
   }
   return s;
 }
@@ -412,6 +425,10 @@ double normalized_time(int t, int frames) { return frames > 1 ? double(t) / doub
 void camera_pose(int kind, int t, R3& R, P3& tr) {  // synth.cpp:336-344
   R = R3();
   tr = P3();
+  if (kind == kLargeScene) {  // slow pan about the vertical axis: new wall every frame
+    R = rot_y(0.25 * kPi / 180.0 * t);
+    return;
+  }
   if (kind != kRigidOrbit) return;
   const P3 pivot = p3(0.0, 0.0, 1.1);
   R = rot_y(kOrbitStepRad * t);

@@ -91,6 +91,7 @@ struct DevScalars {
   int lm_accepted, lm_attempts_total, pcg_iter_total, lm_rounds;
   int lm_relins, lm_pairs, _pad_lm0, _pad_lm1;
   double lm_e_pre, lm_gnorm, lm_initial, lm_final;
+  double new_bbox[6];  // bounding box of the nodes appended this frame
   double rigid_pose[12];
 };
 

@@ -476,8 +476,29 @@ __global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, 
 }
 
 // update_skinning_incremental (warp_field.cpp:186-236), thread per surfel.
+// Slots live in registers (every index compile-time; insertions are
+// predicated). A full entry can only change if some new node is closer than
+// its worst slot: the new nodes' bounding box (bbox, 6 doubles) gives a lower
+// bound on their distance, so surfels far from every new node exit after one
+// test -- exact (strict >: equal distances still take the index tie-break path).
+__device__ __forceinline__ void slot_swap(double sd[4], int si[4], double sw[4], int b) {
+#pragma unroll
+  for (int t = 1; t < 4; ++t)
+    if (t == b) {
+      const double td = sd[t];
+      sd[t] = sd[t - 1];
+      sd[t - 1] = td;
+      const int ti = si[t];
+      si[t] = si[t - 1];
+      si[t - 1] = ti;
+      const double tw = sw[t];
+      sw[t] = sw[t - 1];
+      sw[t - 1] = tw;
+    }
+}
+
 __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict__ pos, int first,
-                                   int N, int K) {
+                                   int N, int K, const double* __restrict__ bbox) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float4 rp = m.rp[i];
@@ -503,45 +524,54 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
       sw[s] = 0;
     }
   }
-  // insertion sort of the first `count` slots
-  for (int a = 1; a < count; ++a)
-    for (int b = a; b > 0 && nb_less(sd[b], si[b], sd[b - 1], si[b - 1]); --b) {
-      const double td = sd[b];
-      sd[b] = sd[b - 1];
-      sd[b - 1] = td;
-      const int ti = si[b];
-      si[b] = si[b - 1];
-      si[b - 1] = ti;
-      const double tw = sw[b];
-      sw[b] = sw[b - 1];
-      sw[b - 1] = tw;
-    }
+  if (count >= K) {  // full entry: skip unless a new node can come closer than the worst slot
+    double worst = sd[0];
+#pragma unroll
+    for (int s = 1; s < 4; ++s)
+      if (s < count) worst = fmax(worst, sd[s]);
+    const double dx = fmax(fmax(bbox[0] - p.x, p.x - bbox[3]), 0.0);
+    const double dy = fmax(fmax(bbox[1] - p.y, p.y - bbox[4]), 0.0);
+    const double dz = fmax(fmax(bbox[2] - p.z, p.z - bbox[5]), 0.0);
+    if ((dx * dx + dy * dy + dz * dz) * (1.0 - 1e-12) > worst) return;
+  }
+  // insertion sort of the first `count` slots (registers)
+#pragma unroll
+  for (int a = 1; a < 4; ++a)
+#pragma unroll
+    for (int b2 = 3; b2 >= 1; --b2)
+      if (a < count && b2 <= a && nb_less(sd[b2], si[b2], sd[b2 - 1], si[b2 - 1]))
+        slot_swap(sd, si, sw, b2);
   bool changed = false;
   for (int j = first; j < N; ++j) {
     const double4 q = pos[j];
     const double d2 = sqn(sub(v3(q.x, q.y, q.z), p));
     int slot;
+    double ld = sd[0];  // worst slot (count - 1) without a dynamic index
+    int li = si[0];
+#pragma unroll
+    for (int t = 1; t < 4; ++t)
+      if (t == count - 1) {
+        ld = sd[t];
+        li = si[t];
+      }
     if (count < K) {
       slot = count++;
-    } else if (nb_less(d2, j, sd[count - 1], si[count - 1])) {
+    } else if (nb_less(d2, j, ld, li)) {
       slot = count - 1;
     } else {
       continue;
     }
-    sd[slot] = d2;
-    si[slot] = j;
-    sw[slot] = skin_weight(p, v3(q.x, q.y, q.z), q.w);
-    for (int b = slot; b > 0 && nb_less(sd[b], si[b], sd[b - 1], si[b - 1]); --b) {
-      const double td = sd[b];
-      sd[b] = sd[b - 1];
-      sd[b - 1] = td;
-      const int ti = si[b];
-      si[b] = si[b - 1];
-      si[b - 1] = ti;
-      const double tw = sw[b];
-      sw[b] = sw[b - 1];
-      sw[b - 1] = tw;
-    }
+    const double w = skin_weight(p, v3(q.x, q.y, q.z), q.w);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t == slot) {
+        sd[t] = d2;
+        si[t] = j;
+        sw[t] = w;
+      }
+#pragma unroll
+    for (int b2 = 3; b2 >= 1; --b2)
+      if (b2 <= slot && nb_less(sd[b2], si[b2], sd[b2 - 1], si[b2 - 1])) slot_swap(sd, si, sw, b2);
     changed = true;
   }
   if (!changed) return;
@@ -554,6 +584,36 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
   }
   m.ki[i] = make_int4(o[0], o[1], o[2], o[3]);
   m.kw[i] = make_float4(w[0], w[1], w[2], w[3]);
+}
+
+// bounding box of pos[first, N) -> bbox (min xyz, max xyz); one CTA
+__global__ void k_bbox(const double4* __restrict__ pos, int first, int N, double* __restrict__ bbox) {
+  __shared__ double red[6][8];
+  double v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  for (int j = first + threadIdx.x; j < N; j += blockDim.x) {
+    const double4 q = pos[j];
+    v[0] = fmin(v[0], q.x);
+    v[1] = fmin(v[1], q.y);
+    v[2] = fmin(v[2], q.z);
+    v[3] = fmax(v[3], q.x);
+    v[4] = fmax(v[4], q.y);
+    v[5] = fmax(v[5], q.z);
+  }
+#pragma unroll
+  for (int a = 0; a < 6; ++a)
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v[a], off);
+      v[a] = a < 3 ? fmin(v[a], o) : fmax(v[a], o);
+    }
+  if ((threadIdx.x & 31) == 0)
+    for (int a = 0; a < 6; ++a) red[a][threadIdx.x >> 5] = v[a];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double r = red[threadIdx.x][0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      r = threadIdx.x < 3 ? fmin(r, red[threadIdx.x][w]) : fmax(r, red[threadIdx.x][w]);
+    bbox[threadIdx.x] = r;
+  }
 }
 
 HashView hash_view(Ctx& c) {
@@ -671,9 +731,11 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
 
 void update_skinning_incremental(Ctx& c, int first_new) {
   if (first_new >= c.n_nodes || c.n_surfels == 0) return;
+  DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 32.0 * (c.n_nodes - first_new), 1, 256, 0, k_bbox, c.node_pos,
+            first_new, c.n_nodes, c.dsc->new_bbox);
   DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 48.0 * c.n_surfels, cdiv(c.n_surfels, 256), 256, 0,
             k_skin_incremental, c.M(), c.n_surfels, c.node_pos, first_new, c.n_nodes,
-            std::min(4, c.cfg.knn_k));
+            std::min(4, c.cfg.knn_k), (const double*)c.dsc->new_bbox);
 }
 
 }  // namespace ds

@@ -420,37 +420,67 @@ __global__ void __launch_bounds__(256) k_skin_knn_grid(ModelBuf m, int n,
   m.kw[i] = make_float4(w[0], w[1], w[2], w[3]);
 }
 
-// Seeds of appended nodes from their K nearest pre-existing nodes.
-// Warp per new node: exact 4-NN among the N0 pre-existing nodes (lanes scan
-// strided subsets, shuffle merge), then lane 0 blends their DQs.
-__global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, int N, int K,
-                          KnnGridView g, int use_grid) {
-  const int jn = N0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (jn >= N) return;  // warp-uniform
+// Seeds of appended nodes from their K nearest pre-existing nodes
+// (warp_field.cpp:163-177). A CTA per new node: 8 warps scan strided subsets of
+// the N0 pre-existing nodes (or one grid query for large node sets), warp
+// shuffle merges, then warp 0 merges the 8 warp lists and lane 0 blends the DQs.
+constexpr int kSeedThreads = 256;
+__global__ void __launch_bounds__(kSeedThreads) k_seed_dq(const double4* __restrict__ pos,
+                                                         double4* dq, int N0, int N, int K,
+                                                         KnnGridView g, int use_grid) {
+  __shared__ double s_d[kSeedThreads / 32][4];
+  __shared__ int s_i[kSeedThreads / 32][4];
+  const int jn = N0 + blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (jn >= N) return;  // block-uniform
   DQ out = dq_identity();
   if (N0 > 0) {
     const double4 pn = pos[jn];
     const V3 p = v3(pn.x, pn.y, pn.z);
     double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-    double md[4];
-    int mi[4];
-    if (!(use_grid && knn_grid_query<4, 32>(g, pos, p, [N0](int id) { return id < N0; }, md, mi))) {
+    if (use_grid) {
+      if (wid == 0) {
+        double md[4];
+        int mi[4];
+        if (knn_grid_query<4, 32>(g, pos, p, [N0](int id) { return id < N0; }, md, mi)) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            bd[t] = md[t];
+            bi[t] = mi[t];
+          }
+        } else {
+          for (int i = lane; i < N0; i += 32) {
+            const double4 q = pos[i];
+            knn4_insert(sqn(sub(v3(q.x, q.y, q.z), p)), i, bd, bi);
+          }
+          knn4_merge_lanes<32>(bd, bi);
+        }
+      }
+    } else {
 #pragma unroll 4
-      for (int i = lane; i < N0; i += 32) {
+      for (int i = threadIdx.x; i < N0; i += kSeedThreads) {
         const double4 q = pos[i];
         knn4_insert(sqn(sub(v3(q.x, q.y, q.z), p)), i, bd, bi);
       }
       knn4_merge_lanes<32>(bd, bi);
-    } else {
+      if (lane == 0)
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        bd[t] = md[t];
-        bi[t] = mi[t];
+        for (int t = 0; t < 4; ++t) {
+          s_d[wid][t] = bd[t];
+          s_i[wid][t] = bi[t];
+        }
+      __syncthreads();
+      if (wid == 0) {  // lane w < 8 holds warp w's list, then a butterfly over 8 lanes
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          bd[t] = lane < kSeedThreads / 32 ? s_d[lane][t] : INFINITY;
+          bi[t] = lane < kSeedThreads / 32 ? s_i[lane][t] : 0x7fffffff;
+        }
+        knn4_merge_lanes<32>(bd, bi);
       }
     }
-    if (lane != 0) return;
+    if (threadIdx.x != 0) return;
     Q4 rs = q4(0, 0, 0, 0), ds_ = q4(0, 0, 0, 0);
     const int cnt = min(K, N0);
     const Q4 pivot = ld_q_plain(dq + 2 * bi[0]);
@@ -470,7 +500,7 @@ __global__ void k_seed_dq(const double4* __restrict__ pos, double4* dq, int N0, 
       out = dq_normalized(raw);
     }
   }
-  if (lane != 0) return;
+  if (threadIdx.x != 0) return;
   dq[2 * jn] = make_double4(out.r.w, out.r.x, out.r.y, out.r.z);
   dq[2 * jn + 1] = make_double4(out.d.w, out.d.x, out.d.y, out.d.z);
 }
@@ -721,8 +751,7 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
   c.n_nodes = total;
   if (added > 0) {
     const bool grid = total > c.knn_edges_grid && build_ref_grid(c);
-    DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, cdiv((long long)added * 32, 128), 128, 0,
-              k_seed_dq, c.node_pos, c.node_dq, n0, total, std::min(4, c.cfg.knn_k),
+    DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, added, kSeedThreads, 0, k_seed_dq, c.node_pos, c.node_dq, n0, total, std::min(4, c.cfg.knn_k),
               knn_view(c.grid_ref, kKnnRing), grid ? 1 : 0);
     compute_node_edges(c, false);
   }

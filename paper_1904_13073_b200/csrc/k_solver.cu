@@ -518,12 +518,36 @@ __global__ void k_row_fill(const int* __restrict__ up_key, const int* __restrict
     tag[p] = (ub << 1) | 1;
   }
 }
+// Warp per BSR row: the row's (column, tag) entries are ranked by column
+// (columns are distinct within a row) 32 at a time in registers and scattered
+// to their sorted slots; rows longer than 32 entries take the serial path.
 __global__ void k_row_sort(const int* __restrict__ row_ptr, int N, int* __restrict__ col,
                            int* __restrict__ tag, int* __restrict__ up_pos, int* __restrict__ up_mpos,
                            int* __restrict__ diag_pos) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= N) return;
-  const int a0 = row_ptr[r], a1 = row_ptr[r + 1];
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= N) return;  // warp-uniform
+  const int a0 = row_ptr[r], a1 = row_ptr[r + 1], len = a1 - a0;
+  if (len <= 32) {
+    const int vc = lane < len ? col[a0 + lane] : 0x7fffffff;
+    const int vt = lane < len ? tag[a0 + lane] : 0;
+    int rank = 0;
+    for (int q = 0; q < len; ++q) rank += __shfl_sync(0xffffffffu, vc, q) < vc ? 1 : 0;
+    __syncwarp();
+    if (lane < len) {
+      const int a = a0 + rank;
+      col[a] = vc;
+      tag[a] = vt;
+      if (vt & 1) up_mpos[vt >> 1] = a;
+      else up_pos[vt >> 1] = a;
+    }
+    const unsigned d = __ballot_sync(0xffffffffu, lane < len && vc == r);  // warp-uniform
+    int dr = -1;
+    if (d) dr = __shfl_sync(0xffffffffu, rank, __ffs(d) - 1);  // the diagonal's sorted slot
+    if (lane == 0) diag_pos[r] = d ? a0 + dr : -1;
+    return;
+  }
+  if (lane != 0) return;
   for (int a = a0 + 1; a < a1; ++a) {
     const int vc = col[a], vt = tag[a];
     int b = a;
@@ -1545,7 +1569,7 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
     DS_LAUNCH(c, KK_PATTERN, 16.0 * c.n_up, cdiv(c.n_up, 256), 256, 0, k_row_fill, c.up_key,
               n_up_dev, N, c.row_ptr, c.row_cnt, c.bsr_col, c.bsr_tag);
   }
-  DS_LAUNCH(c, KK_PATTERN, 16.0 * c.n_full, cdiv(N, 128), 128, 0, k_row_sort, c.row_ptr, N,
+  DS_LAUNCH(c, KK_PATTERN, 16.0 * c.n_full, cdiv((long long)N * 32, 256), 256, 0, k_row_sort, c.row_ptr, N,
             c.bsr_col, c.bsr_tag, c.up_pos, c.up_mpos, c.diag_pos);
   DS_LAUNCH(c, KK_PATTERN, 16.0 * pcg_ctas(c), cdiv(pcg_ctas(c), 128), 128, 0, k_pcg_slices,
             c.row_ptr, N, c.n_full, pcg_ctas(c), c.pcg_slices);

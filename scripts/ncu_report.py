@@ -7,7 +7,7 @@ import sys
 
 M = [("gpu__time_duration.sum", "us"), ("dram__bytes_read.sum", "DRAM rd"),
      ("dram__bytes_write.sum", "DRAM wr"),
-     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %peak"),
+     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %peak"),
      ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"),
      ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
      ("launch__registers_per_thread", "regs"), ("launch__grid_size", "grid"),

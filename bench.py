@@ -284,10 +284,17 @@ def roofline(ks, peak_gbs):
                               gbs=v["bytes"] / (v["ms"] * 1e-3) / 1e9)
     dom = max(rows, key=lambda n: rows[n]["ms"]) if rows else None
     out = None
+    traffic = None
+    try:  # ncu-measured DRAM bytes per launch of the same kernel (profiles/)
+        t = json.load(open(os.path.join(REPO, "profiles", "r01_traffic.json")))
+        if dom in t:
+            traffic = t[dom]["bytes_per_launch"]
+    except Exception:
+        pass
     if dom:
         r = rows[dom]
         out = {"kernel": dom, "bound": "hbm", "achieved": round(r["gbs"], 1), "peak": peak_gbs,
-               "unit": "GB/s", "frac": round(r["gbs"] / peak_gbs, 4), "traffic": None,
+               "unit": "GB/s", "frac": round(r["gbs"] / peak_gbs, 4), "traffic": traffic,
                "mean_launch_us": round(1e3 * r["ms"] / r["launches"], 2),
                "algorithmic_bytes_per_launch": round(r["bytes"] / r["launches"])}
     per = {n: {"gbs": round(r["gbs"], 1), "frac": round(r["gbs"] / peak_gbs, 4),

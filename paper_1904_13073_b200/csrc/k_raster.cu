@@ -106,15 +106,34 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
   if (sane && rpx < 1e6) {
     const int y0 = max((int)ceil(v - rpx), 0), y1 = min((int)floor(v + rpx), k.H - 1);
     const int x0 = max((int)ceil(u - rpx), 0), x1 = min((int)floor(u + rpx), k.W - 1);
-    for (int y = y0; y <= y1; ++y)
-      for (int x = x0; x <= x1; ++x) {
-        const double dx = x - u, dy = y - v;
-        if (dx * dx + dy * dy <= r2) {
-          const size_t c = (size_t)y * k.W + x;
-          if (!kPass2) zmin(skey + c, zb);
-          else if (skey[c] == zb) imin(sidx + c, i);
+    if (!kPass2) {
+      for (int y = y0; y <= y1; ++y)
+        for (int x = x0; x <= x1; ++x) {
+          const double dx = x - u, dy = y - v;
+          if (dx * dx + dy * dy <= r2) zmin(skey + (size_t)y * k.W + x, zb);
         }
+    } else if (y1 >= y0 && x1 >= x0) {
+      // pass 2 must read the stored depth before its RED: four disk pixels'
+      // loads are issued together instead of one blocking load per pixel
+      const int bw = x1 - x0 + 1, total = bw * (y1 - y0 + 1);
+      for (int base = 0; base < total; base += 4) {
+        unsigned long long kv[4];
+        size_t cc[4];
+        bool in[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int idx = base + q;
+          const int y = y0 + idx / bw, x = x0 + idx % bw;
+          const double dx = x - u, dy = y - v;
+          in[q] = idx < total && dx * dx + dy * dy <= r2;
+          cc[q] = (size_t)y * k.W + x;
+          kv[q] = in[q] ? skey[cc[q]] : 0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (in[q] && kv[q] == zb) imin(sidx + cc[q], i);
       }
+    }
   }
   if (cin) {  // sub-pixel splats keep their own pixel (raster.cpp:101)
     const size_t c = (size_t)ccy * k.W + ccx;

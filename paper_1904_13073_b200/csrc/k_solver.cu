@@ -179,7 +179,7 @@ __device__ __forceinline__ double pair_term_one(int c, int s, const ModelBuf& m,
 // Fused model-map resolve + association (raster.cpp:104-119, solver.cpp:244-271)
 // + per-pair terms: the pixel's winner and correspondence are decided in
 // registers, the CTA packs its paired pixels and evaluates their terms.
-__global__ void __launch_bounds__(256) k_assoc_pair_terms(
+__global__ void __launch_bounds__(256, 3) k_assoc_pair_terms(
     const int* __restrict__ pidx, const int* __restrict__ sidx, const uint8_t* __restrict__ fflag,
     ModelBuf m, const double4* __restrict__ node_dq, const double4* __restrict__ fvert,
     const double4* __restrict__ fnrm, PairParams pp, int* __restrict__ mm_idx,

@@ -113,3 +113,30 @@ def test_config_scenes_sizes():
     st2 = O.OracleState(Hh.oracle_cfg(c2))
     st2.build_frame(d2, 0)
     assert 170000 < st2.get_frame()["valid_count"] < 230000
+
+
+def test_config3_scene_pans_and_fills_the_frame():
+    """BASELINE config 3 (large_scene, 1280x960): ~0.57M valid pixels, a panning
+    camera (pose changes every frame) and the contact spheres closing."""
+    import paper_1904_13073_b200 as pkg
+
+    c3 = pkg.camera_config(1280, 960, 1120.0)
+    seq = pkg.SyntheticSequence("large_scene", 60, c3)
+    d0, d1 = seq.render_depth(0), seq.render_depth(1)
+    assert (d0 > 0).sum() > 500_000  # ~0.57M per frame; the model passes 1M surfels by frame 2
+    assert not np.array_equal(d0, d1)
+    p0, p1 = np.array(seq.camera_pose(0)), np.array(seq.camera_pose(1))
+    assert np.abs(p1 - p0).max() > 1e-4  # pans
+    assert np.allclose(p0, np.eye(3).reshape(9).tolist() + [0, 0, 0])
+
+
+def test_bench_configs_and_reference_arm_for_config3():
+    import argparse
+    import bench
+    import bench_reference
+
+    assert set(bench.CONFIGS) == {"cfg1", "cfg2", "cfg3"}
+    cfg = bench.make_cfg(bench.CFG3)
+    assert cfg["width"] == 1280 and cfg["max_nodes"] == 16384
+    out = bench_reference.run_reference(argparse.Namespace(config="cfg3", steps=1, gpus=1))
+    assert out["impl"] == "reference" and "unavailable" in out

@@ -304,3 +304,32 @@ def test_pipeline_sequence_tracks_oracle(scene, frames):
         assert np.abs(np.array(g["pose"]) - np.array(o.pose)).max() < 1e-4
         assert abs(g["mean_residual"] - o.solver.mean_residual) < 2e-4
     pipe.close()
+
+
+@pytest.mark.parametrize("scene", ["bending_sheet", "articulated_two_part"])
+def test_device_lm_loop_matches_host_loop(monkeypatch, scene):
+    """The device-resident LM loop (WHILE/IF conditional graph, k_lm_decide)
+    makes the host loop's decisions with the same arithmetic: identical
+    per-frame statistics and bit-identical final state."""
+    cfg = pkg.make_config(**SMALL)
+    seq = pkg.SyntheticSequence(scene, 30, cfg)
+    monkeypatch.setenv("DS_HOST_LM", "1")  # read at context creation
+    host = pkg.Pipeline(cfg)
+    monkeypatch.delenv("DS_HOST_LM")
+    dev = pkg.Pipeline(cfg)
+    keys = ["surfel_count", "node_count", "correspondences", "gn_iters", "fused", "appended",
+            "removed", "initial_energy", "final_energy", "mean_residual", "lm_attempts",
+            "pcg_iterations", "pose"]
+    for t in range(6):
+        d = seq.render_depth(t)
+        a, b = host.process_frame(d, t), dev.process_frame(d, t)
+        for k in keys:
+            assert a[k] == b[k], (t, k, a[k], b[k])
+    ma, mb = host.model(), dev.model()
+    for k in ma:
+        assert np.array_equal(ma[k], mb[k]), k
+    na, nb = host.nodes(), dev.nodes()
+    for k in na:
+        assert np.array_equal(na[k], nb[k]), k
+    host.close()
+    dev.close()

@@ -730,55 +730,68 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
     c1 = A.chunk_first[ub + 1];
     const int r0 = A.up_start[ub] + (chunk - c0) * kChunk;
     const int r1 = min(r0 + kChunk, A.up_start[ub + 1]);
-    for (int k = r0 + l; k < r1; k += 2 * kChunkLanes) {
-      const bool has1 = k + kChunkLanes < r1;
-      const int v0 = A.rec_val[k];
-      const int v1 = has1 ? A.rec_val[k + kChunkLanes] : 0;
-      if (v0 >= 0 && v1 >= 0) {
-        // two surfel records in flight
-        const int cnt0 = A.s_cnt[v0 >> 4], off0 = A.s_head[v0 >> 4];
-        int cnt1 = 0, off1 = 0;
-        if (has1) {
-          cnt1 = A.s_cnt[v1 >> 4];
-          off1 = A.s_head[v1 >> 4];
-        }
-        float a0[6], b0[6], a1[6], b1[6];
-        double rr0 = 0.0, rr1 = 0.0;
-        if (cnt0 > 0) {
-          load_rows(A.rows + (size_t)off0 * 24, (v0 >> 2) & 3, v0 & 3, a0, b0);
-          if (diag) rr0 = __ldg(A.pair_r + off0);
-        }
-        if (cnt1 > 0) {
-          load_rows(A.rows + (size_t)off1 * 24, (v1 >> 2) & 3, v1 & 3, a1, b1);
-          if (diag) rr1 = __ldg(A.pair_r + off1);
-        }
-        if (cnt0 > 0) {
-          acc_surfel_record(A, v0, cnt0, off0, a0, b0, rr0, diag, h, gg);
+    // Three-stage software pipeline over steps of two records (lane l takes
+    // records l, l+8, l+16, ... in order): while step s's Jacobian rows are
+    // loaded and accumulated, step s+1's (count, head) and step s+2's record
+    // words are already in flight -- one dependent round trip per step instead
+    // of three. The accumulation order is unchanged.
+    constexpr int kNone = 0x7fffffff;
+    const int k0 = r0 + l;
+    auto rec_at = [&](int k) { return k < r1 ? __ldg(A.rec_val + k) : kNone; };
+    auto info = [&](int v, int& cnt, int& head) {
+      cnt = 0;
+      head = 0;
+      if (v != kNone && v >= 0) {
+        cnt = __ldg(A.s_cnt + (v >> 4));
+        head = __ldg(A.s_head + (v >> 4));
+      }
+    };
+    int vA0 = rec_at(k0), vA1 = rec_at(k0 + kChunkLanes);
+    int vB0 = rec_at(k0 + 2 * kChunkLanes), vB1 = rec_at(k0 + 3 * kChunkLanes);
+    int cA0, hA0, cA1, hA1;
+    info(vA0, cA0, hA0);
+    info(vA1, cA1, hA1);
+    for (int ks = k0; ks < r1; ks += 2 * kChunkLanes) {
+      const int vC0 = rec_at(ks + 4 * kChunkLanes), vC1 = rec_at(ks + 5 * kChunkLanes);
+      int cB0, hB0, cB1, hB1;
+      info(vB0, cB0, hB0);
+      info(vB1, cB1, hB1);
+      float a0[6], b0[6], a1[6], b1[6];
+      double rr0 = 0.0, rr1 = 0.0;
+      if (cA0 > 0) {
+        load_rows(A.rows + (size_t)hA0 * 24, (vA0 >> 2) & 3, vA0 & 3, a0, b0);
+        if (diag) rr0 = __ldg(A.pair_r + hA0);
+      }
+      if (cA1 > 0) {
+        load_rows(A.rows + (size_t)hA1 * 24, (vA1 >> 2) & 3, vA1 & 3, a1, b1);
+        if (diag) rr1 = __ldg(A.pair_r + hA1);
+      }
+      if (vA0 != kNone) {
+        if (vA0 < 0) {
+          acc_reg_record(A, vA0, h, gg);
           touched = 1;
-        }
-        if (cnt1 > 0) {
-          acc_surfel_record(A, v1, cnt1, off1, a1, b1, rr1, diag, h, gg);
+        } else if (cA0 > 0) {
+          acc_surfel_record(A, vA0, cA0, hA0, a0, b0, rr0, diag, h, gg);
           touched = 1;
-        }
-      } else {
-        // a regulariser record is involved (they trail each block's range)
-        for (int u = 0; u < (has1 ? 2 : 1); ++u) {
-          const int v = u == 0 ? v0 : v1;
-          if (v < 0) {
-            acc_reg_record(A, v, h, gg);
-            touched = 1;
-          } else {
-            const int cnt = A.s_cnt[v >> 4], off = A.s_head[v >> 4];
-            if (cnt > 0) {
-              float a0[6], b0[6];
-              load_rows(A.rows + (size_t)off * 24, (v >> 2) & 3, v & 3, a0, b0);
-              acc_surfel_record(A, v, cnt, off, a0, b0, diag ? __ldg(A.pair_r + off) : 0.0, diag, h,
-                                gg);
-              touched = 1;
-            }
-          }
         }
       }
+      if (vA1 != kNone) {
+        if (vA1 < 0) {
+          acc_reg_record(A, vA1, h, gg);
+          touched = 1;
+        } else if (cA1 > 0) {
+          acc_surfel_record(A, vA1, cA1, hA1, a1, b1, rr1, diag, h, gg);
+          touched = 1;
+        }
+      }
+      vA0 = vB0;
+      vA1 = vB1;
+      cA0 = cB0;
+      hA0 = hB0;
+      cA1 = cB1;
+      hA1 = hB1;
+      vB0 = vC0;
+      vB1 = vC1;
     }
   }
   // fixed butterfly over the 8 lanes of the group
@@ -1306,15 +1319,25 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
       pcg_mark(a, 6 + 5 * it);
       grid.sync();
       pcg_mark(a, 7 + 5 * it);
-      const double4 tot = grid_sum3(part, sh);
+      // the grid partials (thread k < G holds CTA k's) and the SpMV gathers are
+      // in flight together: the partials are only summed after the SpMV
+      double qa = 0.0, qb = 0.0, qc = 0.0;
+      if (tid < G) {  // G <= kPcgThreads (one CTA per SM)
+        const double2 ab = __ldcg(reinterpret_cast<const double2*>(part + 4 * tid));
+        qa = ab.x;
+        qb = ab.y;
+        qc = __ldcg(part + 4 * tid + 2);
+      }
+      // n = (H + mu I) m  (same k -> thread map in slice_spmv's row pass and below);
+      // computed before the stopping test -- unused on the last round
+      slice_spmv(V, C, RP, bb0, nb, nr, pub, Mv, mu, IT, Nv);
       pcg_mark(a, 8 + 5 * it);
-      const double gamma = tot.x, delta = tot.y;
-      rr = tot.z;
+      cta_sum3(qa, qb, qc, sh);
+      pcg_mark(a, 9 + 5 * it);
+      const double gamma = qa, delta = qb;
+      rr = qc;
       if (it == 0) rr0 = rr;
       if (it >= a.max_iters || rr == 0.0 || (a.tol2 > 0.0 && rr <= a.tol2 * rr0)) break;
-      // n = (H + mu I) m  (same k -> thread map in slice_spmv's row pass and below)
-      slice_spmv(V, C, RP, bb0, nb, nr, pub, Mv, mu, IT, Nv);
-      pcg_mark(a, 9 + 5 * it);
       const double beta = it > 0 ? gamma / gamma_old : 0.0;
       const double alpha = it > 0 ? gamma / (delta - beta * gamma / alpha_old) : gamma / delta;
       for (int k = tid; k < n6; k += kPcgThreads) {
@@ -2137,7 +2160,8 @@ int pcg_max_grid(int num_sms) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg<true>, kPcgThreads, kPcgSmem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_pcg<false>, kPcgThreads, kPcgSmem);
   per_sm = std::min(per_sm, per_sm2);
-  return std::max(1, per_sm) * num_sms;
+  // <= kPcgThreads: the pipelined loop holds one CTA partial per thread
+  return std::min(std::max(1, per_sm) * num_sms, kPcgThreads);
 }
 
 }  // namespace ds

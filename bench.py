@@ -438,7 +438,7 @@ def main():
                 "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
                 "ms_per_step": round(r["total_ms"] / K, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64 arithmetic, fp32 SoA surfel storage", "data": "synthetic",
+                "dtype": "f64", "storage": "fp32 SoA surfels, fp64 nodes, fp32 JtJ blocks", "data": "synthetic",
                 "config": {"workload": f"cfg5: {S} independent cfg2 sequences per GPU "
                                        f"(articulated_body 640x480, phase-shifted), 10 GN x 10 PCG",
                            "sequences_per_gpu": S, "pcg_ctas_per_context": int(r["pcg_grid"]),
@@ -471,7 +471,7 @@ def main():
         "metric": "frames/s", "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(r["total_ms"] / K, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64 arithmetic, fp32 SoA surfel storage", "data": "synthetic",
+        "dtype": "f64", "storage": "fp32 SoA surfels, fp64 nodes, fp32 JtJ blocks", "data": "synthetic",
         "config": {"workload": f"{args.config}: {r['spec']['scene']} {r['cfg']['width']}x"
                                f"{r['cfg']['height']}, 10 GN x 10 PCG per frame",
                    "surfels": st[-1]["surfel_count"], "nodes": st[-1]["node_count"],

@@ -8,6 +8,7 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -351,7 +352,17 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 }
 
 // Pipeline::process_frame (pipeline.cpp:74-142)
+void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stats* st);
 void process_frame(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stats* st) {
+  const auto t0 = std::chrono::steady_clock::now();
+  process_frame_impl(c, depth_dev, fi, st);
+  if (c.trace_host)
+    std::fprintf(stderr, "frame %d host %.1f us gpu %.1f us\n", fi,
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+                     .count(),
+                 st->total_ms * 1e3);
+}
+void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stats* st) {
   std::memset(st, 0, sizeof *st);
   st->frame = fi;
   const int64_t launches0 = c.total_launches;

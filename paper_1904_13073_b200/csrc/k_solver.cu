@@ -416,7 +416,7 @@ __global__ void k_elig_list(const int* __restrict__ flag, const int* __restrict_
 }
 
 __global__ void k_gen_records(const int4* __restrict__ ki, const int* __restrict__ elig, int n,
-                              int N, int* __restrict__ key, int* __restrict__ val) {
+                              int N, int* __restrict__ key, int* __restrict__ val, int none) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const int s = elig[q];
@@ -426,7 +426,7 @@ __global__ void k_gen_records(const int4* __restrict__ ki, const int* __restrict
 #pragma unroll
   for (int t = 0; t < 10; ++t) {
     const int m1 = kSlotPairs[t][0], m2 = kSlotPairs[t][1];
-    int k = kIntMax, v = 0;
+    int k = none, v = 0;
     if (m2 < cnt) {
       const int a = id[m1], b = id[m2];
       if (a <= b) {
@@ -442,12 +442,12 @@ __global__ void k_gen_records(const int4* __restrict__ ki, const int* __restrict
   }
 }
 __global__ void k_gen_reg_records(const int* __restrict__ nbr, int N, int* __restrict__ key,
-                                  int* __restrict__ val) {
+                                  int* __restrict__ val, int none) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= 8 * N) return;
   const int i = nbr[e];
   const int j = e >> 3;
-  int k0 = kIntMax, k1 = kIntMax, k2 = kIntMax;
+  int k0 = none, k1 = none, k2 = none;
   const int base = (int)(0x80000000u | (unsigned)(e << 2));
   int v2 = 0;
   if (i >= 0) {
@@ -468,19 +468,19 @@ __global__ void k_gen_reg_records(const int* __restrict__ nbr, int N, int* __res
   key[3 * e + 2] = k2;
   val[3 * e + 2] = v2;
 }
-__global__ void k_mark_unique(const int* __restrict__ key, int n, int* __restrict__ flag) {
+__global__ void k_mark_unique(const int* __restrict__ key, int n, int* __restrict__ flag, int none) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int v = key[k];
-  flag[k] = (v != kIntMax && (k == 0 || key[k - 1] != v)) ? 1 : 0;
+  flag[k] = (v != none && (k == 0 || key[k - 1] != v)) ? 1 : 0;
 }
 __global__ void k_write_up(const int* __restrict__ key, const int* __restrict__ scan, int n,
                            int* __restrict__ up_key, int* __restrict__ up_start, int ub_cap,
-                           int* __restrict__ err) {
+                           int* __restrict__ err, int none) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int v = key[k];
-  if (v == kIntMax) return;
+  if (v == none) return;
   const int total = scan[n];
   if (total > ub_cap) {
     if (k == 0) atomicOr(err, DERR_BLOCK_CAP);
@@ -491,7 +491,7 @@ __global__ void k_write_up(const int* __restrict__ key, const int* __restrict__ 
     up_key[ub] = v;
     up_start[ub] = k;
   }
-  if (k + 1 == n || key[k + 1] == kIntMax) up_start[total] = k + 1;
+  if (k + 1 == n || key[k + 1] == none) up_start[total] = k + 1;
 }
 __global__ void k_row_count(const int* __restrict__ up_key, const int* __restrict__ n_up_dev, int N,
                             int* __restrict__ row_cnt) {
@@ -1525,6 +1525,13 @@ __global__ void __launch_bounds__(256) k_bsr_spmv_rows(const int* __restrict__ r
 }  // namespace
 
 // ------------------------------------------------------------------ host side
+// the "no record" block key: 2^bits - 1 with 2^bits > N^2 (sorts after every block)
+int none_key(int N) {
+  int bits = 1;
+  while (bits < 31 && ((long long)1 << bits) <= (long long)N * N) ++bits;
+  return (int)(((long long)1 << bits) - 1);
+}
+
 // a CTA per SM; small systems use fewer CTAs
 int pcg_ctas(const Ctx& c) { return std::min(c.pcg_grid, std::max(1, cdiv(c.n_full, 64))); }
 
@@ -1555,11 +1562,15 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
   int* val = c.rec_val;
   if (n > 0)
     DS_LAUNCH(c, KK_PATTERN, 60.0 * n, cdiv(n, 256), 256, 0, k_gen_records, c.M().ki, c.elig, n,
-              N, key, val);
+              N, key, val, none_key(N));
   if (N > 0)
     DS_LAUNCH(c, KK_PATTERN, 32.0 * 8 * N, cdiv(8 * N, 256), 256, 0, k_gen_reg_records, c.node_nbr,
-              N, key + (size_t)n * 10, val + (size_t)n * 10);
-  const int end_bit = 31;  // the kIntMax sentinel needs all 31 bits
+              N, key + (size_t)n * 10, val + (size_t)n * 10, none_key(N));
+  // block keys row * N + col < N^2; the "no record" key (2^bits - 1) sorts last.
+  // Sorting only `bits` key bits saves radix passes (23 bits at N = 2.6k: 3 of 4)
+  int end_bit = 1;
+  while (end_bit < 31 && ((long long)1 << end_bit) <= (long long)N * N) ++end_bit;
+  const int none = (int)(((long long)1 << end_bit) - 1);
   int *ks, *vs;
   sort_pairs(c, key, val, c.rec_key2, c.rec_val2, R, end_bit, &ks, &vs, KK_PATTERN);
   // keep the sorted arrays in rec_key/rec_val
@@ -1567,11 +1578,12 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
     std::swap(c.rec_key, c.rec_key2);
     std::swap(c.rec_val, c.rec_val2);
   }
-  DS_LAUNCH(c, KK_PATTERN, 8.0 * R, cdiv(R, 256), 256, 0, k_mark_unique, c.rec_key, R, c.rec_flag);
+  DS_LAUNCH(c, KK_PATTERN, 8.0 * R, cdiv(R, 256), 256, 0, k_mark_unique, c.rec_key, R, c.rec_flag,
+            none);
   scan_exclusive(c, c.rec_flag, c.rec_flag, R);
   DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
   DS_LAUNCH(c, KK_PATTERN, 12.0 * R, cdiv(R, 256), 256, 0, k_write_up, c.rec_key, c.rec_flag, R,
-            c.up_key, c.up_start, c.UB_cap, &c.dsc->err);
+            c.up_key, c.up_start, c.UB_cap, &c.dsc->err, none);
   int* n_up_dev = c.rec_flag + R;
   DS_CUDA(cudaMemsetAsync(c.row_cnt, 0, sizeof(int) * (N + 1), c.stream));
   DS_LAUNCH(c, KK_PATTERN, 4.0 * c.UB_cap, cdiv(c.UB_cap, 256), 256, 0, k_row_count, c.up_key,
@@ -2035,7 +2047,12 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
     *out = rep;
     return;
   }
+  const auto tp0 = std::chrono::steady_clock::now();
   build_pattern(c, t_now, t_last);
+  if (c.trace_host)
+    std::fprintf(stderr, "build_pattern %.1f us\n",
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tp0)
+                     .count());
   const int max_pcg = c.cfg.pcg_max_iters > 0 ? c.cfg.pcg_max_iters : 10;
   const double tol = c.cfg.pcg_tol;
   const bool graphs = c.use_graphs && !c.cfg.profile;

@@ -999,6 +999,7 @@ struct PcgArgs {
   double* part;     // grid partials, 2 x 4 x G
   unsigned long long* trace;  // optional phase timestamps (DS_PCG_TRACE), CTA 0
   const int* slices;  // per CTA (r0, r1, bb0, bb1), k_pcg_slices once per frame
+  int smem_cap;       // slice bytes that may live in shared memory (<= kPcgSmem)
   DevScalars* sc;
 };
 
@@ -1193,7 +1194,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
   // ---- slice placement: shared memory when it fits, else global scratch
   const size_t need = (size_t)nr * (36 + 6 * kPcgVecs) * 8 + (size_t)nb * (6 * 8 + 36 * 4 + 4) +
                       (size_t)(nr + 1) * 4;
-  const bool fits = need <= (size_t)kPcgSmem;
+  const bool fits = need <= (size_t)a.smem_cap;
   double *MINV, *vb, *IT;
   const float* V;
   const int* C;
@@ -1750,6 +1751,7 @@ void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   a.items = c.pcg_items;
   a.part = c.pcg_part;
   a.slices = c.pcg_slices;
+  a.smem_cap = c.pcg_smem_cap;
   a.trace = c.pcg_trace;
   a.sc = c.dsc;
   const int grid = pcg_ctas(c);

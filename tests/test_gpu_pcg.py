@@ -85,3 +85,24 @@ def test_bsr_spmv_matches_dense(system):
     ref = H @ x + mu * x
     assert ms > 0
     assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max() + 1e-300
+
+
+@pytest.mark.parametrize("mode", ["pipelined", "classic"])
+def test_pcg_global_scratch_path_matches_reference(monkeypatch, mode):
+    """Slices too large for shared memory (very large N) run the same
+    recurrences on global scratch; forced here with DS_PCG_SMEM=0."""
+    monkeypatch.setenv("DS_PCG_SMEM", "0")  # read at context creation
+    cfg = pkg.camera_config(160, 120, 140.0, pcg_max_iters=10)
+    seq = pkg.SyntheticSequence("bending_sheet", 10, cfg)
+    ctx = pkg.Context(cfg)
+    ctx.process_frame(seq.render_depth(0), 0)
+    ctx.frame_maps(seq.render_depth(2), 2)
+    ne = ctx.build_normal_equations(np.eye(3).reshape(9).tolist() + [0.0, 0.0, 0.0], 2, 0)
+    H, _ = Hh.bsr_to_dense(ne, ctx.num_nodes())
+    g = ne["g"].copy()
+    mu = 1e-5 * np.trace(H) / H.shape[0]
+    x, it, _ = ctx.pcg_solve(mu, 10, 0.0 if mode == "pipelined" else 1e-150)
+    ref = reference_pcg(H, g, mu, 10)
+    assert it == 10
+    assert np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-300) < 1e-8
+    ctx.close()

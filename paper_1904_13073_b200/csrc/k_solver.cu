@@ -1191,29 +1191,40 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
   const int nr = r1 - r0, n6 = 6 * nr;
   const int bb0 = s_rng[2], nb = s_rng[3] - bb0;
   const double mu = *a.mu_ptr;
-  // ---- slice placement: shared memory when it fits, else global scratch
-  const size_t need = (size_t)nr * (36 + 6 * kPcgVecs) * 8 + (size_t)nb * (6 * 8 + 36 * 4 + 4) +
-                      (size_t)(nr + 1) * 4;
+  // ---- slice placement: everything in shared memory when it fits; else the
+  // vectors, inverses and SpMV partials in shared memory with the matrix
+  // streamed from L2 / HBM (large N); else all on global scratch
+  const size_t need_vec = (size_t)nr * (36 + 6 * kPcgVecs) * 8 + (size_t)nb * 6 * 8 +
+                          (size_t)(nr + 1) * 4;
+  const size_t need = need_vec + (size_t)nb * (36 * 4 + 4);
   const bool fits = need <= (size_t)a.smem_cap;
+  const bool fits_vec = !fits && need_vec <= (size_t)a.smem_cap;
   double *MINV, *vb, *IT;
   const float* V;
   const int* C;
   const int* RP;
-  if (fits) {
+  if (fits || fits_vec) {
     double* d = reinterpret_cast<double*>(smem);
     MINV = d;
     vb = MINV + 36 * nr;
     IT = vb + kPcgVecs * n6;
-    float* sv = reinterpret_cast<float*>(IT + 6 * (size_t)nb);
-    int* sc = reinterpret_cast<int*>(sv + 36 * (size_t)nb);
-    int* srp = sc + nb;
-    const float4* gv = reinterpret_cast<const float4*>(a.val + 36 * (size_t)bb0);
-    float4* sv4 = reinterpret_cast<float4*>(sv);
-    for (int k = tid; k < 9 * nb; k += kPcgThreads) sv4[k] = gv[k];
-    for (int k = tid; k < nb; k += kPcgThreads) sc[k] = a.col[bb0 + k];
+    int* srp;
+    if (fits) {
+      float* sv = reinterpret_cast<float*>(IT + 6 * (size_t)nb);
+      int* sc = reinterpret_cast<int*>(sv + 36 * (size_t)nb);
+      srp = sc + nb;
+      const float4* gv = reinterpret_cast<const float4*>(a.val + 36 * (size_t)bb0);
+      float4* sv4 = reinterpret_cast<float4*>(sv);
+      for (int k = tid; k < 9 * nb; k += kPcgThreads) sv4[k] = gv[k];
+      for (int k = tid; k < nb; k += kPcgThreads) sc[k] = a.col[bb0 + k];
+      V = sv;
+      C = sc;
+    } else {
+      srp = reinterpret_cast<int*>(IT + 6 * (size_t)nb);
+      V = a.val + 36 * (size_t)bb0;
+      C = a.col + bb0;
+    }
     for (int k = tid; k <= nr; k += kPcgThreads) srp[k] = a.row_ptr[r0 + k];
-    V = sv;
-    C = sc;
     RP = srp;
   } else {
     MINV = a.minv + 36 * (size_t)r0;

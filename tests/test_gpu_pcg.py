@@ -87,11 +87,14 @@ def test_bsr_spmv_matches_dense(system):
     assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max() + 1e-300
 
 
+@pytest.mark.parametrize("smem", ["0", "12000"])
 @pytest.mark.parametrize("mode", ["pipelined", "classic"])
-def test_pcg_global_scratch_path_matches_reference(monkeypatch, mode):
+def test_pcg_global_scratch_path_matches_reference(monkeypatch, mode, smem):
     """Slices too large for shared memory (very large N) run the same
-    recurrences on global scratch; forced here with DS_PCG_SMEM=0."""
-    monkeypatch.setenv("DS_PCG_SMEM", "0")  # read at context creation
+    recurrences with the matrix streamed from global memory (vectors still in
+    shared memory, DS_PCG_SMEM=12000 at this size) or entirely on global
+    scratch (DS_PCG_SMEM=0)."""
+    monkeypatch.setenv("DS_PCG_SMEM", smem)  # read at context creation
     cfg = pkg.camera_config(160, 120, 140.0, pcg_max_iters=10)
     seq = pkg.SyntheticSequence("bending_sheet", 10, cfg)
     ctx = pkg.Context(cfg)

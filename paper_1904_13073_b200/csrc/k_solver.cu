@@ -1104,6 +1104,7 @@ __device__ __forceinline__ int lower_bound_dev(const int* a, int n, int v) {
 __device__ __forceinline__ void slice_spmv(const float* V, const int* C, const int* RP, int bb0,
                                            int nb, int nr, const double* pub, const double* vown,
                                            double mu, double* IT, double* y) {
+#pragma unroll 2
   for (int k = threadIdx.x; k < 2 * nb; k += kPcgThreads) {
     const int blk = k >> 1, h3 = 3 * (k & 1);
     const double2* vc = reinterpret_cast<const double2*>(pub + 6 * (size_t)C[blk]);

@@ -14,7 +14,8 @@ import os
 from . import errors
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libdynsurf_b200.so")
+# DS_LIB_PATH: load another build of the library (A/B timing of two builds)
+LIB_PATH = os.environ.get("DS_LIB_PATH") or os.path.join(PKG, "lib", "libdynsurf_b200.so")
 
 CONFIG_FIELDS = [
     ("node_sigma", C.c_double), ("knn_k", C.c_int32), ("node_neighbor_k", C.c_int32),

@@ -285,6 +285,7 @@ void allocate(Ctx& c) {
   if (const char* e = std::getenv("DS_HOST_LM")) c.device_lm = e[0] == '0';
   c.trace_host = std::getenv("DS_TRACE_HOST") != nullptr;
   if (const char* e = std::getenv("DS_KNN_EDGES_GRID")) c.knn_edges_grid = std::atoi(e);
+  if (const char* e = std::getenv("DS_SCREEN_GRID")) c.screen_grid = e[0] != '0';
   if (const char* e = std::getenv("DS_PCG_SMEM")) c.pcg_smem_cap = std::min(std::atoi(e), c.pcg_smem_cap);
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));
   DS_CUDA(cudaMemsetAsync(c.node_nbr, 0xff, sizeof(int) * 8 * N, c.stream));

@@ -276,6 +276,7 @@ struct Ctx {
   // CUDA graphs of the GN step / LM attempt (re-captured per frame, updated in place)
   bool use_graphs = true;
   int knn_edges_grid = 8192;
+  bool screen_grid = true;  // DS_SCREEN_GRID=0: brute-force two-pass screening K-NN
   int pcg_smem_cap = 200 * 1024;  // DS_PCG_SMEM: slice bytes allowed in shared memory (tests: 0)  // node count above which edges / seeds use the grid
   bool trace_host = false;  // DS_TRACE_HOST: host-side timing prints
   bool device_lm = true;  // LM loop as a device-side WHILE graph (DS_HOST_LM=1: host loop)

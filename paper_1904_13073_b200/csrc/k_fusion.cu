@@ -648,7 +648,8 @@ void screen_candidates_async(Ctx& c) {
   DS_CUDA(cudaMemsetAsync(&c.dsc->comp_rejected, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(c.cand_ok, 0, sizeof(int) * c.P, c.stream));
   node_live_positions(c);
-  const bool grid = build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
+  const bool grid = c.screen_grid &&
+                    build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
   DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02, cdiv((long long)c.P * kScreenLanes, kScreenThreads),
             kScreenThreads, 0, k_screen, c.cand_p,
             &c.dsc->n_cand, c.node_pos, c.node_live, c.node_live_f, &c.dsc->rmax_bits, c.node_dq,

@@ -574,8 +574,14 @@ __global__ void k_row_sort(const int* __restrict__ row_ptr, int N, int* __restri
 // one thread per block sums its chunk partials in chunk order. Fixed work
 // decomposition + fixed reduction order => bit-deterministic; chunking balances
 // the diagonal blocks (hundreds of records) against off-diagonal ones.
-constexpr int kChunk = 64;
-constexpr int kChunkLanes = 8;
+#ifndef DS_CHUNK
+#define DS_CHUNK 64
+#endif
+#ifndef DS_CHUNK_LANES
+#define DS_CHUNK_LANES 8
+#endif
+constexpr int kChunk = DS_CHUNK;            // records per chunk (A/B builds: -DDS_CHUNK=...)
+constexpr int kChunkLanes = DS_CHUNK_LANES;  // lanes per chunk
 
 struct AsmArgs {
   const int* up_key;

@@ -306,6 +306,9 @@ void release(Ctx& c) {
   if (c.g_attempt.exec) cudaGraphExecDestroy(c.g_attempt.exec);
   if (c.g_solve.exec) cudaGraphExecDestroy(c.g_solve.exec);
   if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
+  if (c.side) cudaStreamDestroy(c.side);
+  if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  if (c.ev_join) cudaEventDestroy(c.ev_join);
 }
 
 void set_identity(double* p) {
@@ -572,6 +575,9 @@ ds_status ds_create(const ds_config* cfg, int32_t device, void* stream, ds_conte
       DS_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
       c.own_stream = true;
     }
+    DS_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    DS_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
     ds::set_identity(c.pose);
     ds::allocate(c);
     ds::sync(c);

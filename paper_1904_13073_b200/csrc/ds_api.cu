@@ -309,6 +309,7 @@ void release(Ctx& c) {
   if (c.side) cudaStreamDestroy(c.side);
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.ev_join) cudaEventDestroy(c.ev_join);
+  if (c.ev_mid) cudaEventDestroy(c.ev_mid);
 }
 
 void set_identity(double* p) {
@@ -578,6 +579,7 @@ ds_status ds_create(const ds_config* cfg, int32_t device, void* stream, ds_conte
     DS_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
     DS_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     DS_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&c.ev_mid, cudaEventDisableTiming));
     ds::set_identity(c.pose);
     ds::allocate(c);
     ds::sync(c);

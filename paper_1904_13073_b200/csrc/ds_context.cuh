@@ -127,7 +127,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t side = nullptr;  // fork/join branch inside the GN step (parallel graph branch)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join = nullptr;
   int num_sms = 148;
   int W = 0, H = 0, P = 0;
   int S_cap = 0, N_cap = 0, R_cap = 0, UB_cap = 0, B_cap = 0, HT = 0;

@@ -1666,15 +1666,22 @@ PairParams pair_params(Ctx& c, const double* pose) {
 // e_reg, ginf, |g|^2 (in pcg_rr slot) and tr(H) in DevScalars (no host sync).
 void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor) {
   const int n = c.n_surfels, N = c.n_nodes, P = c.P;
-  // fork: the node transforms and E_reg (needed only by the assembly) run on a
-  // side branch, concurrently with the splats / association / pair terms
+  // fork: the pair-list resets (needed by the association kernel) and the node
+  // transforms + E_reg (needed only by the assembly) run on a side branch,
+  // concurrently with the warp + splat passes
   const int nbp = cdiv(P, 256);
+  DS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+  DS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
   {
-    DS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
-    DS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
     cudaStream_t main_stream = c.stream;
     c.stream = c.side;
     try {
+      DS_CUDA(cudaMemsetAsync(c.s_cnt, 0, sizeof(int) * (n + 1), c.stream));
+      DS_CUDA(cudaMemsetAsync(c.s_head, 0x7f, sizeof(int) * (n + 1), c.stream));
+      DS_CUDA(cudaMemsetAsync(c.s_fill, 0, sizeof(int) * (n + 1), c.stream));
+      DS_CUDA(cudaMemsetAsync(&c.dsc->pair_list_n, 0, sizeof(int), c.stream));
+      DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
+      DS_CUDA(cudaEventRecord(c.ev_mid, c.stream));
       node_se3(c, c.node_dq, c.node_se3);
       DS_LAUNCH(c, KK_ENERGY, 200.0 * N, cdiv(8 * N, 256), 256, 0, k_reg_energy, c.node_pos,
                 c.node_nbr, c.node_se3, N, c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg_pre,
@@ -1686,15 +1693,11 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
     c.stream = main_stream;
     DS_CUDA(cudaEventRecord(c.ev_join, c.side));
   }
-  DS_CUDA(cudaMemsetAsync(c.s_cnt, 0, sizeof(int) * (n + 1), c.stream));
-  DS_CUDA(cudaMemsetAsync(c.s_head, 0x7f, sizeof(int) * (n + 1), c.stream));
-  DS_CUDA(cudaMemsetAsync(c.s_fill, 0, sizeof(int) * (n + 1), c.stream));
-  DS_CUDA(cudaMemsetAsync(&c.dsc->pair_list_n, 0, sizeof(int), c.stream));
-  DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
   // only render-eligible surfels can be drawn / paired during the solve (the
   // post-solve forward_warp, pipeline.cpp:108, rewrites every live surfel):
   // warp + splat pass 1 fused, splat pass 2, then resolve + associate + terms
   render_model_maps_list(c, pose, t_now, t_last, pose, c.elig, c.n_elig, c.node_dq, false);
+  DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_mid, 0));  // pair-list resets done
   // per pixel: 2 x 4 B winner ids, frame maps 65 B, winner live 32 B, ids out 8 B; per pair:
   // surfel ref + skin 48 B, rows 96 B + r 8 B out
   DS_LAUNCH(c, KK_PAIR_TERMS, 113.0 * P + 152.0 * c.n_pairs_ok_est, nbp, 256, 0,

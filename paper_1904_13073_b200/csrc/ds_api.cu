@@ -73,14 +73,22 @@ void launch_end(Ctx& c, int kind, double bytes) {
   }
 }
 void prof_flush(Ctx& c) {
+  // launches on another stream (the side branch) may still be running after
+  // this stream's sync: keep those records for a later flush
+  std::vector<ProfRec> keep;
   for (auto& r : c.prof_pending) {
+    if (cudaEventQuery(r.b) != cudaSuccess) {
+      cudaGetLastError();
+      keep.push_back(r);
+      continue;
+    }
     float ms = 0;
     DS_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
     c.prof_ms[r.kind] += ms;
     c.event_pool.push_back(r.a);
     c.event_pool.push_back(r.b);
   }
-  c.prof_pending.clear();
+  c.prof_pending.swap(keep);
 }
 void sync(Ctx& c) {
   DS_CUDA(cudaStreamSynchronize(c.stream));
@@ -391,7 +399,24 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
     return;
   }
   const int t_now = fi;
-  rigid_align(c, c.pose, c.pose, t_now, c.t_last_reinit, &st->rigid);
+  // the rigid ICP (main stream) and the frame's JtJ pattern build (side stream,
+  // independent of the pose) overlap; the pattern's host syncs wait only on it
+  rigid_align_enqueue(c, c.pose, c.pose, t_now, c.t_last_reinit);
+  if (c.n_nodes > 0 && c.n_surfels > 0) {
+    cudaStream_t main_stream = c.stream;
+    c.stream = c.side;
+    try {
+      build_pattern(c, t_now, c.t_last_reinit);
+    } catch (...) {
+      c.stream = main_stream;
+      throw;
+    }
+    c.stream = main_stream;
+    c.pattern_frame = t_now;
+    DS_CUDA(cudaEventRecord(c.ev_join, c.side));  // work enqueued after its last sync
+    DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+  }
+  rigid_align_finish(c, c.pose, &st->rigid);
   std::copy(st->rigid.pose, st->rigid.pose + 12, c.pose);
   DS_CUDA(cudaEventRecord(ev.e[2], c.stream));
   solve_nonrigid(c, c.pose, t_now, c.t_last_reinit, &st->solver);

@@ -89,7 +89,7 @@ struct DevScalars {
   // device-resident LM loop (solver.cpp:296-406 state, k_lm_decide)
   int lm_iter, lm_attempt, lm_relin, lm_done;
   int lm_accepted, lm_attempts_total, pcg_iter_total, lm_rounds;
-  int lm_relins, lm_pairs, _pad_lm0, _pad_lm1;
+  int lm_relins, lm_pairs, any_stable_pat, _pad_lm1;  // any_stable_pat: build_pattern's copy
   double lm_e_pre, lm_gnorm, lm_initial, lm_final;
   double new_bbox[6];  // bounding box of the nodes appended this frame
   double rigid_pose[12];
@@ -281,7 +281,8 @@ struct Ctx {
   bool screen_grid = true;  // DS_SCREEN_GRID=0: brute-force two-pass screening K-NN
   int pcg_smem_cap = 200 * 1024;  // DS_PCG_SMEM: slice bytes allowed in shared memory (tests: 0)  // node count above which edges / seeds use the grid
   bool trace_host = false;  // DS_TRACE_HOST: host-side timing prints
-  bool device_lm = true;  // LM loop as a device-side WHILE graph (DS_HOST_LM=1: host loop)
+  bool device_lm = true;
+  int pattern_frame = -1;  // frame whose JtJ pattern was built ahead (overlapping the rigid ICP)  // LM loop as a device-side WHILE graph (DS_HOST_LM=1: host loop)
   GraphSlot g_step, g_attempt, g_solve;
   double* h_mu = nullptr;  // pinned staging for mu
   int* h_int = nullptr;    // pinned staging for small ints
@@ -345,6 +346,10 @@ void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_p
 void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double* rel_res);
 void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int t_now,
                  int t_last, ds_rigid_result* out);
+// rigid_align split: enqueue the device work / wait and assemble the result
+void rigid_align_enqueue(Ctx& c, const double* render_pose, const double* init_pose, int t_now,
+                         int t_last);
+void rigid_align_finish(Ctx& c, const double* init_pose, ds_rigid_result* out);
 
 // ---- fusion (k_fusion.cu)
 void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out);

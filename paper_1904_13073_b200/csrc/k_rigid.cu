@@ -301,6 +301,12 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
 
 void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int t_now, int t_last,
                  ds_rigid_result* out) {
+  rigid_align_enqueue(c, render_pose, init_pose, t_now, t_last);
+  rigid_align_finish(c, init_pose, out);
+}
+
+void rigid_align_enqueue(Ctx& c, const double* render_pose, const double* init_pose, int t_now,
+                         int t_last) {
   render_model_maps(c, render_pose, t_now, t_last, false, nullptr);
   DS_CUDA(cudaMemcpyAsync(c.d_pose, init_pose, 12 * sizeof(double), cudaMemcpyHostToDevice,
                           c.stream));
@@ -327,6 +333,9 @@ void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int
                 c.tickets + 3, level, c.d_pose, c.dsc, c.pcg_trace ? c.pcg_trace + 32 : nullptr);
     }
   }
+}
+
+void rigid_align_finish(Ctx& c, const double* init_pose, ds_rigid_result* out) {
   double pose[12];
   DS_CUDA(cudaMemcpyAsync(pose, c.d_pose, sizeof pose, cudaMemcpyDeviceToHost, c.stream));
   fetch_scalars(c);  // syncs

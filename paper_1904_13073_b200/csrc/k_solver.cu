@@ -1560,13 +1560,15 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
   // eligible surfels (the only ones render_model_maps can pair this frame)
   int n = 0;
   if (n_all > 0) {
-    DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable, 0, sizeof(int), c.stream));
+    // own flag: the pattern may be built concurrently with the rigid ICP, whose
+    // model-map render computes dsc->any_stable
+    DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable_pat, 0, sizeof(int), c.stream));
     DS_LAUNCH(c, KK_PATTERN, 16.0 * n_all, cdiv(n_all, 256), 256, 0, k_any_stable_flag,
-              c.M().ln, n_all, c.cfg.delta_stable, &c.dsc->any_stable);
+              c.M().ln, n_all, c.cfg.delta_stable, &c.dsc->any_stable_pat);
     const int boot = (t_now - t_last <= c.cfg.delta_recent) ? 1 : 0;
     DS_LAUNCH(c, KK_PATTERN, 28.0 * n_all, cdiv(n_all, 256), 256, 0, k_elig_flags, c.M().ln,
               c.M().t, n_all, c.cfg.delta_stable, t_now, c.cfg.delta_recent, boot,
-              &c.dsc->any_stable, c.keep);
+              &c.dsc->any_stable_pat, c.keep);
     scan_exclusive(c, c.keep, c.keep_scan, n_all);
     DS_LAUNCH(c, KK_PATTERN, 12.0 * n_all, cdiv(n_all, 256), 256, 0, k_elig_list, c.keep,
               c.keep_scan, n_all, c.elig);
@@ -2087,7 +2089,8 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
     return;
   }
   const auto tp0 = std::chrono::steady_clock::now();
-  build_pattern(c, t_now, t_last);
+  if (c.pattern_frame != t_now) build_pattern(c, t_now, t_last);
+  c.pattern_frame = -1;
   if (c.trace_host)
     std::fprintf(stderr, "build_pattern %.1f us\n",
                  std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tp0)

@@ -318,6 +318,7 @@ void release(Ctx& c) {
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.ev_join) cudaEventDestroy(c.ev_join);
   if (c.ev_mid) cudaEventDestroy(c.ev_mid);
+  if (c.ev_live) cudaEventDestroy(c.ev_live);
 }
 
 void set_identity(double* p) {
@@ -421,9 +422,14 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   DS_CUDA(cudaEventRecord(ev.e[2], c.stream));
   solve_nonrigid(c, c.pose, t_now, c.t_last_reinit, &st->solver);
   DS_CUDA(cudaEventRecord(ev.e[3], c.stream));
+  if (c.n_nodes > 0) prepare_live_nodes_async(c);  // overlaps the warp / index map / fusion
   forward_warp(c, false);
   apply_fusion(c, c.pose, t_now, &st->fusion);
   DS_CUDA(cudaEventRecord(ev.e[4], c.stream));
+  if (c.live_pending) {  // not consumed (no fusion): keep the stream order
+    DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_live, 0));
+    c.live_pending = false;
+  }
   c.win_residual.push_back(st->solver.mean_residual);
   c.win_appended.push_back(st->fusion.appended);
   while ((int)c.win_residual.size() > c.cfg.reinit_window) c.win_residual.pop_front();
@@ -605,6 +611,7 @@ ds_status ds_create(const ds_config* cfg, int32_t device, void* stream, ds_conte
     DS_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     DS_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
     DS_CUDA(cudaEventCreateWithFlags(&c.ev_mid, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&c.ev_live, cudaEventDisableTiming));
     ds::set_identity(c.pose);
     ds::allocate(c);
     ds::sync(c);

@@ -127,7 +127,8 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t side = nullptr;  // fork/join branch inside the GN step (parallel graph branch)
-  cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join = nullptr, ev_live = nullptr;
+  bool live_pending = false, live_grid = false;  // prepare_live_nodes_async in flight
   int num_sms = 148;
   int W = 0, H = 0, P = 0;
   int S_cap = 0, N_cap = 0, R_cap = 0, UB_cap = 0, B_cap = 0, HT = 0;
@@ -350,6 +351,7 @@ void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int
 void rigid_align_enqueue(Ctx& c, const double* render_pose, const double* init_pose, int t_now,
                          int t_last);
 void rigid_align_finish(Ctx& c, const double* init_pose, ds_rigid_result* out);
+void prepare_live_nodes_async(Ctx& c);
 
 // ---- fusion (k_fusion.cu)
 void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out);

@@ -643,13 +643,41 @@ void fuse_depth(Ctx& c, const double* pose, int t_now, int* fused, int* n_cand) 
   *n_cand = c.hsc->n_cand;
 }
 
+// Live node positions + their K-NN grid depend only on the solved nodes: the
+// frame loop launches them on the side stream right after the solve, so they
+// overlap the full-model warp, the index map and the depth fusion.
+void prepare_live_nodes_async(Ctx& c) {
+  DS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+  DS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+  cudaStream_t main_stream = c.stream;
+  c.stream = c.side;
+  try {
+    node_live_positions(c);
+    c.live_grid = c.screen_grid &&
+                  build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
+  } catch (...) {
+    c.stream = main_stream;
+    throw;
+  }
+  c.stream = main_stream;
+  DS_CUDA(cudaEventRecord(c.ev_live, c.side));
+  c.live_pending = true;
+}
+
 void screen_candidates_async(Ctx& c) {
   DS_CUDA(cudaMemsetAsync(&c.dsc->low_support, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(&c.dsc->comp_rejected, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(c.cand_ok, 0, sizeof(int) * c.P, c.stream));
-  node_live_positions(c);
-  const bool grid = c.screen_grid &&
-                    build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
+  bool grid;
+  if (c.live_pending) {
+    DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_live, 0));
+    grid = c.live_grid;
+    c.live_pending = false;
+  } else {
+    node_live_positions(c);
+    grid = c.screen_grid &&
+           build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
+  }
   DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02, cdiv((long long)c.P * kScreenLanes, kScreenThreads),
             kScreenThreads, 0, k_screen, c.cand_p,
             &c.dsc->n_cand, c.node_pos, c.node_live, c.node_live_f, &c.dsc->rmax_bits, c.node_dq,

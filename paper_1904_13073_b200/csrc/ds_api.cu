@@ -417,7 +417,12 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
     DS_CUDA(cudaEventRecord(c.ev_join, c.side));  // work enqueued after its last sync
     DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
   }
+  const auto tr0 = std::chrono::steady_clock::now();
   rigid_align_finish(c, c.pose, &st->rigid);
+  if (c.trace_host)
+    std::fprintf(stderr, "pattern (side) built; rigid wait %.1f us\n",
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tr0)
+                     .count());
   std::copy(st->rigid.pose, st->rigid.pose + 12, c.pose);
   DS_CUDA(cudaEventRecord(ev.e[2], c.stream));
   solve_nonrigid(c, c.pose, t_now, c.t_last_reinit, &st->solver);

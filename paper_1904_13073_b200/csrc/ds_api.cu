@@ -319,6 +319,7 @@ void release(Ctx& c) {
   if (c.ev_join) cudaEventDestroy(c.ev_join);
   if (c.ev_mid) cudaEventDestroy(c.ev_mid);
   if (c.ev_live) cudaEventDestroy(c.ev_live);
+  if (c.ev_nodes) cudaEventDestroy(c.ev_nodes);
 }
 
 void set_identity(double* p) {
@@ -617,6 +618,7 @@ ds_status ds_create(const ds_config* cfg, int32_t device, void* stream, ds_conte
     DS_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
     DS_CUDA(cudaEventCreateWithFlags(&c.ev_mid, cudaEventDisableTiming));
     DS_CUDA(cudaEventCreateWithFlags(&c.ev_live, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&c.ev_nodes, cudaEventDisableTiming));
     ds::set_identity(c.pose);
     ds::allocate(c);
     ds::sync(c);
@@ -1276,6 +1278,7 @@ ds_status ds_extend_warp_field(ds_context* ctx, int32_t n, const double* positio
                        (float)positions[3 * i + 2], 0.f);
   DS_CUDA(cudaMemcpyAsync(c.cand_p, p.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, c.stream));
   const int a = ds::extend_warp_field(c, c.cand_p, n);
+  ds::join_node_updates(c);
   ds::sync(c);
   c.pattern_ready = false;
   if (appended) *appended = a;

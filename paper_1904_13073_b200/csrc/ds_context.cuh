@@ -129,6 +129,8 @@ struct Ctx {
   cudaStream_t side = nullptr;  // fork/join branch inside the GN step (parallel graph branch)
   cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join = nullptr, ev_live = nullptr;
   bool live_pending = false, live_grid = false;  // prepare_live_nodes_async in flight
+  cudaEvent_t ev_nodes = nullptr;  // new-node seeds / edges on the side stream
+  bool nodes_pending = false;
   int num_sms = 148;
   int W = 0, H = 0, P = 0;
   int S_cap = 0, N_cap = 0, R_cap = 0, UB_cap = 0, B_cap = 0, HT = 0;
@@ -352,6 +354,12 @@ void rigid_align_enqueue(Ctx& c, const double* render_pose, const double* init_p
                          int t_last);
 void rigid_align_finish(Ctx& c, const double* init_pose, ds_rigid_result* out);
 void prepare_live_nodes_async(Ctx& c);
+// main stream waits for side-stream node updates (seeds / edges), if any
+inline void join_node_updates(Ctx& c) {
+  if (!c.nodes_pending) return;
+  DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_nodes, 0));
+  c.nodes_pending = false;
+}
 
 // ---- fusion (k_fusion.cu)
 void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out);

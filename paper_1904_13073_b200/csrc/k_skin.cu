@@ -750,10 +750,26 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
   const int added = total - n0;
   c.n_nodes = total;
   if (added > 0) {
-    const bool grid = total > c.knn_edges_grid && build_ref_grid(c);
-    DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, added, kSeedThreads, 0, k_seed_dq, c.node_pos, c.node_dq, n0, total, std::min(4, c.cfg.knn_k),
-              knn_view(c.grid_ref, kKnnRing), grid ? 1 : 0);
-    compute_node_edges(c, false);
+    // the new nodes' seeds and the edges (warp_field.cpp:163-182) only touch
+    // node DQs / neighbour lists: they run on the side stream, concurrently with
+    // the caller's incremental reskinning of the surfels (joined at frame end)
+    DS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+    DS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+    cudaStream_t main_stream = c.stream;
+    c.stream = c.side;
+    try {
+      const bool grid = total > c.knn_edges_grid && build_ref_grid(c);
+      DS_LAUNCH(c, KK_GREEDY_NODES, 64.0 * added, added, kSeedThreads, 0, k_seed_dq, c.node_pos,
+                c.node_dq, n0, total, std::min(4, c.cfg.knn_k), knn_view(c.grid_ref, kKnnRing),
+                grid ? 1 : 0);
+      compute_node_edges(c, false);
+    } catch (...) {
+      c.stream = main_stream;
+      throw;
+    }
+    c.stream = main_stream;
+    DS_CUDA(cudaEventRecord(c.ev_nodes, c.side));
+    c.nodes_pending = true;
   }
   return added;
 }

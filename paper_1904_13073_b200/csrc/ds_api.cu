@@ -429,7 +429,7 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   solve_nonrigid(c, c.pose, t_now, c.t_last_reinit, &st->solver);
   DS_CUDA(cudaEventRecord(ev.e[3], c.stream));
   if (c.n_nodes > 0) prepare_live_nodes_async(c);  // overlaps the warp / index map / fusion
-  forward_warp(c, false);
+  c.warp_in_index_map = true;  // forward_warp (pipeline.cpp:108) fused into the index map pass
   apply_fusion(c, c.pose, t_now, &st->fusion);
   DS_CUDA(cudaEventRecord(ev.e[4], c.stream));
   if (c.live_pending) {  // not consumed (no fusion): keep the stream order

@@ -131,6 +131,7 @@ struct Ctx {
   bool live_pending = false, live_grid = false;  // prepare_live_nodes_async in flight
   cudaEvent_t ev_nodes = nullptr;  // new-node seeds / edges on the side stream
   bool nodes_pending = false;
+  bool warp_in_index_map = false;  // next apply_fusion: forward warp fused into index pass 1
   int num_sms = 148;
   int W = 0, H = 0, P = 0;
   int S_cap = 0, N_cap = 0, R_cap = 0, UB_cap = 0, B_cap = 0, HT = 0;
@@ -337,7 +338,7 @@ void update_skinning_incremental(Ctx& c, int first_new);
 // ---- raster (k_raster.cu)
 void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool associate,
                        const double* assoc_pose);
-void render_index_map(Ctx& c, const double* pose, int factor);
+void render_index_map(Ctx& c, const double* pose, int factor, const double4* warp_dq = nullptr);
 // model maps + association over a precomputed render-eligible surfel list
 void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
                             const double* assoc_pose, const int* list, int n,

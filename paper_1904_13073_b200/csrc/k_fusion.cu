@@ -720,7 +720,8 @@ void removal_mask(Ctx& c, const double* pose, int t_now, int n) {
 void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out) {
   ds_fusion_outcome oc{};
   const int P = c.P;
-  render_index_map(c, pose, c.cfg.supersample_factor);
+  render_index_map(c, pose, c.cfg.supersample_factor, c.warp_in_index_map ? c.node_dq : nullptr);
+  c.warp_in_index_map = false;
   fuse_depth_async(c, pose, t_now);
   screen_candidates_async(c);
   // accepted candidates keep row-major order (fusion.cpp:235-257)

@@ -165,12 +165,32 @@ __global__ void k_resolve_associate(const int* __restrict__ pidx, const int* __r
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(n_pairs, __popc(b));
 }
 
-template <bool kPass2>
+// kWarp (pass 1): the full-model forward warp (warp_field.cpp:104-140,
+// pipeline.cpp:108) is done here, the live state written, then splatted.
+template <bool kPass2, bool kWarp = false>
 __global__ void __launch_bounds__(256) k_index_splat(ModelBuf m, int n, CamParams k, int factor,
-                                                     unsigned long long* key, int* idx) {
+                                                     unsigned long long* key, int* idx,
+                                                     const double4* __restrict__ warp_dq = nullptr) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const float4 lp = m.lp[i];
+  float4 lp;
+  if (kWarp) {
+    const float4 rp = __ldcs(m.rp + i), rn = __ldcs(m.rn + i);
+    const Blend b = blend_entry(__ldcs(m.ki + i), __ldcs(m.kw + i), warp_dq);
+    float4 ln = rn;
+    lp = rp;
+    if (!b.degenerate) {
+      const Rig T = blend_rig_fast(b);
+      const V3 p = rig_apply(T, v3(rp.x, rp.y, rp.z));
+      const V3 q = rig_rotate(T, v3(rn.x, rn.y, rn.z));
+      lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
+      ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
+    }
+    m.lp[i] = lp;
+    m.ln[i] = ln;
+  } else {
+    lp = m.lp[i];
+  }
   const V3 pc = rig_apply(k.w2c, v3(lp.x, lp.y, lp.z));
   if (pc.z <= 0) return;
   const double u = k.fx * pc.x / pc.z + k.cx;
@@ -278,7 +298,7 @@ void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
   c.mm_ready = true;
 }
 
-void render_index_map(Ctx& c, const double* pose, int factor) {
+void render_index_map(Ctx& c, const double* pose, int factor, const double4* warp_dq) {
   const int n = c.n_surfels;
   const size_t cells = (size_t)c.P * factor * factor;
   if (factor != c.cfg.supersample_factor && factor > c.cfg.supersample_factor)
@@ -287,10 +307,15 @@ void render_index_map(Ctx& c, const double* pose, int factor) {
   DS_CUDA(cudaMemsetAsync(c.im_idx, 0x7f, 4 * cells, c.stream));
   const CamParams k = cam_params(c, pose);
   if (n > 0) {
-    DS_LAUNCH(c, KK_INDEX_MAP, 16.0 * n, cdiv(n, 256), 256, 0, k_index_splat<false>, c.M(), n, k,
-              factor, c.im_key, c.im_idx);
+    auto k_warp_index = k_index_splat<false, true>;
+    if (warp_dq)  // full forward warp (96 B) + index pass 1 (16 B) per surfel
+      DS_LAUNCH(c, KK_INDEX_MAP, 112.0 * n, cdiv(n, 256), 256, 0, k_warp_index, c.M(), n, k, factor,
+                c.im_key, c.im_idx, warp_dq);
+    else
+      DS_LAUNCH(c, KK_INDEX_MAP, 16.0 * n, cdiv(n, 256), 256, 0, k_index_splat<false>, c.M(), n, k,
+                factor, c.im_key, c.im_idx, (const double4*)nullptr);
     DS_LAUNCH(c, KK_INDEX_MAP, 16.0 * n, cdiv(n, 256), 256, 0, k_index_splat<true>, c.M(), n, k,
-              factor, c.im_key, c.im_idx);
+              factor, c.im_key, c.im_idx, (const double4*)nullptr);
   }
   c.im_factor = factor;
   std::copy(pose, pose + 12, c.im_pose);

@@ -316,8 +316,6 @@ void clear_scalars(Ctx& c);
 void scan_exclusive(Ctx& c, const int* in, int* out, int n);
 void sort_pairs(Ctx& c, int* keys, int* vals, int* keys_alt, int* vals_alt, int n, int end_bit,
                 int** keys_out, int** vals_out, int kind = KK_PATTERN);
-// fixed-order deterministic sum of `n` partials into dst (device)
-void reduce_partials(Ctx& c, const double* part, int n, double* dst, int mode);
 
 // ---- frame (k_frame.cu)
 void frame_maps(Ctx& c, const uint16_t* depth_dev, int frame_index);
@@ -325,7 +323,6 @@ void init_surfels_from_frame(Ctx& c);  // initialize_from_frame (pipeline.cpp:42
 
 // ---- warp field (k_warp.cu, k_skin.cu)
 int forward_warp(Ctx& c, bool count_degenerate);
-void forward_warp_list(Ctx& c, const int* list, int n);  // only the listed surfels
 void node_se3(Ctx& c, const double4* dq, double* se3);
 void node_live_positions(Ctx& c);
 void apply_increments(Ctx& c, const double* delta, double4* out, double* se3 = nullptr);  // solver.cpp:277-286

@@ -46,7 +46,7 @@ __global__ void k_any_stable(const float4* __restrict__ ln, int n, double delta_
 // list == nullptr: every surfel, eligibility tested here (raster.cpp:65-68);
 // list != nullptr: a precomputed render-eligible surfel list (solve loop)
 // kWarp (pass 1 over a list): the surfel is first forward-warped
-// (warp_field.cpp:128-140, as k_forward_warp_list) and its live state written,
+// (warp_field.cpp:128-140, as k_forward_warp) and its live state written,
 // so the solve loop's warp + first splat pass are one launch.
 template <bool kPass2, bool kWarp = false>
 __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const int* __restrict__ list,

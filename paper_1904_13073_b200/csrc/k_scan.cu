@@ -69,25 +69,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int* in, int 
   }
 }
 
-__global__ void k_reduce_fixed(const double* __restrict__ part, int n, double* dst, int mode) {
-  __shared__ double sh[256];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double v = part[i];
-    if (mode == 1) acc = fmax(acc, v);
-    else acc += v;
-  }
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      if (mode == 1) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
-      else sh[threadIdx.x] += sh[threadIdx.x + s];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *dst = sh[0];
-}
 }  // namespace
 
 void scan_exclusive(Ctx& c, const int* in, int* out, int n) {
@@ -120,8 +101,5 @@ size_t sort_temp_bytes(int n) {
   return bytes;
 }
 
-void reduce_partials(Ctx& c, const double* part, int n, double* dst, int mode) {
-  DS_LAUNCH(c, KK_REDUCE, 8.0 * n, 1, 256, 0, k_reduce_fixed, part, n, dst, mode);
-}
 
 }  // namespace ds

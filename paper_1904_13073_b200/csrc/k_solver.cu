@@ -39,7 +39,6 @@ size_t sort_temp_bytes(int n);
 
 namespace {
 
-constexpr int kIntMax = 0x7fffffff;
 
 // ---------------------------------------------------------------- pair terms
 // rows 1..3 of quat_right_matrix(q) (geometry.cpp:23-30), row r, col k

@@ -39,25 +39,6 @@ __global__ void __launch_bounds__(256) k_forward_warp(ModelBuf m, int n,
   __stcs(m.ln + i, ln);
 }
 
-__global__ void __launch_bounds__(256) k_forward_warp_list(ModelBuf m, const int* __restrict__ list,
-                                                           int n, const double4* __restrict__ node_dq) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int i = list[k];
-  const float4 rp = m.rp[i], rn = m.rn[i];
-  const Blend b = blend_entry(m.ki[i], m.kw[i], node_dq);
-  float4 lp = rp, ln = rn;
-  if (!b.degenerate) {
-    const Rig T = blend_rig_fast(b);
-    const V3 p = rig_apply(T, v3(rp.x, rp.y, rp.z));
-    const V3 q = rig_rotate(T, v3(rn.x, rn.y, rn.z));
-    lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
-    ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
-  }
-  m.lp[i] = lp;
-  m.ln[i] = ln;
-}
-
 __global__ void k_node_se3(const double4* __restrict__ dq, int n, double* __restrict__ se3) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -121,12 +102,6 @@ int forward_warp(Ctx& c, bool count_degenerate) {
   DS_CUDA(cudaMemcpyAsync(&deg, &c.dsc->degenerate, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   sync(c);
   return deg;
-}
-
-void forward_warp_list(Ctx& c, const int* list, int n) {
-  if (n == 0) return;
-  DS_LAUNCH(c, KK_FORWARD_WARP, 100.0 * n, cdiv(n, 256), 256, 0, k_forward_warp_list, c.M(), list,
-            n, c.node_dq);
 }
 
 void node_se3(Ctx& c, const double4* dq, double* se3) {

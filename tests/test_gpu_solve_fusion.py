@@ -333,3 +333,41 @@ def test_device_lm_loop_matches_host_loop(monkeypatch, scene):
         assert np.array_equal(na[k], nb[k]), k
     host.close()
     dev.close()
+
+
+def test_concurrent_contexts_match_sequential_runs():
+    """BASELINE config 5 mechanics: two contexts on their own streams, driven
+    from two host threads at once, give bit-identical results to running each
+    sequence alone (no state shared between contexts)."""
+    import threading
+
+    import torch
+
+    cfg = pkg.make_config(**SMALL)
+    scenes = ["bending_sheet", "rigid_orbit"]
+    frames = {sc: [pkg.SyntheticSequence(sc, 30, cfg).render_depth(t) for t in range(5)]
+              for sc in scenes}
+
+    def run(sc, stream, out):
+        p = pkg.Pipeline(cfg, 0, stream)
+        out[sc] = [p.process_frame(d, t) for t, d in enumerate(frames[sc])]
+        out[sc + ":model"] = p.model()
+        p.close()
+
+    alone = {}
+    for sc in scenes:
+        run(sc, None, alone)
+    together = {}
+    streams = [torch.cuda.Stream() for _ in scenes]
+    ths = [threading.Thread(target=run, args=(sc, st.cuda_stream, together))
+           for sc, st in zip(scenes, streams)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    for sc in scenes:
+        for a, b in zip(alone[sc], together[sc]):
+            for k in ("surfel_count", "node_count", "correspondences", "final_energy", "pose"):
+                assert a[k] == b[k], (sc, k)
+        for k in alone[sc + ":model"]:
+            assert np.array_equal(alone[sc + ":model"][k], together[sc + ":model"][k]), (sc, k)

@@ -262,7 +262,7 @@ void allocate(Ctx& c) {
   c.keep = dalloc<int>(c, S + P + 1);
   c.keep_scan = dalloc<int>(c, S + P + 1);
   c.ext_pos = dalloc<float4>(c, P);
-  for (KnnGrid* g : {&c.grid_ref, &c.grid_live}) {
+  for (KnnGrid* g : {&c.grid_ref, &c.grid_live, &c.grid_new}) {
     int slots = 1;
     while (slots < 2 * std::min(c.N_cap, kKnnMaxPoints)) slots <<= 1;
     g->key = dalloc<long long>(c, slots);
@@ -271,7 +271,7 @@ void allocate(Ctx& c) {
     g->prm = dalloc<double>(c, 8);
     g->pslot = dalloc<int>(c, std::min(c.N_cap, kKnnMaxPoints));
     g->fill = dalloc<int>(c, slots);
-    g->mask = slots - 1;
+    g->mask = g->cap_mask = slots - 1;
   }
   c.ht_key = dalloc<long long>(c, c.HT);
   c.ht_cnt = dalloc<int>(c, c.HT);
@@ -294,6 +294,8 @@ void allocate(Ctx& c) {
   c.trace_host = std::getenv("DS_TRACE_HOST") != nullptr;
   if (const char* e = std::getenv("DS_KNN_EDGES_GRID")) c.knn_edges_grid = std::atoi(e);
   if (const char* e = std::getenv("DS_SCREEN_GRID")) c.screen_grid = e[0] != '0';
+  if (const char* e = std::getenv("DS_INCR_GRID_MIN")) c.incr_grid_min = std::atoi(e);
+  if (const char* e = std::getenv("DS_INCR_CELL")) c.incr_cell = std::atof(e);
   if (const char* e = std::getenv("DS_PCG_SMEM")) c.pcg_smem_cap = std::min(std::atoi(e), c.pcg_smem_cap);
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));
   DS_CUDA(cudaMemsetAsync(c.node_nbr, 0xff, sizeof(int) * 8 * N, c.stream));

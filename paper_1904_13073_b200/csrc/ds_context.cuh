@@ -117,7 +117,8 @@ struct KnnGrid {
   double* prm = nullptr;
   int* pslot = nullptr;  // build scratch: slot of every point
   int* fill = nullptr;   // build scratch: per-slot scatter counters
-  int mask = 0;
+  int mask = 0;      // slots - 1 of the current build (<= cap_mask)
+  int cap_mask = 0;  // allocated slots - 1
   bool valid = false;
 };
 
@@ -247,6 +248,9 @@ struct Ctx {
   float4* ext_pos = nullptr;  // uncovered extension candidates (ordered)
   // greedy node hash
   KnnGrid grid_ref, grid_live;  // reference / live node positions
+  KnnGrid grid_new;             // the nodes added this frame (incremental reskinning)
+  int incr_grid_min = 16;       // new nodes above which grid_new is used (DS_INCR_GRID_MIN)
+  double incr_cell = 4.0;       // grid_new cell size in node_sigma (DS_INCR_CELL)
   long long* ht_key = nullptr;
   int* ht_cnt = nullptr;
   int* ht_ids = nullptr;
@@ -328,7 +332,7 @@ void node_live_positions(Ctx& c);
 void apply_increments(Ctx& c, const double* delta, double4* out, double* se3 = nullptr);  // solver.cpp:277-286
 void init_warp_field(Ctx& c);
 void compute_node_edges(Ctx& c, bool build_grid = true);
-bool build_knn_grid(Ctx& c, KnnGrid& g, const double4* pos, int n, double h);
+bool build_knn_grid(Ctx& c, KnnGrid& g, const double4* pos, int n, double h, int load_inv = 2);
 int extend_warp_field(Ctx& c, const float4* positions, int n);  // returns appended
 void update_skinning_incremental(Ctx& c, int first_new);
 

@@ -102,11 +102,15 @@ __global__ void __launch_bounds__(kBuildThreads) k_knn_build(const double4* __re
 
 // (Re)build `g` over pos[0..n) with cell size h. Returns false when n exceeds
 // the shared-memory sort capacity (callers then use the brute-force kernels).
-bool build_knn_grid(Ctx& c, KnnGrid& g, const double4* pos, int n, double h) {
+bool build_knn_grid(Ctx& c, KnnGrid& g, const double4* pos, int n, double h, int load_inv) {
   if (n <= 0 || n > kKnnMaxPoints) {
     g.valid = false;
     return false;
   }
+  // table sized to the point count (load <= 1/load_inv): the build clears only these slots
+  int slots = 1;
+  while (slots < load_inv * n) slots <<= 1;
+  g.mask = std::min(slots - 1, g.cap_mask);
   DS_LAUNCH(c, KK_SKIN_KNN, 40.0 * n, 1, kBuildThreads, 0, k_knn_build, pos, n, h, g, g.pslot,
             g.fill);
   g.valid = true;

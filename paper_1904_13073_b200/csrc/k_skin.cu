@@ -528,7 +528,8 @@ __device__ __forceinline__ void slot_swap(double sd[4], int si[4], double sw[4],
 }
 
 __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict__ pos, int first,
-                                   int N, int K, const double* __restrict__ bbox) {
+                                   int N, int K, const double* __restrict__ bbox, KnnGridView gnew,
+                                   int use_grid) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float4 rp = m.rp[i];
@@ -554,8 +555,8 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
       sw[s] = 0;
     }
   }
+  double worst = sd[0];
   if (count >= K) {  // full entry: skip unless a new node can come closer than the worst slot
-    double worst = sd[0];
 #pragma unroll
     for (int s = 1; s < 4; ++s)
       if (s < count) worst = fmax(worst, sd[s]);
@@ -572,7 +573,10 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
       if (a < count && b2 <= a && nb_less(sd[b2], si[b2], sd[b2 - 1], si[b2 - 1]))
         slot_swap(sd, si, sw, b2);
   bool changed = false;
-  for (int j = first; j < N; ++j) {
+  // streaming top-K over the new nodes (oracle loop, warp_field.cpp:186-236);
+  // the final slots are the (d2, index) top K of old + new, independent of the
+  // order the candidates arrive in
+  auto consider = [&](int j) {
     const double4 q = pos[j];
     const double d2 = sqn(sub(v3(q.x, q.y, q.z), p));
     int slot;
@@ -589,7 +593,7 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
     } else if (nb_less(d2, j, ld, li)) {
       slot = count - 1;
     } else {
-      continue;
+      return;
     }
     const double w = skin_weight(p, v3(q.x, q.y, q.z), q.w);
 #pragma unroll
@@ -603,7 +607,28 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
     for (int b2 = 3; b2 >= 1; --b2)
       if (b2 <= slot && nb_less(sd[b2], si[b2], sd[b2 - 1], si[b2 - 1])) slot_swap(sd, si, sw, b2);
     changed = true;
+  };
+  bool done = false;
+  if (use_grid && count >= K) {
+    // only new nodes with d2 <= worst can enter: the grid cells (over the new
+    // nodes) meeting the box |x - p|_inf <= sqrt(worst) (margin for rounding)
+    const double lox = gnew.prm[0], loy = gnew.prm[1], loz = gnew.prm[2], ih = gnew.prm[4];
+    const double r = sqrt(worst) * (1.0 + 1e-9);
+    const int x0 = (int)floor((p.x - r - lox) * ih), x1 = (int)floor((p.x + r - lox) * ih);
+    const int y0 = (int)floor((p.y - r - loy) * ih), y1 = (int)floor((p.y + r - loy) * ih);
+    const int z0 = (int)floor((p.z - r - loz) * ih), z1 = (int)floor((p.z + r - loz) * ih);
+    if ((x1 - x0 + 1) * (y1 - y0 + 1) * (z1 - z0 + 1) <= 64) {
+      for (int cz = z0; cz <= z1; ++cz)
+        for (int cy = y0; cy <= y1; ++cy)
+          for (int cx = x0; cx <= x1; ++cx) {
+            const int2 rg = knn_find(gnew, knn_pack(cx, cy, cz));
+            for (int k = rg.x; k < rg.x + rg.y; ++k) consider(first + __ldg(gnew.ids + k));
+          }
+      done = true;
+    }
   }
+  if (!done)
+    for (int j = first; j < N; ++j) consider(j);
   if (!changed) return;
   int o[4];
   float w[4];
@@ -778,9 +803,18 @@ void update_skinning_incremental(Ctx& c, int first_new) {
   if (first_new >= c.n_nodes || c.n_surfels == 0) return;
   DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 32.0 * (c.n_nodes - first_new), 1, 256, 0, k_bbox, c.node_pos,
             first_new, c.n_nodes, c.dsc->new_bbox);
+  // a grid over the new nodes restricts each full entry to the cells within its
+  // worst slot distance (worthwhile once there are more than a few new nodes)
+  const int added = c.n_nodes - first_new;
+  // (sparse cells: large, and a table at load <= 1/8 so that most probes of an
+  // empty cell end at the first slot)
+  const bool grid = added > c.incr_grid_min &&
+                    build_knn_grid(c, c.grid_new, c.node_pos + first_new, added,
+                                   c.incr_cell * c.cfg.node_sigma, 8);
   DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 48.0 * c.n_surfels, cdiv(c.n_surfels, 256), 256, 0,
             k_skin_incremental, c.M(), c.n_surfels, c.node_pos, first_new, c.n_nodes,
-            std::min(4, c.cfg.knn_k), (const double*)c.dsc->new_bbox);
+            std::min(4, c.cfg.knn_k), (const double*)c.dsc->new_bbox, knn_view(c.grid_new, 0),
+            grid ? 1 : 0);
 }
 
 }  // namespace ds

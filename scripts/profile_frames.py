@@ -8,10 +8,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
 
 
-def main(skip=40, count=2):
+def main(skip=40, count=2, config="cfg2"):
     import paper_1904_13073_b200 as pkg
 
-    spec = bench.CFG2
+    spec = bench.CONFIGS[config]
     cfg = bench.make_cfg(spec)
     frames = bench.render_frames(spec, cfg, skip + count, 0)
     pipe = pkg.Pipeline(cfg)
@@ -28,4 +28,4 @@ def main(skip=40, count=2):
 
 
 if __name__ == "__main__":
-    main(*(int(a) for a in sys.argv[1:3]))
+    main(*(int(a) for a in sys.argv[1:3]), *sys.argv[3:4])

@@ -216,7 +216,7 @@ def test_removal_and_skin_appended_kats():
     assert out["supported"][1] == 0
 
 
-def test_extend_and_incremental_skinning_match_oracle():
+def test_extend_and_incremental_skinning_match_oracle(offset=0.15):
     rng = np.random.default_rng(809)
     cfg = pkg.make_config(**SMALL)
     surf = [O.make_surfel(O.random_point(rng, 0.08)) for _ in range(300)]
@@ -231,7 +231,7 @@ def test_extend_and_incremental_skinning_match_oracle():
         nd["dq"][j] = O.dq_from_se3(O.random_se3(rng, 0.3, 0.05))
     ctx.upload_nodes(nd)
     st.set_nodes(nd)
-    app = np.array([O.random_point(rng, 0.1) + [0.15, 0, 0] for _ in range(200)], np.float32)
+    app = np.array([O.random_point(rng, 0.1) + [offset, 0, 0] for _ in range(200)], np.float32)
     app = app.astype(np.float64)
     first = ctx.num_nodes()
     assert ctx.extend_warp_field(app) == st.extend_warp_field(app) > 0
@@ -244,6 +244,8 @@ def test_extend_and_incremental_skinning_match_oracle():
     gm, om = ctx.download_model(), st.get_model()
     assert np.array_equal(gm["skin_idx"], om["skin_idx"])
     assert np.array_equal(gm["skin_count"], om["skin_count"])
+    # weights are stored as fp32 on the device (SoA surfel layout)
+    assert np.abs(np.asarray(gm["skin_w"]) - np.asarray(om["skin_w"])).max() < 1e-6
 
 
 def test_grid_knn_paths_match_oracle(monkeypatch):
@@ -251,6 +253,16 @@ def test_grid_knn_paths_match_oracle(monkeypatch):
     instead of the brute-force scans: identical indices and DQs."""
     monkeypatch.setenv("DS_KNN_EDGES_GRID", "0")  # read at context creation
     test_extend_and_incremental_skinning_match_oracle()
+
+
+@pytest.mark.parametrize("grid_min", ["0", "1000000"])
+@pytest.mark.parametrize("offset", [0.0, 0.05])
+def test_incremental_skinning_grid_and_scan_match_oracle(monkeypatch, grid_min, offset):
+    """update_skinning_incremental through the grid over the new nodes (cells
+    within each entry's worst slot distance) and through the full scan, with
+    the new nodes interleaved with the old ones: identical tables."""
+    monkeypatch.setenv("DS_INCR_GRID_MIN", grid_min)  # read at context creation
+    test_extend_and_incremental_skinning_match_oracle(offset)
 
 
 def test_clean_and_reset_matches_oracle():

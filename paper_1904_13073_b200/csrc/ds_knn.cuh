@@ -108,8 +108,14 @@ __device__ __forceinline__ void knnk_merged(const double bd[K], const int bi[K],
 
 // Exact top-K of the points `pos` (x, y, z in double4) around x by (d2, id),
 // ids accepted by `keep(id)`; LANES lanes of an aligned group cooperate (every
-// lane of the group must call it). Returns false if the shell limit was hit
-// before the result was certain (caller falls back to brute force).
+// lane of the group must call it). Shells are walked outwards; once the group
+// holds K points with K-th best d2 = B, a cell whose box is farther than
+// sqrt(B) from x is skipped, and the walk stops when every face of the walked
+// cube is farther than sqrt(B) (unvisited points lie outside the cube). The
+// distances carry a margin of 1e-9 h (cell assignment rounding) and the
+// comparisons are strict, so ties on d2 are still visited for the index
+// tie-break. Returns false if the shell limit was hit before the result was
+// certain (caller falls back to brute force).
 template <int K, int LANES, class Keep>
 __device__ bool knn_grid_query(const KnnGridView& g, const double4* __restrict__ pos, V3 x,
                                Keep keep, double md[K], int mi[K]) {
@@ -117,6 +123,9 @@ __device__ bool knn_grid_query(const KnnGridView& g, const double4* __restrict__
   const double lox = g.prm[0], loy = g.prm[1], loz = g.prm[2], h = g.prm[3], ih = g.prm[4];
   const int cx = (int)floor((x.x - lox) * ih), cy = (int)floor((x.y - loy) * ih),
             cz = (int)floor((x.z - loz) * ih);
+  const double eps = 1e-9 * h;
+  // x relative to its cell's low corner (per axis, in [0, h) up to rounding)
+  const double ox = x.x - (lox + cx * h), oy = x.y - (loy + cy * h), oz = x.z - (loz + cz * h);
   double bd[K];
   int bi[K];
 #pragma unroll
@@ -124,11 +133,20 @@ __device__ bool knn_grid_query(const KnnGridView& g, const double4* __restrict__
     bd[s] = INFINITY;
     bi[s] = 0x7fffffff;
   }
+  double bound = INFINITY;  // K-th best d2 of the group after the last shell
   for (int r = 0; r <= g.max_ring; ++r) {
     const int side = 2 * r + 1, ncell = side * side * side;
     for (int q = lane; q < ncell; q += LANES) {
       const int dx = q % side - r, dy = (q / side) % side - r, dz = q / (side * side) - r;
       if (max(abs(dx), max(abs(dy), abs(dz))) != r) continue;  // interior: done before
+      if (bound < INFINITY) {
+        // distance from x to the cell box [d h, (d + 1) h) relative to x's cell
+        const double ax = dx > 0 ? dx * h - ox : (dx < 0 ? ox - (dx + 1) * h : 0.0);
+        const double ay = dy > 0 ? dy * h - oy : (dy < 0 ? oy - (dy + 1) * h : 0.0);
+        const double az = dz > 0 ? dz * h - oz : (dz < 0 ? oz - (dz + 1) * h : 0.0);
+        const double ex = fmax(ax - eps, 0.0), ey = fmax(ay - eps, 0.0), ez = fmax(az - eps, 0.0);
+        if ((ex * ex + ey * ey + ez * ez) * (1.0 - 1e-9) > bound) continue;
+      }
       const int2 rg = knn_find(g, knn_pack(cx + dx, cy + dy, cz + dz));
       for (int k = rg.x; k < rg.x + rg.y; ++k) {
         const int id = __ldg(g.ids + k);
@@ -138,9 +156,10 @@ __device__ bool knn_grid_query(const KnnGridView& g, const double4* __restrict__
       }
     }
     knnk_merged<K, LANES>(bd, bi, md, mi);
-    // unvisited points are >= r h away; margin for the cell rounding of x
-    const double lim = (double)r * h * (1.0 - 1e-9);
-    if (r >= 1 && md[K - 1] < lim * lim) return true;
+    bound = md[K - 1];
+    // nearest face of the walked cube [c - r, c + r + 1) h
+    const double f = fmin(fmin(fmin(ox, h - ox), fmin(oy, h - oy)), fmin(oz, h - oz)) + r * h - eps;
+    if (f > 0.0 && f * f * (1.0 - 1e-9) > bound) return true;
   }
   return false;
 }

@@ -144,6 +144,31 @@ __device__ double sigma_max3(const double S[3][3]) {
   return sqrt(m);
 }
 
+// sigma_max3(S) <= 1 + eps, deciding from cheap bounds on lambda_max(S^T S)
+// when they are clear of the threshold by a relative 1e-9 (Rayleigh: max
+// diagonal <= lambda_max <= max Gershgorin row sum; the Jacobi result is
+// within ~1e-15 of lambda_max), else by the Jacobi sweep itself.
+__device__ bool strain_within(const double S[3][3], double eps) {
+  double a[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double acc = 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc += S[k][i] * S[k][j];
+      a[i][j] = acc;
+    }
+  const double g0 = a[0][0] + fabs(a[0][1]) + fabs(a[0][2]);
+  const double g1 = a[1][1] + fabs(a[1][0]) + fabs(a[1][2]);
+  const double g2 = a[2][2] + fabs(a[2][0]) + fabs(a[2][1]);
+  const double gmax = fmax(g0, fmax(g1, g2));
+  const double thr = (1.0 + eps) * (1.0 + eps);
+  if (gmax < thr * (1.0 - 1e-9)) return true;  // false for NaN
+  if (gmax == gmax && fmax(a[0][0], fmax(a[1][1], a[2][2])) > thr * (1.0 + 1e-9)) return false;
+  return sigma_max3(S) <= 1.0 + eps;
+}
+
 struct ScreenParams {
   int N, K, compressive;
   double eps, delta_nn;
@@ -221,7 +246,7 @@ __device__ int screen_one(V3 x, const double bd[4], const int bi[4],
       S[1][a] = col.y;
       S[2][a] = col.z;
     }
-    if (!(sigma_max3(S) <= 1.0 + sp.eps)) return 1;
+    if (!strain_within(S, sp.eps)) return 1;
   }
   return 2;
 }
@@ -290,7 +315,7 @@ __device__ int screen_group(V3 x, const double bd[4], const int bi[4],
     S[2][a] = col.z;
   }
   if (lane_k != 0) return 2;  // only lane 0's verdict is used
-  return sigma_max3(S) <= 1.0 + sp.eps ? 2 : 1;
+  return strain_within(S, sp.eps) ? 2 : 1;
 }
 
 // kScreenLanes lanes per candidate, each scanning a strided subset of the

@@ -173,6 +173,42 @@ def test_apply_fusion_matches_oracle(x_range, conf):
         assert g.appended > 0 and g.new_nodes > 0
 
 
+@pytest.mark.parametrize("rot,trans", [(0.05, 0.002), (0.3, 0.02)])
+def test_apply_fusion_compressive_screen_matches_oracle(rot, trans):
+    """fusion.cpp:128-177 with strained warps: random per-node SE(3)s make the
+    re-weighted inverse warp stretch or compress around many candidates; the
+    accept / compressive / low-support decisions match the oracle one for one."""
+    rng = np.random.default_rng(1234)
+    cfg = pkg.make_config(**SMALL)
+    seq = pkg.SyntheticSequence("static_plane", 3, cfg)
+    st = O.OracleState(Hh.oracle_cfg(cfg))
+    st.set_mirror(True)
+    d = seq.render_depth(1)
+    st.build_frame(d, 1)
+    surf = Hh.surfels_from_frame(st.get_frame(), x_range=(0, 80))
+    ctx = pkg.Context(cfg)
+    rm, _ = Hh.round_trip(ctx, O.model_from_surfels(surf))
+    ctx.init_warp_field()
+    st.set_model(rm)
+    st.init_warp_field()
+    nd = st.get_nodes()
+    for j in range(len(nd["pos"])):
+        nd["dq"][j] = O.dq_from_se3(O.random_se3(rng, rot, trans))
+    ctx.upload_nodes(nd)
+    st.set_nodes(nd)
+    ctx.frame_maps(d, 1)
+    I = O.pose_identity()
+    g = ctx.apply_fusion(I, 1)
+    o = st.apply_fusion(I, 1)
+    for k in ("fused", "appended", "removed", "compressive_rejected", "low_support_rejected",
+              "new_nodes", "degenerate_warps"):
+        assert getattr(g, k) == getattr(o, k), k
+    if rot >= 0.3:
+        assert g.compressive_rejected > 0
+    gm, om = ctx.download_model(), st.get_model()
+    assert np.array_equal(gm["skin_idx"], om["skin_idx"])
+
+
 def test_fuse_depth_hand_case():
     """test_fusion.cpp:34-62: c 10 -> 11, z 1.000 -> 1.001."""
     k = dict(fx=140.0, fy=140.0, width=64, height=48, cx=32.0, cy=24.0)

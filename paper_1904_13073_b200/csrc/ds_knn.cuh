@@ -77,6 +77,34 @@ __device__ __forceinline__ void knnk_insert(double d2, int j, double bd[K], int 
     }
 }
 
+// Top K of two sorted (d2, index) lists a and b (K a power of two), into a:
+// c[s] = min(a[s], b[K-1-s]) holds exactly the K smallest of the union and is
+// bitonic; a bitonic merge sorts it (K/2 log K compare-exchanges, static
+// register indices).
+template <int K>
+__device__ __forceinline__ void knnk_merge2(double ad[K], int ai[K], const double bd[K],
+                                            const int bi[K]) {
+  static_assert((K & (K - 1)) == 0, "K must be a power of two");
+#pragma unroll
+  for (int s = 0; s < K; ++s)
+    if (nb_less(bd[K - 1 - s], bi[K - 1 - s], ad[s], ai[s])) {
+      ad[s] = bd[K - 1 - s];
+      ai[s] = bi[K - 1 - s];
+    }
+#pragma unroll
+  for (int j = K / 2; j > 0; j >>= 1)
+#pragma unroll
+    for (int s = 0; s < K; ++s)
+      if ((s & j) == 0 && nb_less(ad[s + j], ai[s + j], ad[s], ai[s])) {
+        const double td = ad[s];
+        const int ti = ai[s];
+        ad[s] = ad[s + j];
+        ai[s] = ai[s + j];
+        ad[s + j] = td;
+        ai[s + j] = ti;
+      }
+}
+
 // top-K of the union of the per-lane lists of an aligned LANES group (disjoint
 // point subsets), written to (md, mi) in every lane; the per-lane lists stay.
 template <int K, int LANES>
@@ -101,8 +129,7 @@ __device__ __forceinline__ void knnk_merged(const double bd[K], const int bi[K],
       od[s] = __shfl_xor_sync(gmask, md[s], off);
       oi[s] = __shfl_xor_sync(gmask, mi[s], off);
     }
-#pragma unroll
-    for (int s = 0; s < K; ++s) knnk_insert<K>(od[s], oi[s], md, mi);
+    knnk_merge2<K>(md, mi, od, oi);
   }
 }
 

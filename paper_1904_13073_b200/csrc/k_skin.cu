@@ -283,16 +283,18 @@ __global__ void k_node_edges(const double4* __restrict__ pos, int n, int k, int*
 // queries that exhaust the shell limit fall back to the full scan.
 constexpr int kKnnRing = 3;
 
+constexpr int kEdgeLanes = 8;  // lanes per node query
+
 __global__ void k_node_edges_grid(const double4* __restrict__ pos, int n, int k, KnnGridView g,
                                   int* __restrict__ nbr) {
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (j >= n) return;  // warp-uniform
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) / kEdgeLanes;
+  const int lane = threadIdx.x & (kEdgeLanes - 1);
+  if (j >= n) return;  // whole group
   const double4 pj = pos[j];
   const V3 x = v3(pj.x, pj.y, pj.z);
   double md[8];
   int mi[8];
-  if (!knn_grid_query<8, 32>(g, pos, x, [j](int id) { return id != j; }, md, mi)) {
+  if (!knn_grid_query<8, kEdgeLanes>(g, pos, x, [j](int id) { return id != j; }, md, mi)) {
     double bd[8];
     int bi[8];
 #pragma unroll
@@ -300,12 +302,12 @@ __global__ void k_node_edges_grid(const double4* __restrict__ pos, int n, int k,
       bd[t] = INFINITY;
       bi[t] = 0x7fffffff;
     }
-    for (int i = lane; i < n; i += 32) {
+    for (int i = lane; i < n; i += kEdgeLanes) {
       if (i == j) continue;
       const double4 pi = pos[i];
       knnk_insert<8>(sqn(sub(v3(pi.x, pi.y, pi.z), x)), i, bd, bi);
     }
-    knnk_merged<8, 32>(bd, bi, md, mi);
+    knnk_merged<8, kEdgeLanes>(bd, bi, md, mi);
   }
   if (lane == 0)
 #pragma unroll
@@ -727,7 +729,7 @@ void compute_node_edges(Ctx& c, bool build_grid) {
   const bool big = n > c.knn_edges_grid;
   const bool grid = big && (build_grid ? build_ref_grid(c) : c.grid_ref.valid);
   if (grid)
-    DS_LAUNCH(c, KK_NODE_EDGES, 32.0 * n + 32.0 * n, cdiv((long long)n * 32, 256), 256, 0,
+    DS_LAUNCH(c, KK_NODE_EDGES, 32.0 * n + 32.0 * n, cdiv((long long)n * kEdgeLanes, 256), 256, 0,
               k_node_edges_grid, c.node_pos, n, k, knn_view(c.grid_ref, kKnnRing), c.node_nbr);
   else
     DS_LAUNCH(c, KK_NODE_EDGES, 32.0 * n + 32.0 * n, cdiv((long long)n * 32, 256), 256, 0,

@@ -30,7 +30,8 @@ size_t sort_temp_bytes(int n);
 int pcg_max_grid(int num_sms);
 void build_pattern(Ctx& c, int t_now, int t_last);
 double bsr_spmv(Ctx& c, const double* x_dev, double* y_dev, double mu, int reps);
-void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor);
+void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor,
+                        bool maps_clean = false);
 void fuse_depth_async(Ctx& c, const double* pose, int t_now);
 
 thread_local std::string g_last_error;

@@ -343,7 +343,9 @@ void render_index_map(Ctx& c, const double* pose, int factor, const double4* war
 // model maps + association over a precomputed render-eligible surfel list
 void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
                             const double* assoc_pose, const int* list, int n,
-                            const double4* warp_dq = nullptr, bool resolve = true);
+                            const double4* warp_dq = nullptr, bool resolve = true, bool clear = true);
+// resets the model-map z-buffers (the GN iteration kernel resets what it consumed)
+void clear_model_maps(Ctx& c);
 
 // ---- solver (k_solver.cu, k_rigid.cu)
 void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver_report* out);

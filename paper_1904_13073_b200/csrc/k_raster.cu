@@ -257,14 +257,20 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
   c.mm_ready = true;
 }
 
-void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
-                            const double* assoc_pose, const int* list, int n,
-                            const double4* warp_dq, bool resolve) {
+void clear_model_maps(Ctx& c) {
   const size_t P = c.P;
   DS_CUDA(cudaMemsetAsync(c.mm_pkey, 0xff, 8 * P, c.stream));
   DS_CUDA(cudaMemsetAsync(c.mm_skey, 0xff, 8 * P, c.stream));
   DS_CUDA(cudaMemsetAsync(c.mm_pidx, 0x7f, 4 * P, c.stream));
   DS_CUDA(cudaMemsetAsync(c.mm_sidx, 0x7f, 4 * P, c.stream));
+}
+
+// clear = false: the z-buffers are known to be empty (reset by their last
+// consumer, k_assoc_pair_terms, inside the device LM loop)
+void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
+                            const double* assoc_pose, const int* list, int n,
+                            const double4* warp_dq, bool resolve, bool clear) {
+  if (clear) clear_model_maps(c);
   DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
   SplatParams sp;
   sp.cam = cam_params(c, pose);

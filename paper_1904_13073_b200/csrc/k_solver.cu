@@ -179,7 +179,8 @@ __device__ __forceinline__ double pair_term_one(int c, int s, const ModelBuf& m,
 // + per-pair terms: the pixel's winner and correspondence are decided in
 // registers, the CTA packs its paired pixels and evaluates their terms.
 __global__ void __launch_bounds__(256, 3) k_assoc_pair_terms(
-    const int* __restrict__ pidx, const int* __restrict__ sidx, const uint8_t* __restrict__ fflag,
+    int* __restrict__ pidx, int* __restrict__ sidx, unsigned long long* __restrict__ pkey,
+    unsigned long long* __restrict__ skey, const uint8_t* __restrict__ fflag,
     ModelBuf m, const double4* __restrict__ node_dq, const double4* __restrict__ fvert,
     const double4* __restrict__ fnrm, PairParams pp, int* __restrict__ mm_idx,
     int* __restrict__ pair_s, int* __restrict__ n_pairs, uint8_t* __restrict__ pair_ok,
@@ -191,7 +192,18 @@ __global__ void __launch_bounds__(256, 3) k_assoc_pair_terms(
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   int ps = -1;
   if (c < pp.P) {
-    const int win = resolve_winner(pidx, sidx, c);
+    // resolve (raster.cpp:104-119), then reset the consumed z-buffer entries
+    // so the next GN iteration's splats start from empty maps without memsets
+    const int pw = pidx[c], sw = sidx[c];
+    const int win = pw != kEmptyIdx ? pw : (sw != kEmptyIdx ? sw : -1);
+    if (pw != kEmptyIdx) {
+      pidx[c] = kEmptyIdx;
+      pkey[c] = ~0ull;
+    }
+    if (sw != kEmptyIdx) {
+      sidx[c] = kEmptyIdx;
+      skey[c] = ~0ull;
+    }
     mm_idx[c] = win;
     ps = associate_pixel(c, win, m, fvert, fnrm, fflag, pp.pose);
     pair_s[c] = ps;
@@ -1665,7 +1677,8 @@ PairParams pair_params(Ctx& c, const double* pose) {
 
 // One GN linearisation at the current nodes (solver.cpp:316-369). Leaves e_data,
 // e_reg, ginf, |g|^2 (in pcg_rr slot) and tr(H) in DevScalars (no host sync).
-void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor) {
+void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor,
+                        bool maps_clean = false) {
   const int n = c.n_surfels, N = c.n_nodes, P = c.P;
   // fork: the pair-list resets (needed by the association kernel) and the node
   // transforms + E_reg (needed only by the assembly) run on a side branch,
@@ -1683,6 +1696,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
       DS_CUDA(cudaMemsetAsync(&c.dsc->pair_list_n, 0, sizeof(int), c.stream));
       DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
       DS_CUDA(cudaEventRecord(c.ev_mid, c.stream));
+      DS_CUDA(cudaMemsetAsync(c.g, 0, sizeof(double) * 6 * N, c.stream));  // assembly output
       node_se3(c, c.node_dq, c.node_se3);
       DS_LAUNCH(c, KK_ENERGY, 200.0 * N, cdiv(8 * N, 256), 256, 0, k_reg_energy, c.node_pos,
                 c.node_nbr, c.node_se3, N, c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg_pre,
@@ -1697,12 +1711,13 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   // only render-eligible surfels can be drawn / paired during the solve (the
   // post-solve forward_warp, pipeline.cpp:108, rewrites every live surfel):
   // warp + splat pass 1 fused, splat pass 2, then resolve + associate + terms
-  render_model_maps_list(c, pose, t_now, t_last, pose, c.elig, c.n_elig, c.node_dq, false);
+  render_model_maps_list(c, pose, t_now, t_last, pose, c.elig, c.n_elig, c.node_dq, false,
+                         !maps_clean);
   DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_mid, 0));  // pair-list resets done
   // per pixel: 2 x 4 B winner ids, frame maps 65 B, winner live 32 B, ids out 8 B; per pair:
   // surfel ref + skin 48 B, rows 96 B + r 8 B out
   DS_LAUNCH(c, KK_PAIR_TERMS, 113.0 * P + 152.0 * c.n_pairs_ok_est, nbp, 256, 0,
-            k_assoc_pair_terms, c.mm_pidx, c.mm_sidx, c.f_flag, c.M(), c.node_dq, c.f_vert,
+            k_assoc_pair_terms, c.mm_pidx, c.mm_sidx, c.mm_pkey, c.mm_skey, c.f_flag, c.M(), c.node_dq, c.f_vert,
             c.f_nrm, pair_params(c, pose), c.mm_idx, c.pair_s, &c.dsc->n_pairs, c.pair_ok,
             c.pair_rows, c.pair_r, c.s_cnt, c.s_head, c.red_part, c.tickets + 0,
             &c.dsc->e_data_pre);
@@ -1713,7 +1728,6 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   DS_LAUNCH(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_pair_next, c.pair_s, c.pair_ok, P, c.s_cnt,
             c.s_base, c.p_list, c.p_next);
   DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));  // join
-  DS_CUDA(cudaMemsetAsync(c.g, 0, sizeof(double) * 6 * N, c.stream));
   AsmArgs A;
   A.up_key = c.up_key;
   A.up_start = c.up_start;
@@ -1965,7 +1979,8 @@ bool build_solve_graph(Ctx& c, const double* pose, int t_now, int t_last, int ma
                                     cudaStreamCaptureModeThreadLocal) != cudaSuccess)
     return fail_();
   try {
-    gn_linearize_async(c, pose, t_now, t_last, true);
+    // maps are cleared before the graph launch and reset by their consumer
+    gn_linearize_async(c, pose, t_now, t_last, true, true);
   } catch (...) {
     cudaStreamEndCapture(c.stream, &tmp);
     fail_();
@@ -2108,6 +2123,7 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tb0)
                        .count());
     if (built) {
+      clear_model_maps(c);
       DS_CUDA(cudaGraphLaunch(c.g_solve.exec, c.stream));
       fetch_scalars(c);
       const DevScalars& h = *c.hsc;

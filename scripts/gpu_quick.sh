@@ -1,1 +1,1 @@
-python -m pytest tests/test_gpu_solve_fusion.py -m gpu -x -q -k "incremental or grid_knn or sequence" 2>&1 | tail -3
+python -m pytest tests -m gpu -x -q 2>&1 | grep -E "Error|error|assert|FAILED|passed|failed|>" | head -30

@@ -296,6 +296,7 @@ void allocate(Ctx& c) {
   if (const char* e = std::getenv("DS_KNN_EDGES_GRID")) c.knn_edges_grid = std::atoi(e);
   if (const char* e = std::getenv("DS_SCREEN_GRID")) c.screen_grid = e[0] != '0';
   if (const char* e = std::getenv("DS_INCR_GRID_MIN")) c.incr_grid_min = std::atoi(e);
+  if (const char* e = std::getenv("DS_NO_PDL")) c.use_pdl = e[0] == '0';
   if (const char* e = std::getenv("DS_INCR_CELL")) c.incr_cell = std::atof(e);
   if (const char* e = std::getenv("DS_PCG_SMEM")) c.pcg_smem_cap = std::min(std::atoi(e), c.pcg_smem_cap);
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));

@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <deque>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -249,6 +250,7 @@ struct Ctx {
   // greedy node hash
   KnnGrid grid_ref, grid_live;  // reference / live node positions
   KnnGrid grid_new;             // the nodes added this frame (incremental reskinning)
+  bool use_pdl = true;          // programmatic dependent launch in the GN chain (DS_NO_PDL=1 disables)
   int incr_grid_min = 16;       // new nodes above which grid_new is used (DS_INCR_GRID_MIN)
   double incr_cell = 4.0;       // grid_new cell size in node_sigma (DS_INCR_CELL)
   long long* ht_key = nullptr;
@@ -303,6 +305,36 @@ struct Ctx {
 void launch_begin(Ctx& c, int kind);
 void launch_end(Ctx& c, int kind, double bytes);
 void prof_flush(Ctx& c);
+// Programmatic dependent launch (PDL): the kernel may be scheduled while its
+// stream predecessor drains; it must call pdl_wait() before touching anything
+// the predecessor produces (every kernel launched with DS_LAUNCH_PDL does so
+// first thing; without the attribute the wait is a no-op).
+// (no early launch_dependents trigger: measured slower -- the dependents'
+// waiting CTAs then take slots from the draining predecessor)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(Ctx& c, dim3 grid, dim3 block, size_t smem, void (*k)(KArgs...),
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c.use_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+#define DS_LAUNCH_PDL(ctx, kind, bytes, grid, block, smem, kernel, ...)                    \
+  do {                                                                                     \
+    ::ds::launch_begin((ctx), (kind));                                                     \
+    DS_CUDA(::ds::launch_pdl((ctx), dim3(grid), dim3(block), (smem), kernel, __VA_ARGS__)); \
+    ::ds::launch_end((ctx), (kind), (double)(bytes));                                      \
+  } while (0)
+
 #define DS_LAUNCH(ctx, kind, bytes, grid, block, smem, kernel, ...)        \
   do {                                                                     \
     ::ds::launch_begin((ctx), (kind));                                     \

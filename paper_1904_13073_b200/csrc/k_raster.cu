@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
                                                      unsigned long long* skey, int* pidx,
                                                      int* sidx,
                                                      const double4* __restrict__ warp_dq = nullptr) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   const int k0 = blockIdx.x * blockDim.x + threadIdx.x;
   if (k0 >= n) return;
   const int i = list ? list[k0] : k0;
@@ -271,7 +272,9 @@ void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
                             const double* assoc_pose, const int* list, int n,
                             const double4* warp_dq, bool resolve, bool clear) {
   if (clear) clear_model_maps(c);
-  DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
+  // the pair counter of the resolve pass (without it, the caller's consumer
+  // counts and the caller resets it)
+  if (resolve) DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
   SplatParams sp;
   sp.cam = cam_params(c, pose);
   sp.t_now = t_now;
@@ -281,13 +284,13 @@ void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
   if (n > 0) {
     auto k_warp_splat = k_model_splat<false, true>;
     if (warp_dq)  // warp (96 B) + pass 1 (36 B) per listed surfel
-      DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 132.0 * n, cdiv(n, 256), 256, 0, k_warp_splat, c.M(), n,
+      DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 132.0 * n, cdiv(n, 256), 256, 0, k_warp_splat, c.M(), n,
                 list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx, warp_dq);
     else
-      DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(),
+      DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(),
                 n, list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
                 (const double4*)nullptr);
-    DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
+    DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
               list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
               (const double4*)nullptr);
   }

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(256, 3) k_assoc_pair_terms(
     float* __restrict__ rows, double* __restrict__ pair_r, int* __restrict__ s_cnt,
     int* __restrict__ s_head, double* __restrict__ part, unsigned* __restrict__ ticket,
     double* __restrict__ out) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   __shared__ int s_pix[256], s_srf[256];
   __shared__ int s_wcnt[8];
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(256) k_energy(const int* __restrict__ pair_s, 
                                                 unsigned* __restrict__ tickets,
                                                 double* __restrict__ e_data,
                                                 double* __restrict__ e_reg) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   if ((int)blockIdx.x < nbp) {
     __shared__ int s_list[256];
     __shared__ int s_wcnt[8];
@@ -372,6 +374,7 @@ __global__ void k_any_stable_flag(const float4* __restrict__ ln, int n, double d
 __global__ void k_pair_reserve(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
                                int P, const int* __restrict__ s_cnt, const int* __restrict__ s_head,
                                int* __restrict__ s_base, int* __restrict__ counter) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= P || !pair_ok[c]) return;
   const int s = pair_s[c];
@@ -381,6 +384,7 @@ __global__ void k_pair_reserve(const int* __restrict__ pair_s, const uint8_t* __
 __global__ void k_pair_fill(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
                             int P, const int* __restrict__ s_cnt, const int* __restrict__ s_base,
                             int* __restrict__ s_fill, int* __restrict__ p_list) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= P || !pair_ok[c]) return;
   const int s = pair_s[c];
@@ -389,6 +393,7 @@ __global__ void k_pair_fill(const int* __restrict__ pair_s, const uint8_t* __res
 __global__ void k_pair_next(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
                             int P, const int* __restrict__ s_cnt, const int* __restrict__ s_base,
                             const int* __restrict__ p_list, int* __restrict__ p_next) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= P || !pair_ok[c]) return;
   const int s = pair_s[c];
@@ -727,6 +732,7 @@ __device__ __forceinline__ void acc_surfel_record(const AsmArgs& A, int v, int c
 // flight per step (their count/offset and first-pair rows are loaded before
 // either is accumulated), the accumulation order is unchanged.
 __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int chunk = gid / kChunkLanes, l = gid % kChunkLanes;
   const bool valid = chunk < A.n_chunks;  // uniform within a lane group
@@ -860,6 +866,7 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
 // block, entry 42 the touched flag
 constexpr int kFinishEntries = 43;
 __global__ void k_assemble_finish(AsmArgs A, const int* __restrict__ multi, const int* __restrict__ n_multi) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int mi = gid / kFinishEntries, t = gid % kFinishEntries;
   if (mi >= *n_multi) return;
@@ -917,6 +924,7 @@ __global__ void __launch_bounds__(kStatsThreads) k_g_stats(
     const double* __restrict__ g, const float* __restrict__ val, const int* __restrict__ diag_pos,
     int N, int lm, double* __restrict__ part, unsigned* __restrict__ ticket,
     DevScalars* __restrict__ sc) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   __shared__ double smax[kStatsThreads], ssq[kStatsThreads], str[kStatsThreads];
   __shared__ bool last;
   const int tid = threadIdx.x, j = blockIdx.x * kStatsThreads + tid;
@@ -1694,6 +1702,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
       DS_CUDA(cudaMemsetAsync(c.s_head, 0x7f, sizeof(int) * (n + 1), c.stream));
       DS_CUDA(cudaMemsetAsync(c.s_fill, 0, sizeof(int) * (n + 1), c.stream));
       DS_CUDA(cudaMemsetAsync(&c.dsc->pair_list_n, 0, sizeof(int), c.stream));
+      DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
       DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
       DS_CUDA(cudaEventRecord(c.ev_mid, c.stream));
       DS_CUDA(cudaMemsetAsync(c.g, 0, sizeof(double) * 6 * N, c.stream));  // assembly output
@@ -1716,16 +1725,16 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_mid, 0));  // pair-list resets done
   // per pixel: 2 x 4 B winner ids, frame maps 65 B, winner live 32 B, ids out 8 B; per pair:
   // surfel ref + skin 48 B, rows 96 B + r 8 B out
-  DS_LAUNCH(c, KK_PAIR_TERMS, 113.0 * P + 152.0 * c.n_pairs_ok_est, nbp, 256, 0,
+  DS_LAUNCH_PDL(c, KK_PAIR_TERMS, 113.0 * P + 152.0 * c.n_pairs_ok_est, nbp, 256, 0,
             k_assoc_pair_terms, c.mm_pidx, c.mm_sidx, c.mm_pkey, c.mm_skey, c.f_flag, c.M(), c.node_dq, c.f_vert,
             c.f_nrm, pair_params(c, pose), c.mm_idx, c.pair_s, &c.dsc->n_pairs, c.pair_ok,
             c.pair_rows, c.pair_r, c.s_cnt, c.s_head, c.red_part, c.tickets + 0,
             &c.dsc->e_data_pre);
-  DS_LAUNCH(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_reserve, c.pair_s, c.pair_ok, P,
+  DS_LAUNCH_PDL(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_reserve, c.pair_s, c.pair_ok, P,
             c.s_cnt, c.s_head, c.s_base, &c.dsc->pair_list_n);
-  DS_LAUNCH(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_fill, c.pair_s, c.pair_ok, P, c.s_cnt,
+  DS_LAUNCH_PDL(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_fill, c.pair_s, c.pair_ok, P, c.s_cnt,
             c.s_base, c.s_fill, c.p_list);
-  DS_LAUNCH(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_pair_next, c.pair_s, c.pair_ok, P, c.s_cnt,
+  DS_LAUNCH_PDL(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_pair_next, c.pair_s, c.pair_ok, P, c.s_cnt,
             c.s_base, c.p_list, c.p_next);
   DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));  // join
   AsmArgs A;
@@ -1761,13 +1770,13 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
     // blocks written 144 B (both triangles) + g
     const double bytes = 12.0 * c.n_records + 104.0 * c.n_pairs_ok_est + 200.0 * 2 * c.n_chunks +
                          144.0 * c.n_full + 48.0 * N;
-    DS_LAUNCH(c, KK_BLOCK_ASSEMBLY, bytes, cdiv((long long)c.n_chunks * kChunkLanes, 256), 256, 0,
+    DS_LAUNCH_PDL(c, KK_BLOCK_ASSEMBLY, bytes, cdiv((long long)c.n_chunks * kChunkLanes, 256), 256, 0,
               k_assemble_chunks, A);
     if (c.n_multi > 0)
-      DS_LAUNCH(c, KK_BLOCK_ASSEMBLY, 0.0, cdiv((long long)c.n_multi * kFinishEntries, 256), 256, 0,
+      DS_LAUNCH_PDL(c, KK_BLOCK_ASSEMBLY, 0.0, cdiv((long long)c.n_multi * kFinishEntries, 256), 256, 0,
                 k_assemble_finish, A, c.multi_list, c.multi_scan + c.n_up);
   }
-  DS_LAUNCH(c, KK_REDUCE, 48.0 * N + 24.0 * N, std::max(1, cdiv(N, kStatsThreads)), kStatsThreads, 0,
+  DS_LAUNCH_PDL(c, KK_REDUCE, 48.0 * N + 24.0 * N, std::max(1, cdiv(N, kStatsThreads)), kStatsThreads, 0,
             k_g_stats, c.g, c.bsr_val, c.diag_pos, N, lm_floor ? 1 : 0, c.gst_part, c.tickets + 2,
             c.dsc);
 }
@@ -1833,7 +1842,7 @@ void energy_async(Ctx& c, const double* pose, const double4* dq, double* se3) {
   const int N = c.n_nodes, P = c.P;
   const int nbp = cdiv(P, 256), nbe = cdiv(8 * N, 256);
   // the node transforms `se3` of `dq` are written by apply_increments (fused)
-  DS_LAUNCH(c, KK_ENERGY, 120.0 * c.n_pairs_ok_est + 200.0 * N, nbp + nbe, 256, 0, k_energy,
+  DS_LAUNCH_PDL(c, KK_ENERGY, 120.0 * c.n_pairs_ok_est + 200.0 * N, nbp + nbe, 256, 0, k_energy,
             c.pair_s, c.M(), dq, c.f_vert, c.f_nrm, pair_params(c, pose), c.node_pos, c.node_nbr,
             se3, N, nbp, c.red_part, c.tickets, &c.dsc->e_data, &c.dsc->e_reg);
 }
@@ -1882,6 +1891,7 @@ __global__ void k_lm_init(DevScalars* sc) {
 __global__ void __launch_bounds__(256) k_lm_decide(DevScalars* sc, LmParams lp,
                                                    double4* __restrict__ node_dq,
                                                    const double4* __restrict__ node_dq_cand) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   __shared__ int s_acc;
   if (threadIdx.x == 0) {
     ++sc->lm_rounds;
@@ -2004,7 +2014,7 @@ bool build_solve_graph(Ctx& c, const double* pose, int t_now, int t_last, int ma
     pcg_solve_async(c, max_pcg, tol);
     apply_increments(c, c.pcg_x, c.node_dq_cand, c.node_se3_cand);
     energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
-    DS_LAUNCH(c, KK_MISC, 64.0 * 2 * c.n_nodes, 1, 256, 0, k_lm_decide, c.dsc, lp, c.node_dq,
+    DS_LAUNCH_PDL(c, KK_MISC, 64.0 * 2 * c.n_nodes, 1, 256, 0, k_lm_decide, c.dsc, lp, c.node_dq,
               c.node_dq_cand);
   } catch (...) {
     cudaStreamEndCapture(c.stream, &tmp);

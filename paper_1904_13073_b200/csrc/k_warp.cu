@@ -70,6 +70,7 @@ __global__ void k_node_live(const double4* __restrict__ pos, const double4* __re
 // the energy evaluation, fused here instead of a separate k_node_se3 launch
 __global__ void k_apply_increments(const double4* __restrict__ dq, const double* __restrict__ delta,
                                    int n, double4* __restrict__ out, double* __restrict__ se3) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const double* d = delta + 6 * j;
@@ -87,7 +88,7 @@ __global__ void k_apply_increments(const double4* __restrict__ dq, const double*
 
 void apply_increments(Ctx& c, const double* delta, double4* out, double* se3) {
   if (c.n_nodes == 0) return;
-  DS_LAUNCH(c, KK_NODE_UPDATE, (se3 ? 208.0 : 112.0) * c.n_nodes, cdiv(c.n_nodes, 128), 128, 0,
+  DS_LAUNCH_PDL(c, KK_NODE_UPDATE, (se3 ? 208.0 : 112.0) * c.n_nodes, cdiv(c.n_nodes, 128), 128, 0,
             k_apply_increments, c.node_dq, delta, c.n_nodes, out, se3);
 }
 

@@ -207,7 +207,7 @@ void allocate(Ctx& c) {
   c.rec_key = dalloc<int>(c, c.R_cap);
   c.rec_val = dalloc<int>(c, c.R_cap);
   c.rec_key2 = dalloc<int>(c, c.R_cap);
-  c.rec_val2 = dalloc<int>(c, c.R_cap);
+  c.rec_val2 = dalloc<int>(c, c.R_cap + 1);
   c.rec_flag = dalloc<int>(c, c.R_cap + 1);
   c.up_key = dalloc<int>(c, c.UB_cap);
   c.up_start = dalloc<int>(c, c.UB_cap + 1);
@@ -229,6 +229,16 @@ void allocate(Ctx& c) {
   c.part_h = dalloc<float>(c, (size_t)c.CH_cap * 36);
   c.part_g = dalloc<double>(c, (size_t)c.CH_cap * 6);
   c.part_t = dalloc<int>(c, c.CH_cap);
+  c.REG_cap = 24 * N;  // 3 records per directed edge, 8 edges per node
+  c.RB_cap = 9 * N;    // distinct upper blocks of the graph: N diagonal + <= 8 N edges
+  c.reg_rec = dalloc<int>(c, c.REG_cap + 1);
+  c.reg_ub = dalloc<int>(c, c.REG_cap + 1);
+  c.reg_bf = dalloc<int>(c, c.REG_cap + 1);
+  c.reg_bscan = dalloc<int>(c, c.REG_cap + 2);
+  c.reg_blk_start = dalloc<int>(c, c.RB_cap + 2);
+  c.ub_reg = dalloc<int>(c, c.UB_cap + 1);
+  c.reg_h = dalloc<double>(c, (size_t)c.RB_cap * 36);
+  c.reg_g = dalloc<double>(c, (size_t)c.RB_cap * 6);
   c.elig = dalloc<int>(c, S);
   c.cub_tmp_bytes = std::max(sort_temp_bytes(c.R_cap), sort_temp_bytes(P));
   c.cub_tmp = dalloc<char>(c, c.cub_tmp_bytes);

@@ -208,6 +208,18 @@ struct Ctx {
   float* part_h = nullptr;     // per chunk: 6x6 partial
   double* part_g = nullptr;    // per chunk: g partial
   int* part_t = nullptr;       // per chunk: touched
+  // regulariser terms, assembled apart from the surfel records (per frame:
+  // the reg records' sorted positions grouped by upper block; per GN
+  // iteration: their 6x6 sums on the side branch, added by the assembly)
+  int* reg_rec = nullptr;        // reg record words (edge, type) in sorted order
+  int* reg_ub = nullptr;         // their upper blocks
+  int* reg_bf = nullptr;         // block-start flags -> exclusive scan (reg_bscan)
+  int* reg_bscan = nullptr;
+  int* reg_blk_start = nullptr;  // per reg block: first reg record (+ end)
+  int* ub_reg = nullptr;         // per upper block: reg block or -1
+  double* reg_h = nullptr;       // per reg block: 6x6 sum
+  double* reg_g = nullptr;       // per reg block: g sum (diagonal blocks)
+  int REG_cap = 0, RB_cap = 0, reg_cap_now = 0;
   int* elig = nullptr;  // render-eligible surfels of the current frame's solve
   int n_elig = 0;
   int n_records = 0, n_up = 0, n_full = 0, n_chunks = 0, n_multi = 0, CH_cap = 0;

@@ -509,6 +509,43 @@ __global__ void k_write_up(const int* __restrict__ key, const int* __restrict__ 
   }
   if (k + 1 == n || key[k + 1] == none) up_start[total] = k + 1;
 }
+// Regulariser records grouped by upper block (per frame). rec_flag holds the
+// exclusive scan of the block-start flags, so record k lies in block
+// rec_flag[k + 1] - 1.
+__global__ void k_reg_mark(const int* __restrict__ key, const int* __restrict__ val, int n, int none,
+                           int* __restrict__ flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  flag[k] = (key[k] != none && val[k] < 0) ? 1 : 0;
+}
+__global__ void k_reg_compact(const int* __restrict__ flag, const int* __restrict__ scan, int n,
+                              const int* __restrict__ val, const int* __restrict__ ub_scan,
+                              int* __restrict__ reg_rec, int* __restrict__ reg_ub) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || !flag[k]) return;
+  const int j = scan[k];
+  reg_rec[j] = val[k];  // the record word (edge, type), in sorted order
+  reg_ub[j] = ub_scan[k + 1] - 1;
+}
+__global__ void k_reg_bmark(const int* __restrict__ reg_ub, const int* __restrict__ n_reg_dev,
+                            int cap, int* __restrict__ bf) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cap) return;
+  bf[j] = (j < *n_reg_dev && (j == 0 || reg_ub[j] != reg_ub[j - 1])) ? 1 : 0;
+}
+__global__ void k_reg_bfill(const int* __restrict__ reg_ub, const int* __restrict__ bf,
+                            const int* __restrict__ bscan, const int* __restrict__ n_reg_dev,
+                            int cap, int* __restrict__ blk_start, int* __restrict__ ub_reg) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_reg = *n_reg_dev;
+  if (j >= n_reg) return;
+  if (bf[j]) {
+    blk_start[bscan[j]] = j;
+    ub_reg[reg_ub[j]] = bscan[j];
+  }
+  if (j == n_reg - 1) blk_start[bscan[cap]] = n_reg;
+}
+
 __global__ void k_row_count(const int* __restrict__ up_key, const int* __restrict__ n_up_dev, int N,
                             int* __restrict__ row_cnt) {
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
@@ -626,6 +663,9 @@ struct AsmArgs {
   float* bsr_val;
   uint8_t* bsr_touch;
   double* g;
+  const int* ub_reg;   // per upper block: regulariser block or -1
+  const double* reg_h;  // per regulariser block: 6x6 sum (k_reg_blocks)
+  const double* reg_g;
 };
 
 // column x of reg_jacobian_j = [-[a]x, I] (sel 0) or reg_jacobian_i = [[b]x, -I]
@@ -647,43 +687,62 @@ __device__ __forceinline__ V3 reg_col(int sel, int x, const V3& a, const V3& b) 
   }
 }
 
-// Regulariser record (edge e = 8 j + slot, type 0: JjtJj / gj, 1: JitJi / gi,
-// 2: JjtJi, 3: JitJj) accumulated like the surfel records (float per term).
-__device__ __forceinline__ void acc_reg_record(const AsmArgs& A, int v, float h[36],
-                                               double gg[6]) {
-  const int e = (v & 0x7fffffff) >> 2, type = v & 3;
-  const double2* ab = reinterpret_cast<const double2*>(A.reg_ab + 6 * (size_t)e);
-  const double2 u0 = __ldg(ab), u1 = __ldg(ab + 1), u2 = __ldg(ab + 2);
-  const V3 a = v3(u0.x, u0.y, u1.x), b = v3(u1.y, u2.x, u2.y);
-  const V3 rv = sub(a, b);
-  const int ls = (type == 0 || type == 2) ? 0 : 1, rs = (type == 0 || type == 3) ? 0 : 1;
-  // one block row at a time (rolled loop, constant-index row update via the
-  // switch) keeps the live set small next to the 36 accumulators
-#pragma unroll 1
-  for (int x = 0; x < 6; ++x) {
-    const V3 L = reg_col(ls, x, a, b);
-    float t[6];
+inline int reg_rb_pad(int N) { return (9 * N + 31) / 32 * 32; }  // reg block bound, warp multiple
+
+// Regulariser blocks (per GN iteration, side branch): thread per (block row
+// x, reg block), x uniform across a warp (the reg_col switch on x does not
+// diverge); the thread sums row x of the 6x6 block and g[x] of a diagonal
+// block over the block's records in order, in fp64. Records: edge e = 8 j +
+// slot, type 0: JjtJj / gj, 1: JitJi / gi, 2: JjtJi, 3: JitJj
+// (solver.cpp:118-130). Four records per step are loaded together.
+__global__ void __launch_bounds__(256) k_reg_blocks(const int* __restrict__ reg_val,
+                                                    const int* __restrict__ blk_start,
+                                                    const int* __restrict__ n_rb_dev, int rb_pad,
+                                                    const double* __restrict__ reg_ab, double lambda,
+                                                    double* __restrict__ reg_h,
+                                                    double* __restrict__ reg_g) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int x = gid / rb_pad, rb = gid % rb_pad;
+  if (x >= 6 || rb >= *n_rb_dev) return;
+  const int j0 = blk_start[rb], j1 = blk_start[rb + 1];
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  double gacc = 0.0;
+  for (int j = j0; j < j1; j += 4) {
+    int v[4];
+    double2 u[4][3];
 #pragma unroll
-    for (int y = 0; y < 6; ++y) {
-      const V3 R = reg_col(rs, y, a, b);
-      t[y] = (float)(A.lambda * ((L.x * R.x + L.y * R.y) + L.z * R.z));
-    }
-    const double gx = type <= 1 ? A.lambda * ((L.x * rv.x + L.y * rv.y) + L.z * rv.z) : 0.0;
-    switch (x) {
-#define DS_REG_ROW(X)                                   \
-  case X:                                               \
-    _Pragma("unroll") for (int y = 0; y < 6; ++y) h[X * 6 + y] += t[y]; \
-    if (type <= 1) gg[X] += gx;                         \
-    break;
-      DS_REG_ROW(0)
-      DS_REG_ROW(1)
-      DS_REG_ROW(2)
-      DS_REG_ROW(3)
-      DS_REG_ROW(4)
-      DS_REG_ROW(5)
-#undef DS_REG_ROW
+    for (int q = 0; q < 4; ++q) v[q] = j + q < j1 ? __ldg(reg_val + j + q) : 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (j + q < j1) {
+        const double2* ab =
+            reinterpret_cast<const double2*>(reg_ab + 6 * (size_t)((v[q] & 0x7fffffff) >> 2));
+        u[q][0] = __ldg(ab);
+        u[q][1] = __ldg(ab + 1);
+        u[q][2] = __ldg(ab + 2);
+      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j + q >= j1) continue;
+      const int type = v[q] & 3;
+      const V3 a = v3(u[q][0].x, u[q][0].y, u[q][1].x), b = v3(u[q][1].y, u[q][2].x, u[q][2].y);
+      const int ls = (type == 0 || type == 2) ? 0 : 1, rs = (type == 0 || type == 3) ? 0 : 1;
+      const V3 L = reg_col(ls, x, a, b);
+#pragma unroll
+      for (int y = 0; y < 6; ++y) {
+        const V3 R = reg_col(rs, y, a, b);
+        acc[y] += lambda * ((L.x * R.x + L.y * R.y) + L.z * R.z);
+      }
+      if (type <= 1) {
+        const V3 rv = sub(a, b);
+        gacc += lambda * ((L.x * rv.x + L.y * rv.y) + L.z * rv.z);
+      }
     }
   }
+#pragma unroll
+  for (int y = 0; y < 6; ++y) reg_h[(size_t)rb * 36 + x * 6 + y] = acc[y];
+  reg_g[(size_t)rb * 6 + x] = gacc;
 }
 
 __device__ __forceinline__ void load_rows(const float* __restrict__ rw, int mr, int mc, float a[6],
@@ -700,15 +759,18 @@ __device__ __forceinline__ void load_rows(const float* __restrict__ rw, int mr, 
   }
 }
 
+// explicit fused multiply-adds (one rounding per term; the build's
+// --fmad=false only stops implicit contraction, which the fp64 decision
+// arithmetic elsewhere relies on)
 __device__ __forceinline__ void acc_pair(const float a[6], const float b[6], bool diag, double r,
                                          float h[36], double gg[6]) {
 #pragma unroll
   for (int x = 0; x < 6; ++x)
 #pragma unroll
-    for (int y = 0; y < 6; ++y) h[x * 6 + y] += a[x] * b[y];
+    for (int y = 0; y < 6; ++y) h[x * 6 + y] = __fmaf_rn(a[x], b[y], h[x * 6 + y]);
   if (diag) {
 #pragma unroll
-    for (int x = 0; x < 6; ++x) gg[x] += (double)a[x] * r;
+    for (int x = 0; x < 6; ++x) gg[x] = __fma_rn((double)a[x], r, gg[x]);
   }
 }
 
@@ -789,20 +851,15 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
         load_rows(A.rows + (size_t)hA1 * 24, (vA1 >> 2) & 3, vA1 & 3, a1, b1);
         if (diag) rr1 = __ldg(A.pair_r + hA1);
       }
+      // regulariser records (v < 0) are summed by k_reg_blocks
       if (vA0 != kNone) {
-        if (vA0 < 0) {
-          acc_reg_record(A, vA0, h, gg);
-          touched = 1;
-        } else if (cA0 > 0) {
+        if (vA0 >= 0 && cA0 > 0) {
           acc_surfel_record(A, vA0, cA0, hA0, a0, b0, rr0, diag, h, gg);
           touched = 1;
         }
       }
       if (vA1 != kNone) {
-        if (vA1 < 0) {
-          acc_reg_record(A, vA1, h, gg);
-          touched = 1;
-        } else if (cA1 > 0) {
+        if (vA1 >= 0 && cA1 > 0) {
           acc_surfel_record(A, vA1, cA1, hA1, a1, b1, rr1, diag, h, gg);
           touched = 1;
         }
@@ -828,15 +885,19 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
   }
   if (!valid) return;
   if (c1 - c0 == 1) {
-    // single-chunk block (most off-diagonal ones): the partial is final; the
-    // lanes write it straight into the BSR (both triangles) and g
+    // single-chunk block (most off-diagonal ones): the partial plus the
+    // block's regulariser sum is final; the lanes write it straight into the
+    // BSR (both triangles) and g
     const int pu = A.up_pos[ub];
     const int pm = diag ? -1 : A.up_mpos[ub];
+    const int rb = A.ub_reg[ub];
+    if (rb >= 0) touched = 1;
 #pragma unroll
     for (int t = 0; t < 36; ++t) {
       if (t % kChunkLanes != l) continue;
-      A.bsr_val[(size_t)pu * 36 + t] = h[t];
-      if (pm >= 0) A.bsr_val[(size_t)pm * 36 + (t % 6) * 6 + t / 6] = h[t];
+      const float v = rb >= 0 ? (float)((double)h[t] + __ldg(A.reg_h + (size_t)rb * 36 + t)) : h[t];
+      A.bsr_val[(size_t)pu * 36 + t] = v;
+      if (pm >= 0) A.bsr_val[(size_t)pm * 36 + (t % 6) * 6 + t / 6] = v;
     }
     if (l == 0) {
       A.bsr_touch[pu] = touched ? 1 : 0;
@@ -846,7 +907,7 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
       const int row = key / A.N;
 #pragma unroll
       for (int x = 0; x < 6; ++x)
-        if (x == l) A.g[6 * row + x] = gg[x];
+        if (x == l) A.g[6 * row + x] = rb >= 0 ? gg[x] + __ldg(A.reg_g + (size_t)rb * 6 + x) : gg[x];
     }
     return;
   }
@@ -876,10 +937,12 @@ __global__ void k_assemble_finish(AsmArgs A, const int* __restrict__ multi, cons
   const int c0 = A.chunk_first[ub], c1 = A.chunk_first[ub + 1];
   const int pu = A.up_pos[ub];
   const int pm = row != colb ? A.up_mpos[ub] : -1;
+  const int rb = A.ub_reg[ub];
   if (t < 36) {
     double acc = 0.0;
 #pragma unroll 4
     for (int c = c0; c < c1; ++c) acc += (double)A.part_h[(size_t)c * 36 + t];
+    if (rb >= 0) acc += A.reg_h[(size_t)rb * 36 + t];
     A.bsr_val[(size_t)pu * 36 + t] = (float)acc;
     if (pm >= 0) A.bsr_val[(size_t)pm * 36 + (t % 6) * 6 + t / 6] = (float)acc;
   } else if (t < 42) {
@@ -887,9 +950,10 @@ __global__ void k_assemble_finish(AsmArgs A, const int* __restrict__ multi, cons
     double acc = 0.0;
 #pragma unroll 4
     for (int c = c0; c < c1; ++c) acc += A.part_g[(size_t)c * 6 + (t - 36)];
+    if (rb >= 0) acc += A.reg_g[(size_t)rb * 6 + (t - 36)];
     A.g[6 * row + (t - 36)] = acc;
   } else {
-    int touched = 0;
+    int touched = rb >= 0 ? 1 : 0;
     for (int c = c0; c < c1; ++c) touched |= A.part_t[c];
     A.bsr_touch[pu] = touched ? 1 : 0;
     if (pm >= 0) A.bsr_touch[pm] = touched ? 1 : 0;
@@ -1640,6 +1704,23 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
   c.n_up = host[0];
   c.n_full = host[1];
   c.n_records = R;
+  // regulariser records grouped by upper block (k_reg_blocks sums them per
+  // GN iteration; the assembly adds the sums)
+  c.reg_cap_now = 24 * N;
+  if (N > 0) {
+    DS_LAUNCH(c, KK_PATTERN, 12.0 * R, cdiv(R, 256), 256, 0, k_reg_mark, c.rec_key, c.rec_val, R,
+              none, c.rec_key2);
+    scan_exclusive(c, c.rec_key2, c.rec_val2, R);
+    DS_LAUNCH(c, KK_PATTERN, 12.0 * R, cdiv(R, 256), 256, 0, k_reg_compact, c.rec_key2, c.rec_val2,
+              R, c.rec_val, c.rec_flag, c.reg_rec, c.reg_ub);
+    DS_LAUNCH(c, KK_PATTERN, 12.0 * c.reg_cap_now, cdiv(c.reg_cap_now, 256), 256, 0, k_reg_bmark,
+              c.reg_ub, c.rec_val2 + R, c.reg_cap_now, c.reg_bf);
+    scan_exclusive(c, c.reg_bf, c.reg_bscan, c.reg_cap_now);
+    DS_CUDA(cudaMemsetAsync(c.ub_reg, 0xff, sizeof(int) * std::max(1, c.n_up), c.stream));
+    DS_LAUNCH(c, KK_PATTERN, 16.0 * c.reg_cap_now, cdiv(c.reg_cap_now, 256), 256, 0, k_reg_bfill,
+              c.reg_ub, c.reg_bf, c.reg_bscan, c.rec_val2 + R, c.reg_cap_now, c.reg_blk_start,
+              c.ub_reg);
+  }
   if (c.n_up > 0) {
     DS_LAUNCH(c, KK_PATTERN, 16.0 * c.n_up, cdiv(c.n_up, 256), 256, 0, k_row_fill, c.up_key,
               n_up_dev, N, c.row_ptr, c.row_cnt, c.bsr_col, c.bsr_tag);
@@ -1710,6 +1791,10 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
       DS_LAUNCH(c, KK_ENERGY, 200.0 * N, cdiv(8 * N, 256), 256, 0, k_reg_energy, c.node_pos,
                 c.node_nbr, c.node_se3, N, c.red_part + nbp, c.tickets + 1, &c.dsc->e_reg_pre,
                 c.reg_ab);
+      if (N > 0)
+        DS_LAUNCH(c, KK_ENERGY, 48.0 * c.reg_cap_now, cdiv(6LL * reg_rb_pad(N), 256), 256, 0,
+                  k_reg_blocks, c.reg_rec, c.reg_blk_start, c.reg_bscan + c.reg_cap_now,
+                  reg_rb_pad(N), c.reg_ab, c.cfg.lambda, c.reg_h, c.reg_g);
     } catch (...) {
       c.stream = main_stream;
       throw;
@@ -1764,6 +1849,9 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   A.bsr_val = c.bsr_val;
   A.bsr_touch = c.bsr_touch;
   A.g = c.g;
+  A.ub_reg = c.ub_reg;
+  A.reg_h = c.reg_h;
+  A.reg_g = c.reg_g;
   if (c.n_up > 0) {
     // algorithmic bytes: records 4 B + (count, offset) 8 B each, the paired
     // surfels' list-ordered rows/residuals (104 B) once, chunk partials out+in,

@@ -290,6 +290,7 @@ void allocate(Ctx& c) {
   const size_t scan_max = std::max({(size_t)c.R_cap, S + P, P * f * f, N + 1});
   c.scan_tmp_n = cdiv((long long)scan_max, 4096) + 16;
   c.scan_tmp = dalloc<int>(c, c.scan_tmp_n);
+  c.scan_status = dalloc<unsigned long long>(c, c.scan_tmp_n);
   c.red_part_n = cdiv(c.P, 256) * 29 + cdiv(8 * (long long)N, 256) + cdiv(c.P, 256) + 64;
   c.red_part = dalloc<double>(c, c.red_part_n);
   c.d_pose = dalloc<double>(c, 12);

@@ -270,6 +270,7 @@ struct Ctx {
   int* ht_ids = nullptr;
   // scratch
   int* scan_tmp = nullptr;
+  unsigned long long* scan_status = nullptr;  // look-back scan tile status words
   int scan_tmp_n = 0;
   double* red_part = nullptr;
   int red_part_n = 0;

@@ -1,7 +1,9 @@
 // k_scan.cu — deterministic scan / reduction utilities used for stream compaction
 // (order-preserving, fusion.cpp:264-284) and fixed-order fp64 reductions.
+#include <cub/block/block_load.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/block/block_store.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "ds_context.cuh"
@@ -9,64 +11,75 @@
 namespace ds {
 
 namespace {
-constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 4;
+// Single-pass exclusive scan with decoupled look-back: tile t publishes its
+// aggregate (flag A), sums its predecessors' published values back to the
+// first inclusive prefix (flag P), publishes its own inclusive prefix and
+// adds the exclusive prefix to its locally scanned items. Integer sums: the
+// result does not depend on the order. Status words (flag << 32 | value) are
+// cleared by a memset before each scan (graph-replay safe).
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
+#define kFlagA (1ull << 32)
+#define kFlagP (2ull << 32)
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(const int* __restrict__ in, int n,
-                                                                 int* __restrict__ sums) {
-  using BR = cub::BlockReduce<int, kScanThreads>;
-  __shared__ typename BR::TempStorage tmp;
-  const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-  int s = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k)
-    if (base + k < n) s += in[base + k];
-  const int tot = BR(tmp).Sum(s);
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_sums(int* __restrict__ sums, int nb,
-                                                            int* __restrict__ total) {
+__global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int* in, int n, int* out,
+                                                                unsigned long long* status) {
+  using BL = cub::BlockLoad<int, kScanThreads, kScanItems, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
   using BS = cub::BlockScan<int, kScanThreads>;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < nb; base += kScanThreads) {
-    const int i = base + threadIdx.x;
-    const int v = i < nb ? sums[i] : 0;
-    int ex, agg;
-    BS(tmp).ExclusiveSum(v, ex, agg);
-    if (i < nb) sums[i] = ex + carry;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += agg;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total = carry;
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int* in, int n,
-                                                             const int* __restrict__ sums,
-                                                             int* out) {
-  using BS = cub::BlockScan<int, kScanThreads>;
-  __shared__ typename BS::TempStorage tmp;
-  const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  using BST = cub::BlockStore<int, kScanThreads, kScanItems, cub::BLOCK_STORE_WARP_TRANSPOSE>;
+  __shared__ union {
+    typename BL::TempStorage load;
+    typename BS::TempStorage scan;
+    typename BST::TempStorage store;
+  } tmp;
+  __shared__ int s_prefix;
+  const int tile = blockIdx.x;
+  const long long base = (long long)tile * kScanTile;
+  const int valid = (int)min((long long)kScanTile, (long long)n - base);
   int v[kScanItems];
-  int s = 0;
+  BL(tmp.load).Load(in + base, v, valid, 0);  // in == out allowed: read before written
+  __syncthreads();
+  int agg;
+  BS(tmp.scan).ExclusiveSum(v, v, agg);
+  if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors at a time
+    volatile unsigned long long* st = status;
+    const int lane = threadIdx.x;
+    int prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st[0] = kFlagP | (unsigned)agg;
+    } else {
+      if (lane == 0) st[tile] = kFlagA | (unsigned)agg;
+      int hi = tile - 1;  // window [hi - 31, hi], lane l reads hi - l
+      while (true) {
+        const int j = hi - lane;
+        unsigned long long w = j >= 0 ? st[j] : kFlagP;  // before tile 0: prefix 0
+        while (__any_sync(0xffffffffu, (w & (3ull << 32)) == 0))
+          if ((w & (3ull << 32)) == 0) w = st[j];
+        const unsigned pmask = __ballot_sync(0xffffffffu, (w & (3ull << 32)) == kFlagP);
+        // lanes up to the nearest inclusive prefix contribute
+        const int stop = pmask ? __ffs(pmask) - 1 : 31;
+        int val = (lane <= stop && j >= 0) ? (int)(unsigned)w : 0;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    v[k] = (base + k < n) ? in[base + k] : 0;
-    s += v[k];
+        for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
+        prefix += val;
+        if (pmask) break;
+        hi -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        st[tile] = kFlagP | (unsigned)(prefix + agg);
+      }
+    }
+    if (lane == 0) {
+      s_prefix = prefix;
+      if (tile == gridDim.x - 1) out[n] = prefix + agg;
+    }
   }
-  int ex;
-  BS(tmp).ExclusiveSum(s, ex);
-  int run = ex + sums[blockIdx.x];
+  __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    if (base + k < n) out[base + k] = run;
-    run += v[k];
-  }
+  for (int k = 0; k < kScanItems; ++k) v[k] += s_prefix;
+  BST(tmp.store).Store(out + base, v, valid);
 }
 
 }  // namespace
@@ -78,9 +91,8 @@ void scan_exclusive(Ctx& c, const int* in, int* out, int n) {
   }
   const int nb = cdiv(n, kScanTile);
   if (nb > c.scan_tmp_n) fail(DS_ERR_CAPACITY, "scan scratch too small");
-  DS_LAUNCH(c, KK_SCAN, 4.0 * n, nb, kScanThreads, 0, k_scan_tile_sums, in, n, c.scan_tmp);
-  DS_LAUNCH(c, KK_SCAN, 8.0 * nb, 1, kScanThreads, 0, k_scan_sums, c.scan_tmp, nb, out + n);
-  DS_LAUNCH(c, KK_SCAN, 8.0 * n, nb, kScanThreads, 0, k_scan_apply, in, n, c.scan_tmp, out);
+  DS_CUDA(cudaMemsetAsync(c.scan_status, 0, sizeof(unsigned long long) * nb, c.stream));
+  DS_LAUNCH(c, KK_SCAN, 8.0 * n, nb, kScanThreads, 0, k_scan_lookback, in, n, out, c.scan_status);
 }
 
 void sort_pairs(Ctx& c, int* keys, int* vals, int* keys_alt, int* vals_alt, int n, int end_bit,

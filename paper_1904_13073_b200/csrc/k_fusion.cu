@@ -507,22 +507,39 @@ __global__ void __launch_bounds__(256) k_remove(ModelBuf m, const int* __restric
       const double fsx = floor(rp.f * (u + 0.5)), fsy = floor(rp.f * (v + 0.5));
       const int Wf = rp.W * rp.f, Hf = rp.H * rp.f;
       if (fabs(fsx) < 1e9 && fabs(fsy) < 1e9) {
+        // the 3x3 neighbourhood's ids, then their surfels three at a time: the
+        // verdict is an OR over the neighbours, so all loads can be in flight
         const int sx = (int)fsx, sy = (int)fsy;
-        for (int dy = -1; dy <= 1 && !rm; ++dy)
-          for (int dx = -1; dx <= 1; ++dx) {
-            const int nx = sx + dx, ny = sy + dy;
-            if (nx < 0 || nx >= Wf || ny < 0 || ny >= Hf) continue;
-            const int j = im_idx[(size_t)ny * Wf + nx];
+        int js[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+          const int nx = sx + q % 3 - 1, ny = sy + q / 3 - 1;
+          js[q] = (nx < 0 || nx >= Wf || ny < 0 || ny >= Hf) ? kEmptyIdx
+                                                             : __ldg(im_idx + (size_t)ny * Wf + nx);
+        }
+#pragma unroll
+        for (int g = 0; g < 9; g += 3) {
+          float4 op[3], on[3];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const int j = js[g + q];
+            if (j != kEmptyIdx && j != i) {
+              op[q] = m.lp[j];
+              on[q] = m.ln[j];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const int j = js[g + q];
             if (j == kEmptyIdx || j == i) continue;
-            const float4 op = m.lp[j], on = m.ln[j];
-            const double oc = on.w;
+            const double oc = on[q].w;
             if (oc <= rp.delta_stable) continue;
             if (oc <= ci) continue;
-            if (nrm(sub(v3(op.x, op.y, op.z), sp)) >= rp.delta_distance) continue;
-            if (dot(v3(on.x, on.y, on.z), sn) < rp.delta_normal) continue;
+            if (nrm(sub(v3(op[q].x, op[q].y, op[q].z), sp)) >= rp.delta_distance) continue;
+            if (dot(v3(on[q].x, on[q].y, on[q].z), sn) < rp.delta_normal) continue;
             rm = 1;
-            break;
           }
+        }
       }
     }
   }

@@ -200,12 +200,42 @@ __global__ void __launch_bounds__(kGreedyThreads) k_greedy_nodes(
 // Exact pre-filter for extension: a candidate within sigma of a pre-existing
 // node is skipped by the ordered greedy whatever happens before it, so only the
 // uncovered ones (kept in order) need the sequential pass.
+// kUncLanes lanes per candidate split the 27 cells; a covered candidate
+// (the common case) stops after the first round, where lane 0 holds its own cell.
+constexpr int kUncLanes = 8;
 __global__ void k_uncovered(const float4* __restrict__ cand, int M, double sigma, HashView h,
                             const double4* __restrict__ node_pos, int* __restrict__ flag) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = gt / kUncLanes, lane = gt % kUncLanes;
+  if (i >= M) return;  // whole group
+  const unsigned gmask = 0xffu << ((threadIdx.x & 31) & ~(unsigned)(kUncLanes - 1));
   const float4 cp = cand[i];
-  flag[i] = ht_any_within(h, node_pos, v3(cp.x, cp.y, cp.z), sigma * sigma) ? 0 : 1;
+  const V3 p = v3(cp.x, cp.y, cp.z);
+  const double r2 = sigma * sigma;
+  int cx, cy, cz;
+  cell_of(h, p, cx, cy, cz);
+  bool found = false;
+  for (int base = 0; base < 27; base += kUncLanes) {
+    const int o = base + lane;
+    if (o < 27 && !found) {
+      const int oc = (o + 13) % 27;  // 13 = (0,0,0): lane 0 of round 0 takes the own cell
+      const int dx = oc % 3 - 1, dy = (oc / 3) % 3 - 1, dz = oc / 9 - 1;
+      const int s = ht_find(h, pack_cell(cx + dx, cy + dy, cz + dz));
+      if (s >= 0) {
+        const int c = __ldcg(h.cnt + s);
+        for (int q = 0; q < c && !found; ++q) {
+          const int id = __ldcg(h.ids + 8 * s + q);
+          const double4 np = ldcg_d4(node_pos + id);
+          if (sqn(sub(v3(np.x, np.y, np.z), p)) < r2) found = true;
+        }
+      }
+    }
+    if (__any_sync(gmask, found)) {
+      found = true;
+      break;
+    }
+  }
+  if (lane == 0) flag[i] = found ? 0 : 1;
 }
 __global__ void k_gather_uncovered(const float4* __restrict__ cand, const int* __restrict__ flag,
                                    const int* __restrict__ scan, int M, float4* __restrict__ out) {
@@ -763,7 +793,7 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
     DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
     DS_LAUNCH(c, KK_GREEDY_NODES, 32.0 * n0, cdiv(n0, 256), 256, 0, k_ht_prefill, hash_view(c),
               c.node_pos, n0, &c.dsc->err);
-    DS_LAUNCH(c, KK_GREEDY_NODES, 20.0 * n, cdiv(n, 256), 256, 0, k_uncovered, positions, n,
+    DS_LAUNCH(c, KK_GREEDY_NODES, 20.0 * n, cdiv((long long)n * kUncLanes, 256), 256, 0, k_uncovered, positions, n,
               c.cfg.node_sigma, hash_view(c), c.node_pos, c.keep);
     scan_exclusive(c, c.keep, c.keep_scan, n);
     DS_LAUNCH(c, KK_GREEDY_NODES, 24.0 * n, cdiv(n, 256), 256, 0, k_gather_uncovered, positions,

@@ -323,18 +323,15 @@ __device__ int screen_group(V3 x, const double bd[4], const int bi[4],
 constexpr int kScreenLanes = 8;
 constexpr int kScreenThreads = 256;
 
-__global__ void __launch_bounds__(kScreenThreads, 2) k_screen(
-    const float4* __restrict__ cp, const int* __restrict__ n_cand_dev,
+// one block's group of kScreenThreads / kScreenLanes candidates from `kb`
+__device__ __forceinline__ void screen_block(
+    int kb, int n, float4* tile, const float4* __restrict__ cp,
     const double4* __restrict__ node_pos, const double4* __restrict__ node_live,
     const float4* __restrict__ node_live_f, const int* __restrict__ rmax_bits,
-    const double4* __restrict__ node_dq, ScreenParams sp, int4* __restrict__ cki,
+    const double4* __restrict__ node_dq, const ScreenParams& sp, int4* __restrict__ cki,
     float4* __restrict__ ckw, int* __restrict__ ok, int* __restrict__ res_out,
-    int* __restrict__ low, int* __restrict__ comp, KnnGridView grid, int use_grid) {
-  __shared__ float4 tile[kScreenThreads];
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int k = gt / kScreenLanes, lane_k = gt % kScreenLanes;
-  const int n = *n_cand_dev;
-  if (blockIdx.x * (kScreenThreads / kScreenLanes) >= n) return;  // whole block idle
+    int* __restrict__ low, int* __restrict__ comp, const KnnGridView& grid, int use_grid) {
+  const int k = kb + threadIdx.x / kScreenLanes, lane_k = threadIdx.x % kScreenLanes;
   const bool active = k < n;
   double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
   int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
@@ -453,6 +450,24 @@ __global__ void __launch_bounds__(kScreenThreads, 2) k_screen(
   if (res == 1) atomicAdd(comp, 1);
   cki[k] = make_int4(ids[0], ids[1], ids[2], ids[3]);
   ckw[k] = make_float4(ws[0], ws[1], ws[2], ws[3]);
+}
+
+// Persistent grid (the candidate count is on the device): blocks stride over
+// candidate groups; every thread of a block runs the same rounds (the tiled
+// fallback synchronises the block).
+__global__ void __launch_bounds__(kScreenThreads, 2) k_screen(
+    const float4* __restrict__ cp, const int* __restrict__ n_cand_dev,
+    const double4* __restrict__ node_pos, const double4* __restrict__ node_live,
+    const float4* __restrict__ node_live_f, const int* __restrict__ rmax_bits,
+    const double4* __restrict__ node_dq, ScreenParams sp, int4* __restrict__ cki,
+    float4* __restrict__ ckw, int* __restrict__ ok, int* __restrict__ res_out,
+    int* __restrict__ low, int* __restrict__ comp, KnnGridView grid, int use_grid) {
+  __shared__ float4 tile[kScreenThreads];
+  const int n = *n_cand_dev;
+  constexpr int kPerBlock = kScreenThreads / kScreenLanes;
+  for (int kb = blockIdx.x * kPerBlock; kb < n; kb += gridDim.x * kPerBlock)
+    screen_block(kb, n, tile, cp, node_pos, node_live, node_live_f, rmax_bits, node_dq, sp, cki,
+                 ckw, ok, res_out, low, comp, grid, use_grid);
 }
 
 __global__ void k_append(const int* __restrict__ ok, const int* __restrict__ scan,
@@ -720,7 +735,8 @@ void screen_candidates_async(Ctx& c) {
     grid = c.screen_grid &&
            build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
   }
-  DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02, cdiv((long long)c.P * kScreenLanes, kScreenThreads),
+  DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02,
+            std::min(cdiv((long long)c.P * kScreenLanes, kScreenThreads), 2 * c.num_sms),
             kScreenThreads, 0, k_screen, c.cand_p,
             &c.dsc->n_cand, c.node_pos, c.node_live, c.node_live_f, &c.dsc->rmax_bits, c.node_dq,
             screen_params(c), c.cand_ki,

@@ -279,6 +279,7 @@ void allocate(Ctx& c) {
     g->key = dalloc<long long>(c, slots);
     g->range = dalloc<int2>(c, slots);
     g->ids = dalloc<int>(c, std::min(c.N_cap, kKnnMaxPoints));
+    g->cpos = dalloc<double4>(c, std::min(c.N_cap, kKnnMaxPoints));
     g->prm = dalloc<double>(c, 8);
     g->pslot = dalloc<int>(c, std::min(c.N_cap, kKnnMaxPoints));
     g->fill = dalloc<int>(c, slots);

@@ -115,6 +115,7 @@ struct KnnGrid {
   long long* key = nullptr;
   int2* range = nullptr;
   int* ids = nullptr;
+  double4* cpos = nullptr;  // the points' positions in cell order (copy of pos[ids[k]])
   double* prm = nullptr;
   int* pslot = nullptr;  // build scratch: slot of every point
   int* fill = nullptr;   // build scratch: per-slot scatter counters

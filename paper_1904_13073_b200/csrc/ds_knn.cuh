@@ -24,6 +24,7 @@ struct KnnGridView {
   const long long* key;  // slot -> packed cell key, kKnnEmpty if free
   const int2* range;     // slot -> (start, count) into ids
   const int* ids;        // point ids sorted by cell
+  const double4* cpos;   // their positions, same order
   const double* prm;     // lo.x, lo.y, lo.z, h, 1/h
   int mask;              // slots - 1
   int max_ring;          // shells walked before giving up (then brute force)
@@ -34,10 +35,17 @@ inline KnnGridView knn_view(const KnnGrid& g, int max_ring) {
   v.key = g.key;
   v.range = g.range;
   v.ids = g.ids;
+  v.cpos = g.cpos;
   v.prm = g.prm;
   v.mask = g.mask;
   v.max_ring = max_ring;
   return v;
+}
+
+__device__ __forceinline__ double4 ldg_d4(const double4* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
 }
 
 __device__ __forceinline__ long long knn_pack(int cx, int cy, int cz) {
@@ -177,8 +185,8 @@ __device__ bool knn_grid_query(const KnnGridView& g, const double4* __restrict__
       const int2 rg = knn_find(g, knn_pack(cx + dx, cy + dy, cz + dz));
       for (int k = rg.x; k < rg.x + rg.y; ++k) {
         const int id = __ldg(g.ids + k);
+        const double4 p = ldg_d4(g.cpos + k);  // independent of the id load
         if (!keep(id)) continue;
-        const double4 p = pos[id];
         knnk_insert<K>(sqn(sub(v3(p.x, p.y, p.z), x)), id, bd, bi);
       }
     }

@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(kBuildThreads) k_knn_build(const double4* __re
   // scatter ids by cell (order within a cell is irrelevant: queries rank by (d2, id))
   for (int i = tid; i < n; i += kBuildThreads) {
     const int s = pslot[i];
-    g.ids[g.range[s].x + atomicAdd(fill + s, 1)] = i;
+    const int k = g.range[s].x + atomicAdd(fill + s, 1);
+    g.ids[k] = i;
+    g.cpos[k] = pos[i];
   }
 }
 

@@ -608,8 +608,7 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
   // streaming top-K over the new nodes (oracle loop, warp_field.cpp:186-236);
   // the final slots are the (d2, index) top K of old + new, independent of the
   // order the candidates arrive in
-  auto consider = [&](int j) {
-    const double4 q = pos[j];
+  auto consider = [&](int j, const double4 q) {
     const double d2 = sqn(sub(v3(q.x, q.y, q.z), p));
     int slot;
     double ld = sd[0];  // worst slot (count - 1) without a dynamic index
@@ -654,13 +653,14 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
         for (int cy = y0; cy <= y1; ++cy)
           for (int cx = x0; cx <= x1; ++cx) {
             const int2 rg = knn_find(gnew, knn_pack(cx, cy, cz));
-            for (int k = rg.x; k < rg.x + rg.y; ++k) consider(first + __ldg(gnew.ids + k));
+            for (int k = rg.x; k < rg.x + rg.y; ++k)
+              consider(first + __ldg(gnew.ids + k), ldg_d4(gnew.cpos + k));
           }
       done = true;
     }
   }
   if (!done)
-    for (int j = first; j < N; ++j) consider(j);
+    for (int j = first; j < N; ++j) consider(j, pos[j]);
   if (!changed) return;
   int o[4];
   float w[4];

@@ -310,6 +310,8 @@ void allocate(Ctx& c) {
   if (const char* e = std::getenv("DS_INCR_GRID_MIN")) c.incr_grid_min = std::atoi(e);
   if (const char* e = std::getenv("DS_NO_PDL")) c.use_pdl = e[0] == '0';
   if (const char* e = std::getenv("DS_INCR_CELL")) c.incr_cell = std::atof(e);
+  if (const char* e = std::getenv("DS_LIVE_CELL")) c.live_cell = std::atof(e);
+  if (const char* e = std::getenv("DS_REF_CELL")) c.ref_cell = std::atof(e);
   if (const char* e = std::getenv("DS_PCG_SMEM")) c.pcg_smem_cap = std::min(std::atoi(e), c.pcg_smem_cap);
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));
   DS_CUDA(cudaMemsetAsync(c.node_nbr, 0xff, sizeof(int) * 8 * N, c.stream));

@@ -266,6 +266,8 @@ struct Ctx {
   bool use_pdl = true;          // programmatic dependent launch in the GN chain (DS_NO_PDL=1 disables)
   int incr_grid_min = 16;       // new nodes above which grid_new is used (DS_INCR_GRID_MIN)
   double incr_cell = 4.0;       // grid_new cell size in node_sigma (DS_INCR_CELL)
+  double live_cell = 2.0;       // grid_live (screening) cell size in node_sigma (DS_LIVE_CELL)
+  double ref_cell = 2.0;        // grid_ref (edges, seeds, skinning) cell size (DS_REF_CELL)
   long long* ht_key = nullptr;
   int* ht_cnt = nullptr;
   int* ht_ids = nullptr;

@@ -183,11 +183,20 @@ __device__ bool knn_grid_query(const KnnGridView& g, const double4* __restrict__
         if ((ex * ex + ey * ey + ez * ez) * (1.0 - 1e-9) > bound) continue;
       }
       const int2 rg = knn_find(g, knn_pack(cx + dx, cy + dy, cz + dz));
-      for (int k = rg.x; k < rg.x + rg.y; ++k) {
-        const int id = __ldg(g.ids + k);
-        const double4 p = ldg_d4(g.cpos + k);  // independent of the id load
-        if (!keep(id)) continue;
-        knnk_insert<K>(sqn(sub(v3(p.x, p.y, p.z), x)), id, bd, bi);
+      // points four at a time: their (id, position) loads are in flight together
+      for (int k0 = rg.x; k0 < rg.x + rg.y; k0 += 4) {
+        int id[4];
+        double4 p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (k0 + u < rg.x + rg.y) {
+            id[u] = __ldg(g.ids + k0 + u);
+            p[u] = ldg_d4(g.cpos + k0 + u);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (k0 + u < rg.x + rg.y && keep(id[u]))
+            knnk_insert<K>(sqn(sub(v3(p[u].x, p[u].y, p[u].z), x)), id[u], bd, bi);
       }
     }
     knnk_merged<K, LANES>(bd, bi, md, mi);

@@ -711,7 +711,7 @@ void prepare_live_nodes_async(Ctx& c) {
   try {
     node_live_positions(c);
     c.live_grid = c.screen_grid &&
-                  build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
+                  build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, c.live_cell * c.cfg.node_sigma);
   } catch (...) {
     c.stream = main_stream;
     throw;
@@ -733,7 +733,7 @@ void screen_candidates_async(Ctx& c) {
   } else {
     node_live_positions(c);
     grid = c.screen_grid &&
-           build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, 2.0 * c.cfg.node_sigma);
+           build_knn_grid(c, c.grid_live, c.node_live, c.n_nodes, c.live_cell * c.cfg.node_sigma);
   }
   DS_LAUNCH(c, KK_SKIN_APPEND, 64.0 * c.P * 0.02,
             std::min(cdiv((long long)c.P * kScreenLanes, kScreenThreads), 2 * c.num_sms),

@@ -745,7 +745,7 @@ int greedy(Ctx& c, const float4* cand, int M, int n0, int list_mode) {
 
 // grid over the reference node positions, cell 2 sigma (nodes are >= sigma apart)
 bool build_ref_grid(Ctx& c) {
-  return build_knn_grid(c, c.grid_ref, c.node_pos, c.n_nodes, 2.0 * c.cfg.node_sigma);
+  return build_knn_grid(c, c.grid_ref, c.node_pos, c.n_nodes, c.ref_cell * c.cfg.node_sigma);
 }
 
 // Node edges stay a brute-force warp-per-node scan up to the grid capacity: at

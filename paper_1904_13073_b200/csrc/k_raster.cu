@@ -29,6 +29,16 @@ struct CamParams {
   int W, H;
 };
 
+#ifndef DS_SPLAT_LANES1
+#define DS_SPLAT_LANES1 1
+#endif
+#ifndef DS_SPLAT_LANES2
+#define DS_SPLAT_LANES2 4
+#endif
+// lanes per surfel in the solve-loop splats: pass 1 (with the fp64 warp, done
+// redundantly per lane) and pass 2 (depth-test loads, the latency-bound one)
+constexpr int kSplatLanes1 = DS_SPLAT_LANES1, kSplatLanes2 = DS_SPLAT_LANES2;
+
 struct SplatParams {
   CamParams cam;
   int t_now, delta_recent, host_bootstrap;
@@ -48,7 +58,7 @@ __global__ void k_any_stable(const float4* __restrict__ ln, int n, double delta_
 // kWarp (pass 1 over a list): the surfel is first forward-warped
 // (warp_field.cpp:128-140, as k_forward_warp) and its live state written,
 // so the solve loop's warp + first splat pass are one launch.
-template <bool kPass2, bool kWarp = false>
+template <bool kPass2, bool kWarp = false, int kL = 1>
 __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const int* __restrict__ list,
                                                      SplatParams sp,
                                                      const int* __restrict__ any_stable,
@@ -57,7 +67,10 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
                                                      int* sidx,
                                                      const double4* __restrict__ warp_dq = nullptr) {
   pdl_wait();  // programmatic dependent launch: predecessor results visible
-  const int k0 = blockIdx.x * blockDim.x + threadIdx.x;
+  // kL lanes per surfel: each computes the surfel's projection (bit-identical
+  // in every lane) and takes every kL-th pixel of its splat disk
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k0 = gt / kL, lane = gt % kL;
   if (k0 >= n) return;
   const int i = list ? list[k0] : k0;
   float4 lp, ln;
@@ -73,8 +86,10 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
       lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
       ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
     }
-    m.lp[i] = lp;
-    m.ln[i] = ln;
+    if (lane == 0) {
+      m.lp[i] = lp;
+      m.ln[i] = ln;
+    }
   } else {
     lp = m.lp[i];
     ln = m.ln[i];
@@ -97,7 +112,7 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
   const bool sane = fabs(u) < 1e9 && fabs(v) < 1e9;
   const int ccx = sane ? (int)llround(u) : -1, ccy = sane ? (int)llround(v) : -1;
   const bool cin = ccx >= 0 && ccx < k.W && ccy >= 0 && ccy < k.H;
-  if (cin) {
+  if (cin && lane == 0) {
     const size_t c = (size_t)ccy * k.W + ccx;
     if (!kPass2) zmin(pkey + c, zb);
     else if (pkey[c] == zb) imin(pidx + c, i);
@@ -107,36 +122,38 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
   if (sane && rpx < 1e6) {
     const int y0 = max((int)ceil(v - rpx), 0), y1 = min((int)floor(v + rpx), k.H - 1);
     const int x0 = max((int)ceil(u - rpx), 0), x1 = min((int)floor(u + rpx), k.W - 1);
-    if (!kPass2) {
-      for (int y = y0; y <= y1; ++y)
-        for (int x = x0; x <= x1; ++x) {
+    if (y1 >= y0 && x1 >= x0) {
+      const int bw = x1 - x0 + 1, total = bw * (y1 - y0 + 1);
+      if (!kPass2) {
+        for (int idx = lane; idx < total; idx += kL) {
+          const int y = y0 + idx / bw, x = x0 + idx % bw;
           const double dx = x - u, dy = y - v;
           if (dx * dx + dy * dy <= r2) zmin(skey + (size_t)y * k.W + x, zb);
         }
-    } else if (y1 >= y0 && x1 >= x0) {
-      // pass 2 must read the stored depth before its RED: four disk pixels'
-      // loads are issued together instead of one blocking load per pixel
-      const int bw = x1 - x0 + 1, total = bw * (y1 - y0 + 1);
-      for (int base = 0; base < total; base += 4) {
-        unsigned long long kv[4];
-        size_t cc[4];
-        bool in[4];
+      } else {
+        // pass 2 must read the stored depth before its RED: four disk pixels'
+        // loads per lane are issued together instead of one blocking load each
+        for (int base = 0; base < total; base += 4 * kL) {
+          unsigned long long kv[4];
+          size_t cc[4];
+          bool in[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int idx = base + q;
-          const int y = y0 + idx / bw, x = x0 + idx % bw;
-          const double dx = x - u, dy = y - v;
-          in[q] = idx < total && dx * dx + dy * dy <= r2;
-          cc[q] = (size_t)y * k.W + x;
-          kv[q] = in[q] ? skey[cc[q]] : 0ull;
+          for (int q = 0; q < 4; ++q) {
+            const int idx = base + q * kL + lane;
+            const int y = y0 + idx / bw, x = x0 + idx % bw;
+            const double dx = x - u, dy = y - v;
+            in[q] = idx < total && dx * dx + dy * dy <= r2;
+            cc[q] = (size_t)y * k.W + x;
+            kv[q] = in[q] ? skey[cc[q]] : 0ull;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (in[q] && kv[q] == zb) imin(sidx + cc[q], i);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (in[q] && kv[q] == zb) imin(sidx + cc[q], i);
       }
     }
   }
-  if (cin) {  // sub-pixel splats keep their own pixel (raster.cpp:101)
+  if (cin && lane == 0) {  // sub-pixel splats keep their own pixel (raster.cpp:101)
     const size_t c = (size_t)ccy * k.W + ccx;
     if (!kPass2) zmin(skey + c, zb);
     else if (skey[c] == zb) imin(sidx + c, i);
@@ -282,17 +299,21 @@ void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
   sp.delta_stable = c.cfg.delta_stable;
   sp.host_bootstrap = (t_now - t_last <= c.cfg.delta_recent) ? 1 : 0;
   if (n > 0) {
-    auto k_warp_splat = k_model_splat<false, true>;
+    // several lanes per listed surfel (the solve loop's short lists)
+    auto k_warp_splat = k_model_splat<false, true, kSplatLanes1>;
+    auto k_pass1 = k_model_splat<false, false, kSplatLanes1>;
+    auto k_pass2 = k_model_splat<true, false, kSplatLanes2>;
+    const int nb = cdiv((long long)n * kSplatLanes1, 256), nb2 = cdiv((long long)n * kSplatLanes2, 256);
     if (warp_dq)  // warp (96 B) + pass 1 (36 B) per listed surfel
-      DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 132.0 * n, cdiv(n, 256), 256, 0, k_warp_splat, c.M(), n,
-                list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx, warp_dq);
+      DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 132.0 * n, nb, 256, 0, k_warp_splat, c.M(), n, list, sp,
+                    &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx, warp_dq);
     else
-      DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(),
-                n, list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
-                (const double4*)nullptr);
-    DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 36.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
-              list, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
-              (const double4*)nullptr);
+      DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 36.0 * n, nb, 256, 0, k_pass1, c.M(), n, list, sp,
+                    &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
+                    (const double4*)nullptr);
+    DS_LAUNCH_PDL(c, KK_MODEL_MAP_SPLAT, 36.0 * n, nb2, 256, 0, k_pass2, c.M(), n, list, sp,
+                  &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
+                  (const double4*)nullptr);
   }
   if (resolve) {
     AssocParams ap;

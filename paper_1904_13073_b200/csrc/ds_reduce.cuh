@@ -47,6 +47,51 @@ __device__ __forceinline__ void grid_sum_part(double v, double* __restrict__ par
   }
 }
 
+// Barrier-free variant: each warp reduces (xor butterfly) and publishes its
+// sum; the last warp of the block to arrive adds the warp sums in warp order,
+// the last block adds the block partials in block order (one warp). Warps may
+// exit right after the call, so idle warps do not wait for the busy ones.
+// Requires *wcnt == 0 on entry, made visible by a __syncthreads before the call
+// (the caller zeroes it at kernel start); every warp of the block calls it once.
+template <int kBlock>
+__device__ __forceinline__ void grid_sum_warps(double v, unsigned* wcnt, double* wsum,
+                                               double* __restrict__ part,
+                                               unsigned* __restrict__ ticket,
+                                               double* __restrict__ out, int bid, int nblocks) {
+  constexpr int kWarps = kBlock / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  int lastw = 0;
+  if (lane == 0) {
+    wsum[w] = v;
+    __threadfence_block();
+    lastw = atomicAdd(wcnt, 1u) == (unsigned)kWarps - 1;
+  }
+  if (!__shfl_sync(0xffffffffu, lastw, 0)) return;
+  int lastb = 0;
+  if (lane == 0) {
+    __threadfence_block();
+    const volatile double* ws = wsum;
+    double b = 0.0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) b += ws[i];
+    part[bid] = b;
+    __threadfence();
+    lastb = atomicAdd(ticket, 1u) == (unsigned)nblocks - 1;
+  }
+  if (!__shfl_sync(0xffffffffu, lastb, 0)) return;
+  __threadfence();
+  double acc = 0.0;
+  for (int b = lane; b < nblocks; b += 32) acc += __ldcg(part + b);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    *out = acc;
+    *ticket = 0u;
+  }
+}
+
 template <int kBlock>
 __device__ __forceinline__ void grid_sum(double v, double* __restrict__ part,
                                          unsigned* __restrict__ ticket, double* __restrict__ out) {

@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(256, 3) k_assoc_pair_terms(
   pdl_wait();  // programmatic dependent launch: predecessor results visible
   __shared__ int s_pix[256], s_srf[256];
   __shared__ int s_wcnt[8];
+  __shared__ unsigned s_done;
+  __shared__ double s_wsum[8];
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x == 0) s_done = 0u;  // visible after the packing barriers below
   int ps = -1;
   if (c < pp.P) {
     // resolve (raster.cpp:104-119), then reset the consumed z-buffer entries
@@ -230,7 +233,8 @@ __global__ void __launch_bounds__(256, 3) k_assoc_pair_terms(
   const int sc = threadIdx.x < tot ? s_srf[threadIdx.x] : -1;
   const double e = pair_term_one(pc, sc, m, node_dq, fvert, fnrm, pp, pair_ok, rows, pair_r, s_cnt,
                                  s_head);
-  grid_sum<256>(e, part, ticket, out);  // data energy, fixed order
+  // data energy, fixed order; warps past the packed pairs finish at once
+  grid_sum_warps<256>(e, &s_done, s_wsum, part, ticket, out, blockIdx.x, gridDim.x);
 }
 
 // E_data at arbitrary node transforms over the fixed pair set (solver.cpp:132-143);
@@ -316,6 +320,9 @@ __global__ void __launch_bounds__(256) k_energy(const int* __restrict__ pair_s, 
                                                 double* __restrict__ e_data,
                                                 double* __restrict__ e_reg) {
   pdl_wait();  // programmatic dependent launch: predecessor results visible
+  __shared__ unsigned s_done;
+  __shared__ double s_wsum[8];
+  if (threadIdx.x == 0) s_done = 0u;  // visible after the next barrier
   if ((int)blockIdx.x < nbp) {
     __shared__ int s_list[256];
     __shared__ int s_wcnt[8];
@@ -335,8 +342,9 @@ __global__ void __launch_bounds__(256) k_energy(const int* __restrict__ pair_s, 
         e = r * r;
       }
     }
-    grid_sum_part<256>(e, part, tickets + 0, e_data, blockIdx.x, nbp);
+    grid_sum_warps<256>(e, &s_done, s_wsum, part, tickets + 0, e_data, blockIdx.x, nbp);
   } else {
+    __syncthreads();
     const int bid = blockIdx.x - nbp, nbe = gridDim.x - nbp;
     const int e = bid * blockDim.x + threadIdx.x;
     double v = 0.0;
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(256) k_energy(const int* __restrict__ pair_s, 
         v = sqn(sub(rig_apply(Tj, p), rig_apply(Ti, p)));
       }
     }
-    grid_sum_part<256>(v, part + nbp, tickets + 1, e_reg, bid, nbe);
+    grid_sum_warps<256>(v, &s_done, s_wsum, part + nbp, tickets + 1, e_reg, bid, nbe);
   }
 }
 

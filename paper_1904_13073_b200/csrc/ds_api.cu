@@ -425,8 +425,13 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   if (c.n_nodes > 0 && c.n_surfels > 0) {
     cudaStream_t main_stream = c.stream;
     c.stream = c.side;
+    const auto tp0 = std::chrono::steady_clock::now();
     try {
       build_pattern(c, t_now, c.t_last_reinit);
+      if (c.trace_host)
+        std::fprintf(stderr, "build_pattern (side, host) %.1f us\n",
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tp0)
+                         .count());
     } catch (...) {
       c.stream = main_stream;
       throw;

@@ -1869,7 +1869,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
     DS_LAUNCH_PDL(c, KK_BLOCK_ASSEMBLY, bytes, cdiv((long long)c.n_chunks * kChunkLanes, 256), 256, 0,
               k_assemble_chunks, A);
     if (c.n_multi > 0)
-      DS_LAUNCH_PDL(c, KK_BLOCK_ASSEMBLY, 0.0, cdiv((long long)c.n_multi * kFinishEntries, 256), 256, 0,
+      DS_LAUNCH_PDL(c, KK_REDUCE, 0.0, cdiv((long long)c.n_multi * kFinishEntries, 256), 256, 0,
                 k_assemble_finish, A, c.multi_list, c.multi_scan + c.n_up);
   }
   DS_LAUNCH_PDL(c, KK_REDUCE, 48.0 * N + 24.0 * N, std::max(1, cdiv(N, kStatsThreads)), kStatsThreads, 0,

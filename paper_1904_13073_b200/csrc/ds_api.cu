@@ -226,6 +226,8 @@ void allocate(Ctx& c) {
   c.multi_scan = dalloc<int>(c, c.UB_cap + 1);
   c.multi_list = dalloc<int>(c, c.UB_cap + 1);
   c.chunk_ub = dalloc<int>(c, c.CH_cap);
+  c.chunk_d0 = dalloc<int4>(c, c.CH_cap);
+  c.chunk_d1 = dalloc<int4>(c, c.CH_cap);
   c.part_h = dalloc<float>(c, (size_t)c.CH_cap * 36);
   c.part_g = dalloc<double>(c, (size_t)c.CH_cap * 6);
   c.part_t = dalloc<int>(c, c.CH_cap);

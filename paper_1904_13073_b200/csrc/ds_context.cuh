@@ -206,6 +206,8 @@ struct Ctx {
   int* diag_pos = nullptr;
   int* chunk_first = nullptr;  // per upper block: first assembly chunk (n_up + 1)
   int* chunk_ub = nullptr;     // per chunk: upper block
+  int4* chunk_d0 = nullptr;    // per chunk: assembly descriptor (k_chunk_fill)
+  int4* chunk_d1 = nullptr;
   float* part_h = nullptr;     // per chunk: 6x6 partial
   double* part_g = nullptr;    // per chunk: g partial
   int* part_t = nullptr;       // per chunk: touched

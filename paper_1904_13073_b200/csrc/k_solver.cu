@@ -651,6 +651,8 @@ struct AsmArgs {
   const int* up_mpos;
   const int* chunk_ub;
   const int* chunk_first;
+  const int4* chunk_d0;  // per chunk: (record range, BSR position, mirror position)
+  const int4* chunk_d1;  // per chunk: (diagonal g row, regulariser block, single-chunk)
   const int* rec_val;
   const int* s_cnt;
   const int* s_head;   // lowest pixel of the surfel's pairs
@@ -813,16 +815,13 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
 #pragma unroll
   for (int t = 0; t < 6; ++t) gg[t] = 0.0;
   int touched = 0;
-  int ub = 0, key = 0, c0 = 0, c1 = 0;
+  int4 d0 = make_int4(0, 0, 0, -1), d1 = make_int4(-1, -1, 0, 0);
   bool diag = false;
   if (valid) {
-    ub = A.chunk_ub[chunk];
-    key = A.up_key[ub];
-    diag = (key / A.N) == (key % A.N);
-    c0 = A.chunk_first[ub];
-    c1 = A.chunk_first[ub + 1];
-    const int r0 = A.up_start[ub] + (chunk - c0) * kChunk;
-    const int r1 = min(r0 + kChunk, A.up_start[ub + 1]);
+    d0 = A.chunk_d0[chunk];
+    d1 = A.chunk_d1[chunk];
+    diag = d1.x >= 0;
+    const int r0 = d0.x, r1 = d0.y;
     // Three-stage software pipeline over steps of two records (lane l takes
     // records l, l+8, l+16, ... in order): while step s's Jacobian rows are
     // loaded and accumulated, step s+1's (count, head) and step s+2's record
@@ -882,28 +881,69 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
       vB1 = vC1;
     }
   }
-  // fixed butterfly over the 8 lanes of the group
+  // fixed reduce-scatter over the 8 lanes of the group: three halving rounds
+  // (xor 4, 2, 1); afterwards lane l holds the sums of entries t = l (mod 8)
+  static_assert(kChunkLanes == 8, "reduce-scatter is written for 8-lane groups");
+  float r1[20];
 #pragma unroll
-  for (int off = kChunkLanes / 2; off > 0; off >>= 1) {
+  for (int q = 0; q < 5; ++q)
 #pragma unroll
-    for (int t = 0; t < 36; ++t) h[t] += __shfl_xor_sync(0xffffffffu, h[t], off);
+    for (int j = 0; j < 4; ++j) {
+      const float a = q * 8 + j < 36 ? h[q * 8 + j] : 0.f;
+      const float b = q * 8 + j + 4 < 36 ? h[q * 8 + j + 4] : 0.f;
+      const bool hi = l & 4;
+      r1[q * 4 + j] = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 4);
+    }
+  float r2[10];
 #pragma unroll
-    for (int t = 0; t < 6; ++t) gg[t] += __shfl_xor_sync(0xffffffffu, gg[t], off);
-    touched |= __shfl_xor_sync(0xffffffffu, touched, off);
+  for (int q = 0; q < 5; ++q)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float a = r1[q * 4 + j], b = r1[q * 4 + j + 2];
+      const bool hi = l & 2;
+      r2[q * 2 + j] = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 2);
+    }
+  float hs[5];  // hs[q] = entry 8 q + l
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const float a = r2[q * 2], b = r2[q * 2 + 1];
+    const bool hi = l & 1;
+    hs[q] = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 1);
   }
+  double g1[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double a = gg[j], b = j + 4 < 6 ? gg[j + 4] : 0.0;
+    const bool hi = l & 4;
+    g1[j] = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 4);
+  }
+  double g2[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double a = g1[j], b = g1[j + 2];
+    const bool hi = l & 2;
+    g2[j] = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 2);
+  }
+  double gs;  // entry l of g (lanes 0..5)
+  {
+    const double a = g2[0], b = g2[1];
+    const bool hi = l & 1;
+    gs = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 1);
+  }
+#pragma unroll
+  for (int off = 4; off > 0; off >>= 1) touched |= __shfl_xor_sync(0xffffffffu, touched, off);
   if (!valid) return;
-  if (c1 - c0 == 1) {
+  if (d1.z) {
     // single-chunk block (most off-diagonal ones): the partial plus the
     // block's regulariser sum is final; the lanes write it straight into the
     // BSR (both triangles) and g
-    const int pu = A.up_pos[ub];
-    const int pm = diag ? -1 : A.up_mpos[ub];
-    const int rb = A.ub_reg[ub];
+    const int pu = d0.z, pm = d0.w, rb = d1.y;
     if (rb >= 0) touched = 1;
 #pragma unroll
-    for (int t = 0; t < 36; ++t) {
-      if (t % kChunkLanes != l) continue;
-      const float v = rb >= 0 ? (float)((double)h[t] + __ldg(A.reg_h + (size_t)rb * 36 + t)) : h[t];
+    for (int q = 0; q < 5; ++q) {
+      const int t = 8 * q + l;
+      if (t >= 36) continue;
+      const float v = rb >= 0 ? (float)((double)hs[q] + __ldg(A.reg_h + (size_t)rb * 36 + t)) : hs[q];
       A.bsr_val[(size_t)pu * 36 + t] = v;
       if (pm >= 0) A.bsr_val[(size_t)pm * 36 + (t % 6) * 6 + t / 6] = v;
     }
@@ -911,22 +951,15 @@ __global__ void __launch_bounds__(256, 2) k_assemble_chunks(AsmArgs A) {
       A.bsr_touch[pu] = touched ? 1 : 0;
       if (pm >= 0) A.bsr_touch[pm] = touched ? 1 : 0;
     }
-    if (diag) {
-      const int row = key / A.N;
-#pragma unroll
-      for (int x = 0; x < 6; ++x)
-        if (x == l) A.g[6 * row + x] = rb >= 0 ? gg[x] + __ldg(A.reg_g + (size_t)rb * 6 + x) : gg[x];
-    }
+    if (diag && l < 6)
+      A.g[6 * d1.x + l] = rb >= 0 ? gs + __ldg(A.reg_g + (size_t)rb * 6 + l) : gs;
     return;
   }
-  // multi-chunk block: lanes write the partial (float4 per lane pair)
-  float4* ph = reinterpret_cast<float4*>(A.part_h + (size_t)chunk * 36);
+  // multi-chunk block: the lanes write the partial
 #pragma unroll
-  for (int t = 0; t < 9; ++t)
-    if (t % kChunkLanes == l) ph[t] = make_float4(h[4 * t], h[4 * t + 1], h[4 * t + 2], h[4 * t + 3]);
-#pragma unroll
-  for (int x = 0; x < 6; ++x)
-    if (x == l) A.part_g[(size_t)chunk * 6 + x] = gg[x];
+  for (int q = 0; q < 5; ++q)
+    if (8 * q + l < 36) A.part_h[(size_t)chunk * 36 + 8 * q + l] = hs[q];
+  if (l < 6) A.part_g[(size_t)chunk * 6 + l] = gs;
   if (l == 0) A.part_t[chunk] = touched;
 }
 
@@ -981,10 +1014,28 @@ __global__ void k_multi_list(const int* __restrict__ flag, const int* __restrict
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
   if (ub < n_up && flag[ub]) list[scan[ub]] = ub;
 }
-__global__ void k_chunk_fill(const int* __restrict__ first, int n_up, int* __restrict__ chunk_ub) {
+// per chunk: its upper block and a descriptor the assembly reads in one go:
+// d0 = (first record, end record, BSR position, mirrored position or -1),
+// d1 = (g row of a diagonal block or -1, regulariser block or -1, single-chunk)
+__global__ void k_chunk_fill(const int* __restrict__ first, int n_up, const int* __restrict__ up_key,
+                             const int* __restrict__ up_start, const int* __restrict__ up_pos,
+                             const int* __restrict__ up_mpos, const int* __restrict__ ub_reg, int N,
+                             int* __restrict__ chunk_ub, int4* __restrict__ d0,
+                             int4* __restrict__ d1) {
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
   if (ub >= n_up) return;
-  for (int c = first[ub]; c < first[ub + 1]; ++c) chunk_ub[c] = ub;
+  const int c0 = first[ub], c1 = first[ub + 1];
+  const int key = up_key[ub], row = key / N;
+  const bool diag = row == key % N;
+  const int pu = up_pos[ub], pm = diag ? -1 : up_mpos[ub];
+  const int s0 = up_start[ub], s1 = up_start[ub + 1];
+  const int rb = ub_reg[ub];
+  for (int c = c0; c < c1; ++c) {
+    chunk_ub[c] = ub;
+    const int r0 = s0 + (c - c0) * kChunk;
+    d0[c] = make_int4(r0, min(r0 + kChunk, s1), pu, pm);
+    d1[c] = make_int4(diag ? row : -1, rb, c1 - c0 == 1 ? 1 : 0, 0);
+  }
 }
 
 // ginf, |g|^2, tr(H) (solver.cpp:371, 378), thread per node; the last block
@@ -1757,8 +1808,9 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
     c.n_chunks = hc[0];
     c.n_multi = hc[1];
     if (c.n_chunks > c.CH_cap) fail(DS_ERR_CAPACITY, "assembly chunk capacity exceeded");
-    DS_LAUNCH(c, KK_PATTERN, 8.0 * c.n_chunks, cdiv(c.n_up, 256), 256, 0, k_chunk_fill,
-              c.chunk_first, c.n_up, c.chunk_ub);
+    DS_LAUNCH(c, KK_PATTERN, 40.0 * c.n_chunks, cdiv(c.n_up, 256), 256, 0, k_chunk_fill,
+              c.chunk_first, c.n_up, c.up_key, c.up_start, c.up_pos, c.up_mpos, c.ub_reg, N,
+              c.chunk_ub, c.chunk_d0, c.chunk_d1);
   }
   c.pattern_ready = true;
 }
@@ -1837,6 +1889,8 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   A.up_mpos = c.up_mpos;
   A.chunk_ub = c.chunk_ub;
   A.chunk_first = c.chunk_first;
+  A.chunk_d0 = c.chunk_d0;
+  A.chunk_d1 = c.chunk_d1;
   A.rec_val = c.rec_val;
   A.s_cnt = c.s_cnt;
   A.s_head = c.s_head;

@@ -251,7 +251,16 @@ __device__ int screen_one(V3 x, const double bd[4], const int bi[4],
   return 2;
 }
 
-// screen_one for an aligned 8-lane group (all lanes call it): the Eq. 6 entry
+// kScreenLanes lanes per candidate (>= 4: the compressive check's four
+// inverse warps run on lanes 0-3), each scanning a strided subset of the node
+// tiles / grid cells; the per-lane top-4 lists are merged by shuffles.
+#ifndef DS_SCREEN_LANES
+#define DS_SCREEN_LANES 4
+#endif
+constexpr int kScreenLanes = DS_SCREEN_LANES;
+static_assert(kScreenLanes >= 4 && (kScreenLanes & (kScreenLanes - 1)) == 0, "lanes: 4, 8, 16 or 32");
+
+// screen_one for an aligned kScreenLanes group (all lanes call it): the Eq. 6 entry
 // is built redundantly, the four inverse warps of the compressive check
 // (x and the three 1 mm probes, fusion.cpp:151-176) run on lanes 0-3 and
 // meet in lane 0 for the strain's sigma_max. Same arithmetic as screen_one.
@@ -261,7 +270,8 @@ __device__ int screen_group(V3 x, const double bd[4], const int bi[4],
                             const double4* __restrict__ node_dq, const ScreenParams& sp, int ids[4],
                             float ws[4], int& cnt, int lane_k) {
   (void)bd;
-  const unsigned gmask = 0xffu << ((threadIdx.x & 31) & ~7u);
+  const unsigned gmask = kScreenLanes >= 32 ? 0xffffffffu
+                        : ((1u << kScreenLanes) - 1u) << ((threadIdx.x & 31) & ~(unsigned)(kScreenLanes - 1));
   const int k = min(sp.K, sp.N);
   const int n0 = bi[0];
   const double4 l0 = node_live[n0], p0 = node_pos[n0];
@@ -298,7 +308,7 @@ __device__ int screen_group(V3 x, const double bd[4], const int bi[4],
   int oks = 1;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const int src = ((threadIdx.x & 31) & ~7) + a;
+    const int src = ((threadIdx.x & 31) & ~(kScreenLanes - 1)) + a;
     rx[a] = __shfl_sync(gmask, r.x, src);
     ry[a] = __shfl_sync(gmask, r.y, src);
     rz[a] = __shfl_sync(gmask, r.z, src);
@@ -318,9 +328,7 @@ __device__ int screen_group(V3 x, const double bd[4], const int bi[4],
   return strain_within(S, sp.eps) ? 2 : 1;
 }
 
-// kScreenLanes lanes per candidate, each scanning a strided subset of the
-// node tiles; the per-lane top-4 lists are merged by a shuffle butterfly.
-constexpr int kScreenLanes = 8;
+// (kScreenLanes: see above)
 constexpr int kScreenThreads = 256;
 
 // one block's group of kScreenThreads / kScreenLanes candidates from `kb`

@@ -1048,9 +1048,12 @@ __global__ void __launch_bounds__(kStatsThreads) k_g_stats(
     int N, int lm, double* __restrict__ part, unsigned* __restrict__ ticket,
     DevScalars* __restrict__ sc) {
   pdl_wait();  // programmatic dependent launch: predecessor results visible
-  __shared__ double smax[kStatsThreads], ssq[kStatsThreads], str[kStatsThreads];
-  __shared__ bool last;
+  constexpr int kWarps = kStatsThreads / 32;
+  __shared__ double wmax[kWarps], wsq[kWarps], wtr[kWarps];
+  __shared__ unsigned wdone;
   const int tid = threadIdx.x, j = blockIdx.x * kStatsThreads + tid;
+  const int lane = tid & 31, w = tid >> 5;
+  if (tid == 0) wdone = 0u;
   double mx = 0, sq = 0, tr = 0;
   if (j < N) {
 #pragma unroll
@@ -1066,35 +1069,56 @@ __global__ void __launch_bounds__(kStatsThreads) k_g_stats(
            (double)b[35];
     }
   }
-  smax[tid] = mx;
-  ssq[tid] = sq;
-  str[tid] = tr;
-  __syncthreads();
-  for (int k = kStatsThreads / 2; k > 0; k >>= 1) {
-    if (tid < k) {
-      smax[tid] = fmax(smax[tid], smax[tid + k]);
-      ssq[tid] += ssq[tid + k];
-      str[tid] += str[tid + k];
+  __syncthreads();  // wdone visible
+  // warp xor butterflies, then the last warp of the block combines in warp
+  // order and the last block combines the block partials (fixed orders)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    tr += __shfl_xor_sync(0xffffffffu, tr, off);
+  }
+  int lastw = 0;
+  if (lane == 0) {
+    wmax[w] = mx;
+    wsq[w] = sq;
+    wtr[w] = tr;
+    __threadfence_block();
+    lastw = atomicAdd(&wdone, 1u) == (unsigned)kWarps - 1;
+  }
+  if (!__shfl_sync(0xffffffffu, lastw, 0)) return;
+  int lastb = 0;
+  if (lane == 0) {
+    __threadfence_block();
+    const volatile double *vm = wmax, *vq = wsq, *vt = wtr;
+    double m = 0, q = 0, t = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) {
+      m = fmax(m, vm[i]);
+      q += vq[i];
+      t += vt[i];
     }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    part[3 * blockIdx.x + 0] = smax[0];
-    part[3 * blockIdx.x + 1] = ssq[0];
-    part[3 * blockIdx.x + 2] = str[0];
+    part[3 * blockIdx.x + 0] = m;
+    part[3 * blockIdx.x + 1] = q;
+    part[3 * blockIdx.x + 2] = t;
     __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    lastb = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
-  __syncthreads();
-  if (!last || tid != 0) return;
+  if (!__shfl_sync(0xffffffffu, lastb, 0)) return;
   __threadfence();
   double m = 0, q = 0, t = 0;
-#pragma unroll 8
-  for (int b = 0; b < (int)gridDim.x; ++b) {
+  for (int b = lane; b < (int)gridDim.x; b += 32) {
     m = fmax(m, __ldcg(part + 3 * b));
     q += __ldcg(part + 3 * b + 1);
     t += __ldcg(part + 3 * b + 2);
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    q += __shfl_xor_sync(0xffffffffu, q, off);
+    t += __shfl_xor_sync(0xffffffffu, t, off);
+  }
+  if (lane != 0) return;
   sc->ginf = m;
   sc->g_sq = q;  // |g|^2
   sc->htrace = t;

@@ -29,6 +29,8 @@ const char* kKernelNames[KK_COUNT] = {
 size_t sort_temp_bytes(int n);
 int pcg_max_grid(int num_sms);
 void build_pattern(Ctx& c, int t_now, int t_last);
+void build_pattern_enqueue(Ctx& c, int t_now, int t_last);
+void pattern_adopt(Ctx& c, bool have_scalars);
 double bsr_spmv(Ctx& c, const double* x_dev, double* y_dev, double mu, int reps);
 void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool lm_floor,
                         bool maps_clean = false);
@@ -429,7 +431,7 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
     c.stream = c.side;
     const auto tp0 = std::chrono::steady_clock::now();
     try {
-      build_pattern(c, t_now, c.t_last_reinit);
+      build_pattern_enqueue(c, t_now, c.t_last_reinit);
       if (c.trace_host)
         std::fprintf(stderr, "build_pattern (side, host) %.1f us\n",
                      std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tp0)
@@ -445,6 +447,7 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   }
   const auto tr0 = std::chrono::steady_clock::now();
   rigid_align_finish(c, c.pose, &st->rigid);
+  pattern_adopt(c, true);  // counts came with the rigid ICP's scalar fetch
   if (c.trace_host)
     std::fprintf(stderr, "pattern (side) built; rigid wait %.1f us\n",
                  std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tr0)

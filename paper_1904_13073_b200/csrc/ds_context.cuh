@@ -94,6 +94,9 @@ struct DevScalars {
   double lm_e_pre, lm_gnorm, lm_initial, lm_final;
   double new_bbox[6];  // bounding box of the nodes appended this frame
   double rigid_pose[12];
+  // JtJ pattern counts, published by its last kernel (read with the frame's
+  // next scalar fetch instead of host syncs inside the pattern build)
+  int pat_n_up, pat_n_full, pat_n_chunks, pat_n_multi, pat_err, _pad_pat[3];
 };
 
 enum DevErr { DERR_NODE_CAP = 1, DERR_HASH_CELL = 2, DERR_HASH_FULL = 4, DERR_BLOCK_CAP = 8 };
@@ -231,6 +234,7 @@ struct Ctx {
   int* multi_list = nullptr;
   double n_pairs_ok_est = 0;
   bool pattern_ready = false;
+  bool pattern_pending = false;  // enqueued, counts not adopted yet (pattern_adopt)
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
   // PCG

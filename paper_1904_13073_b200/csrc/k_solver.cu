@@ -565,9 +565,9 @@ __global__ void k_row_count(const int* __restrict__ up_key, const int* __restric
 }
 __global__ void k_row_fill(const int* __restrict__ up_key, const int* __restrict__ n_up_dev, int N,
                            const int* __restrict__ row_ptr, int* __restrict__ row_cur,
-                           int* __restrict__ col, int* __restrict__ tag) {
+                           int* __restrict__ col, int* __restrict__ tag, int ub_cap, int b_cap) {
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ub >= *n_up_dev) return;
+  if (ub >= min(*n_up_dev, ub_cap) || row_ptr[N] > b_cap) return;  // capacity: reported later
   const int k = up_key[ub];
   const int r = k / N, cc = k % N;
   int p = row_ptr[r] + atomicAdd(row_cur + r, 1);
@@ -584,10 +584,10 @@ __global__ void k_row_fill(const int* __restrict__ up_key, const int* __restrict
 // to their sorted slots; rows longer than 32 entries take the serial path.
 __global__ void k_row_sort(const int* __restrict__ row_ptr, int N, int* __restrict__ col,
                            int* __restrict__ tag, int* __restrict__ up_pos, int* __restrict__ up_mpos,
-                           int* __restrict__ diag_pos) {
+                           int* __restrict__ diag_pos, int b_cap) {
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (r >= N) return;  // warp-uniform
+  if (r >= N || row_ptr[N] > b_cap) return;  // warp-uniform
   const int a0 = row_ptr[r], a1 = row_ptr[r + 1], len = a1 - a0;
   if (len <= 32) {
     const int vc = lane < len ? col[a0 + lane] : 0x7fffffff;
@@ -1001,29 +1001,50 @@ __global__ void k_assemble_finish(AsmArgs A, const int* __restrict__ multi, cons
   }
 }
 
-__global__ void k_chunk_count(const int* __restrict__ up_start, int n_up, int* __restrict__ cnt,
-                              int* __restrict__ multi_flag) {
+// bound >= n_up entries: those past the device count get 0 (the scans run
+// over the host-known bound)
+__global__ void k_chunk_count(const int* __restrict__ up_start, const int* __restrict__ n_up_dev,
+                              int bound, int* __restrict__ cnt, int* __restrict__ multi_flag) {
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ub >= n_up) return;
+  if (ub >= bound) return;
+  if (ub >= *n_up_dev) {
+    cnt[ub] = 0;
+    multi_flag[ub] = 0;
+    return;
+  }
   const int k = (up_start[ub + 1] - up_start[ub] + kChunk - 1) / kChunk;
   cnt[ub] = k;
   multi_flag[ub] = k > 1 ? 1 : 0;
 }
-__global__ void k_multi_list(const int* __restrict__ flag, const int* __restrict__ scan, int n_up,
+__global__ void k_multi_list(const int* __restrict__ flag, const int* __restrict__ scan, int bound,
                              int* __restrict__ list) {
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ub < n_up && flag[ub]) list[scan[ub]] = ub;
+  if (ub < bound && flag[ub]) list[scan[ub]] = ub;
 }
 // per chunk: its upper block and a descriptor the assembly reads in one go:
 // d0 = (first record, end record, BSR position, mirrored position or -1),
 // d1 = (g row of a diagonal block or -1, regulariser block or -1, single-chunk)
-__global__ void k_chunk_fill(const int* __restrict__ first, int n_up, const int* __restrict__ up_key,
-                             const int* __restrict__ up_start, const int* __restrict__ up_pos,
-                             const int* __restrict__ up_mpos, const int* __restrict__ ub_reg, int N,
+// Thread 0 also publishes the pattern's counts (and capacity errors) into
+// DevScalars for the host, which reads them with the frame's next fetch.
+__global__ void k_chunk_fill(const int* __restrict__ first, const int* __restrict__ n_up_dev,
+                             const int* __restrict__ up_key, const int* __restrict__ up_start,
+                             const int* __restrict__ up_pos, const int* __restrict__ up_mpos,
+                             const int* __restrict__ ub_reg, int N, const int* __restrict__ row_ptr,
+                             const int* __restrict__ multi_scan, int ub_cap, int b_cap, int ch_cap,
+                             const int* __restrict__ err_in, DevScalars* __restrict__ sc,
                              int* __restrict__ chunk_ub, int4* __restrict__ d0,
                              int4* __restrict__ d1) {
   const int ub = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ub >= n_up) return;
+  const int n_up = *n_up_dev;
+  const bool over = n_up > ub_cap || row_ptr[N] > b_cap || (n_up <= ub_cap && first[n_up] > ch_cap);
+  if (ub == 0) {
+    sc->pat_n_up = n_up;
+    sc->pat_n_full = row_ptr[N];
+    sc->pat_n_chunks = n_up <= ub_cap ? first[n_up] : 0;
+    sc->pat_n_multi = n_up <= ub_cap ? multi_scan[n_up] : 0;
+    sc->pat_err = (over || (*err_in & DERR_BLOCK_CAP)) ? 1 : 0;
+  }
+  if (ub >= n_up || over) return;
   const int c0 = first[ub], c1 = first[ub + 1];
   const int key = up_key[ub], row = key / N;
   const bool diag = row == key % N;
@@ -1326,11 +1347,10 @@ __device__ __forceinline__ void apply_minv(const double* MINV, const double* v, 
 // CTA b of the PCG owns the block rows [r0, r1) whose BSR blocks are
 // [nnzb b / G, nnzb (b+1) / G) rounded to row starts; computed once per frame
 // (the pattern is fixed for the frame), thread per CTA.
-__global__ void k_pcg_slices(const int* __restrict__ row_ptr, int N, int nnzb, int G,
-                             int* __restrict__ out) {
+__global__ void k_pcg_slices(const int* __restrict__ row_ptr, int N, int G, int* __restrict__ out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= G) return;
-  const long long nz = nnzb;
+  const long long nz = row_ptr[N];
   const int t_lo = (int)(nz * b / G), t_hi = (int)(nz * (b + 1) / G);
   const int r0 = b == 0 ? 0 : min(lower_bound_dev(row_ptr, N + 1, t_lo), N);
   int r1 = b == G - 1 ? N : min(lower_bound_dev(row_ptr, N + 1, t_hi), N);
@@ -1720,7 +1740,7 @@ int none_key(int N) {
 // a CTA per SM; small systems use fewer CTAs
 int pcg_ctas(const Ctx& c) { return std::min(c.pcg_grid, std::max(1, cdiv(c.n_full, 64))); }
 
-void build_pattern(Ctx& c, int t_now, int t_last) {
+void build_pattern_enqueue(Ctx& c, int t_now, int t_last) {
   const int n_all = c.n_surfels, N = c.n_nodes;
   if ((long long)N * N >= 0x7fffffffLL) fail(DS_ERR_CAPACITY, "too many nodes for block keys");
   // eligible surfels (the only ones render_model_maps can pair this frame)
@@ -1777,15 +1797,10 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
             n_up_dev, N, c.row_cnt);
   scan_exclusive(c, c.row_cnt, c.row_ptr, N);
   DS_CUDA(cudaMemsetAsync(c.row_cnt, 0, sizeof(int) * (N + 1), c.stream));
-  int host[3] = {0, 0, 0};
-  DS_CUDA(cudaMemcpyAsync(&host[0], n_up_dev, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  DS_CUDA(cudaMemcpyAsync(&host[1], c.row_ptr + N, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  DS_CUDA(cudaMemcpyAsync(&host[2], &c.dsc->err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  sync(c);
-  if ((host[2] & DERR_BLOCK_CAP) || host[0] > c.UB_cap || host[1] > c.B_cap)
-    fail(DS_ERR_CAPACITY, "JtJ block capacity exceeded");
-  c.n_up = host[0];
-  c.n_full = host[1];
+  // No host sync from here on: kernels take the device counts and run over
+  // host-known bounds (ubb >= n_up); k_chunk_fill publishes the counts, which
+  // pattern_adopt reads (capacity errors included) before the solve uses them.
+  const int ubb = std::max(1, std::min(R, c.UB_cap));
   c.n_records = R;
   // regulariser records grouped by upper block (k_reg_blocks sums them per
   // GN iteration; the assembly adds the sums)
@@ -1799,44 +1814,50 @@ void build_pattern(Ctx& c, int t_now, int t_last) {
     DS_LAUNCH(c, KK_PATTERN, 12.0 * c.reg_cap_now, cdiv(c.reg_cap_now, 256), 256, 0, k_reg_bmark,
               c.reg_ub, c.rec_val2 + R, c.reg_cap_now, c.reg_bf);
     scan_exclusive(c, c.reg_bf, c.reg_bscan, c.reg_cap_now);
-    DS_CUDA(cudaMemsetAsync(c.ub_reg, 0xff, sizeof(int) * std::max(1, c.n_up), c.stream));
+    DS_CUDA(cudaMemsetAsync(c.ub_reg, 0xff, sizeof(int) * ubb, c.stream));
     DS_LAUNCH(c, KK_PATTERN, 16.0 * c.reg_cap_now, cdiv(c.reg_cap_now, 256), 256, 0, k_reg_bfill,
               c.reg_ub, c.reg_bf, c.reg_bscan, c.rec_val2 + R, c.reg_cap_now, c.reg_blk_start,
               c.ub_reg);
   }
-  if (c.n_up > 0) {
-    DS_LAUNCH(c, KK_PATTERN, 16.0 * c.n_up, cdiv(c.n_up, 256), 256, 0, k_row_fill, c.up_key,
-              n_up_dev, N, c.row_ptr, c.row_cnt, c.bsr_col, c.bsr_tag);
-  }
-  DS_LAUNCH(c, KK_PATTERN, 16.0 * c.n_full, cdiv((long long)N * 32, 256), 256, 0, k_row_sort, c.row_ptr, N,
-            c.bsr_col, c.bsr_tag, c.up_pos, c.up_mpos, c.diag_pos);
-  DS_LAUNCH(c, KK_PATTERN, 16.0 * pcg_ctas(c), cdiv(pcg_ctas(c), 128), 128, 0, k_pcg_slices,
-            c.row_ptr, N, c.n_full, pcg_ctas(c), c.pcg_slices);
+  DS_LAUNCH(c, KK_PATTERN, 16.0 * ubb, cdiv(ubb, 256), 256, 0, k_row_fill, c.up_key, n_up_dev, N,
+            c.row_ptr, c.row_cnt, c.bsr_col, c.bsr_tag, c.UB_cap, c.B_cap);
+  DS_LAUNCH(c, KK_PATTERN, 32.0 * ubb, cdiv((long long)N * 32, 256), 256, 0, k_row_sort, c.row_ptr, N,
+            c.bsr_col, c.bsr_tag, c.up_pos, c.up_mpos, c.diag_pos, c.B_cap);
   if (c.n_pairs_ok_est <= 0) c.n_pairs_ok_est = 0.4 * c.P;
   // fixed-size record chunks for the assembly (per frame)
-  c.n_chunks = 0;
-  c.n_multi = 0;
-  if (c.n_up > 0) {
-    DS_LAUNCH(c, KK_PATTERN, 12.0 * c.n_up, cdiv(c.n_up, 256), 256, 0, k_chunk_count, c.up_start,
-              c.n_up, c.chunk_first, c.multi_flag);
-    scan_exclusive(c, c.chunk_first, c.chunk_first, c.n_up);
-    scan_exclusive(c, c.multi_flag, c.multi_scan, c.n_up);
-    DS_LAUNCH(c, KK_PATTERN, 8.0 * c.n_up, cdiv(c.n_up, 256), 256, 0, k_multi_list, c.multi_flag,
-              c.multi_scan, c.n_up, c.multi_list);
-    int hc[2];
-    DS_CUDA(cudaMemcpyAsync(&hc[0], c.chunk_first + c.n_up, sizeof(int), cudaMemcpyDeviceToHost,
-                            c.stream));
-    DS_CUDA(cudaMemcpyAsync(&hc[1], c.multi_scan + c.n_up, sizeof(int), cudaMemcpyDeviceToHost,
-                            c.stream));
-    sync(c);
-    c.n_chunks = hc[0];
-    c.n_multi = hc[1];
-    if (c.n_chunks > c.CH_cap) fail(DS_ERR_CAPACITY, "assembly chunk capacity exceeded");
-    DS_LAUNCH(c, KK_PATTERN, 40.0 * c.n_chunks, cdiv(c.n_up, 256), 256, 0, k_chunk_fill,
-              c.chunk_first, c.n_up, c.up_key, c.up_start, c.up_pos, c.up_mpos, c.ub_reg, N,
-              c.chunk_ub, c.chunk_d0, c.chunk_d1);
-  }
+  DS_LAUNCH(c, KK_PATTERN, 12.0 * ubb, cdiv(ubb, 256), 256, 0, k_chunk_count, c.up_start, n_up_dev,
+            ubb, c.chunk_first, c.multi_flag);
+  scan_exclusive(c, c.chunk_first, c.chunk_first, ubb);
+  scan_exclusive(c, c.multi_flag, c.multi_scan, ubb);
+  DS_LAUNCH(c, KK_PATTERN, 8.0 * ubb, cdiv(ubb, 256), 256, 0, k_multi_list, c.multi_flag,
+            c.multi_scan, ubb, c.multi_list);
+  DS_LAUNCH(c, KK_PATTERN, 40.0 * ubb, cdiv(ubb, 256), 256, 0, k_chunk_fill, c.chunk_first, n_up_dev,
+            c.up_key, c.up_start, c.up_pos, c.up_mpos, c.ub_reg, N, c.row_ptr, c.multi_scan,
+            c.UB_cap, c.B_cap, c.CH_cap, &c.dsc->err, c.dsc, c.chunk_ub, c.chunk_d0, c.chunk_d1);
+  c.pattern_pending = true;
+}
+
+// Adopt the enqueued pattern's counts: from the scalars the caller already
+// fetched (have_scalars, e.g. the rigid ICP's fetch after the side branch
+// joined), else with a fetch here. Then the PCG slices for its grid.
+void pattern_adopt(Ctx& c, bool have_scalars) {
+  if (!c.pattern_pending) return;
+  if (!have_scalars) fetch_scalars(c);
+  c.pattern_pending = false;
+  const DevScalars& h = *c.hsc;
+  if (h.pat_err) fail(DS_ERR_CAPACITY, "JtJ block / assembly chunk capacity exceeded");
+  c.n_up = h.pat_n_up;
+  c.n_full = h.pat_n_full;
+  c.n_chunks = h.pat_n_chunks;
+  c.n_multi = h.pat_n_multi;
+  DS_LAUNCH(c, KK_PATTERN, 16.0 * pcg_ctas(c), cdiv(pcg_ctas(c), 128), 128, 0, k_pcg_slices,
+            c.row_ptr, c.n_nodes, pcg_ctas(c), c.pcg_slices);
   c.pattern_ready = true;
+}
+
+void build_pattern(Ctx& c, int t_now, int t_last) {
+  build_pattern_enqueue(c, t_now, t_last);
+  pattern_adopt(c, false);
 }
 
 namespace {

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
   __shared__ double sh[kThreads / 32][kTerms];
   __shared__ double tot[kTerms];
   __shared__ bool last;
+  pdl_wait();  // programmatic dependent launch: the previous iteration's pose
   if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
@@ -248,13 +249,19 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
     trace[1] = t_;
   }
   __threadfence();
+  // 8 threads per term (29 x 8 <= 256): each sums every 8th block partial,
+  // then an xor butterfly over the 8 (fixed order)
   const int nb = gridDim.x;
-  for (int term = wid; term < kTerms; term += kThreads / 32) {
-    double s = 0.0;
+  {
+    const int term = threadIdx.x >> 3, sub = threadIdx.x & 7;
+    double sacc = 0.0;
+    if (term < kTerms) {
 #pragma unroll 8
-    for (int b = lane; b < nb; b += 32) s += __ldcg(part + (size_t)term * nb + b);
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-    if (lane == 0) tot[term] = s;
+      for (int b = sub; b < nb; b += 8) sacc += __ldcg(part + (size_t)term * nb + b);
+    }
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
+    if (term < kTerms && sub == 0) tot[term] = sacc;
   }
   __syncthreads();
   if (trace && threadIdx.x == 0) {
@@ -328,7 +335,7 @@ void rigid_align_enqueue(Ctx& c, const double* render_pose, const double* init_p
     const int samples = rp.sw * rp.sh;
     const int nb = std::min(cdiv(samples, kThreads), 2 * c.num_sms);  // grid-stride
     for (int it = 0; it < kIters[level]; ++it) {
-      DS_LAUNCH(c, KK_RIGID, 100.0 * samples + 16.0 * kTerms * nb, nb, kThreads, 0, k_rigid_terms,
+      DS_LAUNCH_PDL(c, KK_RIGID, 100.0 * samples + 16.0 * kTerms * nb, nb, kThreads, 0, k_rigid_terms,
                 rp, c.d_pose, c.mm_idx, c.M(), c.f_vert, c.f_nrm, c.f_flag, c.red_part,
                 c.tickets + 3, level, c.d_pose, c.dsc, c.pcg_trace ? c.pcg_trace + 32 : nullptr);
     }

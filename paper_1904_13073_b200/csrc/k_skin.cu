@@ -126,9 +126,12 @@ constexpr int kListNodes = 1024;  // extension: new nodes kept in shared memory
 // accepted nodes. list_mode = 1 (extension, after k_uncovered removed every
 // candidate covered by a pre-existing node): only the nodes accepted by this
 // launch can cover a candidate; they are tested from shared memory.
+// M_dev != nullptr: the candidate count is read from the device (no host
+// round trip between the pre-filter's compaction and the greedy pass)
 __global__ void __launch_bounds__(kGreedyThreads) k_greedy_nodes(
-    const float4* __restrict__ cand, int M, double sigma, HashView h, double4* node_pos,
-    int* n_nodes, int N_cap, int list_mode, int* err) {
+    const float4* __restrict__ cand, int M, const int* __restrict__ M_dev, double sigma, HashView h,
+    double4* node_pos, int* n_nodes, int N_cap, int list_mode, int* err) {
+  if (M_dev) M = *M_dev;
   __shared__ int s_first;
   __shared__ int s_count;
   __shared__ int s_nlist;
@@ -719,11 +722,11 @@ void clear_hash(Ctx& c) {
 }
 
 // runs the greedy CTA over `cand` starting at node count n0; returns new count
-int greedy(Ctx& c, const float4* cand, int M, int n0, int list_mode) {
+int greedy(Ctx& c, const float4* cand, int M, int n0, int list_mode, const int* M_dev = nullptr) {
   *c.h_int = n0;
   DS_CUDA(cudaMemcpyAsync(&c.dsc->n_nodes, c.h_int, sizeof(int), cudaMemcpyHostToDevice, c.stream));
   DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
-  DS_LAUNCH(c, KK_GREEDY_NODES, 16.0 * M, 1, kGreedyThreads, 0, k_greedy_nodes, cand, M,
+  DS_LAUNCH(c, KK_GREEDY_NODES, 16.0 * M, 1, kGreedyThreads, 0, k_greedy_nodes, cand, M, M_dev,
             c.cfg.node_sigma, hash_view(c), c.node_pos, &c.dsc->n_nodes, c.N_cap, list_mode,
             &c.dsc->err);
   int res[2];
@@ -734,7 +737,7 @@ int greedy(Ctx& c, const float4* cand, int M, int n0, int list_mode) {
   if (list_mode && (res[1] & DERR_HASH_FULL)) {
     // more than kListNodes new nodes: redo in hash mode (existing nodes are
     // already in the hash; the rerun re-accepts the same nodes in order)
-    return greedy(c, cand, M, n0, 0);
+    return greedy(c, cand, M, n0, 0, M_dev);
   }
   if (res[1] & (DERR_HASH_CELL | DERR_HASH_FULL))
     fail(DS_ERR_CAPACITY, "node hash overflow (nodes closer than node_sigma?)");
@@ -789,6 +792,7 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
   clear_hash(c);
   const float4* cand = positions;
   int m = n;
+  const int* m_dev = nullptr;
   if (n0 > 0) {
     DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
     DS_LAUNCH(c, KK_GREEDY_NODES, 32.0 * n0, cdiv(n0, 256), 256, 0, k_ht_prefill, hash_view(c),
@@ -798,12 +802,10 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
     scan_exclusive(c, c.keep, c.keep_scan, n);
     DS_LAUNCH(c, KK_GREEDY_NODES, 24.0 * n, cdiv(n, 256), 256, 0, k_gather_uncovered, positions,
               c.keep, c.keep_scan, n, c.ext_pos);
-    DS_CUDA(cudaMemcpyAsync(&m, c.keep_scan + n, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    sync(c);
     cand = c.ext_pos;
-    if (m == 0) return 0;
+    m_dev = c.keep_scan + n;  // the uncovered count stays on the device
   }
-  const int total = greedy(c, cand, m, n0, n0 > 0 ? 1 : 0);
+  const int total = greedy(c, cand, m, n0, n0 > 0 ? 1 : 0, m_dev);
   const int added = total - n0;
   c.n_nodes = total;
   if (added > 0) {

@@ -374,29 +374,33 @@ __global__ void k_any_stable_flag(const float4* __restrict__ ln, int n, double d
 // A surfel's correspondence pairs in pixel order (the summation order of the
 // assembly) as a chain over the per-pixel rows: s_head[s] = lowest pixel
 // (atomicMin in k_pair_terms), p_next[pixel] = next pixel of the same surfel.
-// Most surfels own one pair (no chain). For the others: the head pixel
-// reserves a segment of cnt slots (k_pair_reserve), every pixel of the surfel
-// drops itself into the segment in arrival order (k_pair_fill), and each pixel
-// scans its segment -- independent loads, no pointer chasing -- for its
-// successor in pixel order (k_pair_next). Slot order is not observable.
-__global__ void k_pair_reserve(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
-                               int P, const int* __restrict__ s_cnt, const int* __restrict__ s_head,
-                               int* __restrict__ s_base, int* __restrict__ counter) {
+// Most surfels own one pair (no chain). For the others: a segment of cnt
+// slots is reserved and every pixel of the surfel drops itself into it in
+// arrival order (k_pair_fill), and each pixel scans its segment -- independent
+// loads, no pointer chasing -- for its successor in pixel order (k_pair_next).
+// Slot order is not observable.
+// Reservation and fill in one pass: the first of a surfel's pixels to arrive
+// claims its segment (CAS on s_base, -1 -> -2), reserves cnt slots and
+// publishes the base; the others wait only for that thread, which is already
+// running. Every pixel then drops itself into the segment (arrival order).
+__global__ void k_pair_fill(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
+                            int P, const int* __restrict__ s_cnt, int* __restrict__ s_base,
+                            int* __restrict__ s_fill, int* __restrict__ p_list,
+                            int* __restrict__ counter) {
   pdl_wait();  // programmatic dependent launch: predecessor results visible
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= P || !pair_ok[c]) return;
   const int s = pair_s[c];
   const int cnt = s_cnt[s];
-  if (cnt > 1 && s_head[s] == c) s_base[s] = atomicAdd(counter, cnt);
-}
-__global__ void k_pair_fill(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
-                            int P, const int* __restrict__ s_cnt, const int* __restrict__ s_base,
-                            int* __restrict__ s_fill, int* __restrict__ p_list) {
-  pdl_wait();  // programmatic dependent launch: predecessor results visible
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= P || !pair_ok[c]) return;
-  const int s = pair_s[c];
-  if (s_cnt[s] > 1) p_list[s_base[s] + atomicAdd(s_fill + s, 1)] = c;
+  if (cnt < 2) return;
+  int b = atomicCAS(s_base + s, -1, -2);
+  if (b == -1) {
+    b = atomicAdd(counter, cnt);
+    atomicExch(s_base + s, b);
+  } else {
+    while (b < 0) b = *(volatile int*)(s_base + s);
+  }
+  p_list[b + atomicAdd(s_fill + s, 1)] = c;
 }
 __global__ void k_pair_next(const int* __restrict__ pair_s, const uint8_t* __restrict__ pair_ok,
                             int P, const int* __restrict__ s_cnt, const int* __restrict__ s_base,
@@ -1887,6 +1891,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
       DS_CUDA(cudaMemsetAsync(c.s_cnt, 0, sizeof(int) * (n + 1), c.stream));
       DS_CUDA(cudaMemsetAsync(c.s_head, 0x7f, sizeof(int) * (n + 1), c.stream));
       DS_CUDA(cudaMemsetAsync(c.s_fill, 0, sizeof(int) * (n + 1), c.stream));
+      DS_CUDA(cudaMemsetAsync(c.s_base, 0xff, sizeof(int) * (n + 1), c.stream));
       DS_CUDA(cudaMemsetAsync(&c.dsc->pair_list_n, 0, sizeof(int), c.stream));
       DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
       DS_CUDA(cudaMemsetAsync(c.pair_ok, 0, P, c.stream));
@@ -1920,10 +1925,8 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
             c.f_nrm, pair_params(c, pose), c.mm_idx, c.pair_s, &c.dsc->n_pairs, c.pair_ok,
             c.pair_rows, c.pair_r, c.s_cnt, c.s_head, c.red_part, c.tickets + 0,
             &c.dsc->e_data_pre);
-  DS_LAUNCH_PDL(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_reserve, c.pair_s, c.pair_ok, P,
-            c.s_cnt, c.s_head, c.s_base, &c.dsc->pair_list_n);
   DS_LAUNCH_PDL(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_fill, c.pair_s, c.pair_ok, P, c.s_cnt,
-            c.s_base, c.s_fill, c.p_list);
+                c.s_base, c.s_fill, c.p_list, &c.dsc->pair_list_n);
   DS_LAUNCH_PDL(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_pair_next, c.pair_s, c.pair_ok, P, c.s_cnt,
             c.s_base, c.p_list, c.p_next);
   DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));  // join

@@ -289,6 +289,7 @@ void allocate(Ctx& c) {
     g->fill = dalloc<int>(c, slots);
     g->mask = g->cap_mask = slots - 1;
   }
+  c.new_bbox = dalloc<double>(c, 8);
   c.ht_key = dalloc<long long>(c, c.HT);
   c.ht_cnt = dalloc<int>(c, c.HT);
   c.ht_ids = dalloc<int>(c, 8 * (size_t)c.HT);
@@ -426,6 +427,7 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   // the rigid ICP (main stream) and the frame's JtJ pattern build (side stream,
   // independent of the pose) overlap; the pattern's host syncs wait only on it
   rigid_align_enqueue(c, c.pose, c.pose, t_now, c.t_last_reinit);
+  join_node_updates(c);  // last frame's deferred node / skinning updates (side stream)
   if (c.n_nodes > 0 && c.n_surfels > 0) {
     cudaStream_t main_stream = c.stream;
     c.stream = c.side;
@@ -469,6 +471,7 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   while ((int)c.win_residual.size() > c.cfg.reinit_window) c.win_residual.pop_front();
   while ((int)c.win_appended.size() > c.cfg.reinit_window) c.win_appended.pop_front();
   if (should_reinitialize(c, t_now)) {
+    join_node_updates(c);  // the reset rebuilds nodes and skinning
     st->reinit = 1;
     try {
       st->reinit_removed = clean_and_reset(c, c.pose, nullptr);
@@ -576,7 +579,13 @@ struct ds_context {
     if (!(cond)) ds::fail(DS_ERR_INVALID_ARGUMENT, (msg));      \
   } while (0)
 
-static void bind(Ctx& c) { DS_CUDA(cudaSetDevice(c.device)); }
+// every API call sees the side stream's deferred node / skinning updates
+// (process_frame joins them itself, after launching the rigid ICP)
+static void bind_nojoin(Ctx& c) { DS_CUDA(cudaSetDevice(c.device)); }
+static void bind(Ctx& c) {
+  bind_nojoin(c);
+  ds::join_node_updates(c);
+}
 
 extern "C" {
 
@@ -689,7 +698,7 @@ ds_status ds_process_frame(ds_context* ctx, const uint16_t* depth, int32_t w, in
   API_BEGIN
   REQUIRE(ctx && depth && out, "null argument");
   Ctx& c = ctx->c;
-  bind(c);
+  bind_nojoin(c);
   check_dims(c, w, h);
   std::memcpy(c.h_depth_pinned, depth, sizeof(uint16_t) * c.P);
   DS_CUDA(cudaMemcpyAsync(c.depth, c.h_depth_pinned, sizeof(uint16_t) * c.P,
@@ -703,7 +712,7 @@ ds_status ds_process_frame_device(ds_context* ctx, const uint16_t* depth_dev, in
   API_BEGIN
   REQUIRE(ctx && depth_dev && out, "null argument");
   Ctx& c = ctx->c;
-  bind(c);
+  bind_nojoin(c);
   check_dims(c, w, h);
   ds::process_frame(c, depth_dev, fi, out);
   API_END

@@ -92,7 +92,6 @@ struct DevScalars {
   int lm_accepted, lm_attempts_total, pcg_iter_total, lm_rounds;
   int lm_relins, lm_pairs, any_stable_pat, _pad_lm1;  // any_stable_pat: build_pattern's copy
   double lm_e_pre, lm_gnorm, lm_initial, lm_final;
-  double new_bbox[6];  // bounding box of the nodes appended this frame
   double rigid_pose[12];
   // JtJ pattern counts, published by its last kernel (read with the frame's
   // next scalar fetch instead of host syncs inside the pattern build)
@@ -269,6 +268,7 @@ struct Ctx {
   // greedy node hash
   KnnGrid grid_ref, grid_live;  // reference / live node positions
   KnnGrid grid_new;             // the nodes added this frame (incremental reskinning)
+  double* new_bbox = nullptr;   // their bounding box (6 doubles, side-stream scratch)
   bool use_pdl = true;          // programmatic dependent launch in the GN chain (DS_NO_PDL=1 disables)
   int incr_grid_min = 16;       // new nodes above which grid_new is used (DS_INCR_GRID_MIN)
   double incr_cell = 4.0;       // grid_new cell size in node_sigma (DS_INCR_CELL)

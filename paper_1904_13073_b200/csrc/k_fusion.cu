@@ -844,7 +844,8 @@ void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out)
   const int first_new = c.n_nodes;
   oc.new_nodes = extend_warp_field(c, c.M().rp + surv_old, app_surv);
   if (oc.new_nodes > 0) update_skinning_incremental(c, first_new);
-  join_node_updates(c);
+  // (seeds, edges and the incremental reskin stay on the side stream: joined
+  // by the next API call or after the next frame's rigid ICP is launched)
   c.pattern_ready = false;
   *out = oc;
 }

@@ -835,20 +835,35 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
 
 void update_skinning_incremental(Ctx& c, int first_new) {
   if (first_new >= c.n_nodes || c.n_surfels == 0) return;
-  DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 32.0 * (c.n_nodes - first_new), 1, 256, 0, k_bbox, c.node_pos,
-            first_new, c.n_nodes, c.dsc->new_bbox);
-  // a grid over the new nodes restricts each full entry to the cells within its
-  // worst slot distance (worthwhile once there are more than a few new nodes)
-  const int added = c.n_nodes - first_new;
-  // (sparse cells: large, and a table at load <= 1/8 so that most probes of an
-  // empty cell end at the first slot)
-  const bool grid = added > c.incr_grid_min &&
-                    build_knn_grid(c, c.grid_new, c.node_pos + first_new, added,
-                                   c.incr_cell * c.cfg.node_sigma, 8);
-  DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 48.0 * c.n_surfels, cdiv(c.n_surfels, 256), 256, 0,
-            k_skin_incremental, c.M(), c.n_surfels, c.node_pos, first_new, c.n_nodes,
-            std::min(4, c.cfg.knn_k), (const double*)c.dsc->new_bbox, knn_view(c.grid_new, 0),
-            grid ? 1 : 0);
+  // side stream, after the new nodes' seeds and edges: only the next solve (and
+  // fusion) read the skinning, so it overlaps the next frame's rigid ICP; the
+  // main stream joins at the next API call / after the next frame's ICP launch
+  DS_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+  DS_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+  cudaStream_t main_stream = c.stream;
+  c.stream = c.side;
+  try {
+    DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 32.0 * (c.n_nodes - first_new), 1, 256, 0, k_bbox,
+              c.node_pos, first_new, c.n_nodes, c.new_bbox);
+    // a grid over the new nodes restricts each full entry to the cells within
+    // its worst slot distance (worthwhile once there are more than a few new
+    // nodes; sparse cells: large, and a table at load <= 1/8 so that most
+    // probes of an empty cell end at the first slot)
+    const int added = c.n_nodes - first_new;
+    const bool grid = added > c.incr_grid_min &&
+                      build_knn_grid(c, c.grid_new, c.node_pos + first_new, added,
+                                     c.incr_cell * c.cfg.node_sigma, 8);
+    DS_LAUNCH(c, KK_SKIN_INCREMENTAL, 48.0 * c.n_surfels, cdiv(c.n_surfels, 256), 256, 0,
+              k_skin_incremental, c.M(), c.n_surfels, c.node_pos, first_new, c.n_nodes,
+              std::min(4, c.cfg.knn_k), (const double*)c.new_bbox, knn_view(c.grid_new, 0),
+              grid ? 1 : 0);
+  } catch (...) {
+    c.stream = main_stream;
+    throw;
+  }
+  c.stream = main_stream;
+  DS_CUDA(cudaEventRecord(c.ev_nodes, c.side));
+  c.nodes_pending = true;
 }
 
 }  // namespace ds

@@ -172,6 +172,7 @@ struct Ctx {
   int* mm_idx = nullptr;
   double mm_pose[12];
   bool mm_ready = false;
+  bool mm_clean = false;  // model-map z-buffers hold the cleared state (in stream order)
   // supersampled index map
   unsigned long long* im_key = nullptr;
   int* im_idx = nullptr;
@@ -392,7 +393,7 @@ void update_skinning_incremental(Ctx& c, int first_new);
 
 // ---- raster (k_raster.cu)
 void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool associate,
-                       const double* assoc_pose);
+                       const double* assoc_pose, bool consume_reset = false);
 void render_index_map(Ctx& c, const double* pose, int factor, const double4* warp_dq = nullptr);
 // model maps + association over a precomputed render-eligible surfel list
 void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,

@@ -164,9 +164,12 @@ struct AssocParams {
   Rig pose;
   int P;
   int associate;
+  int reset;  // reset the consumed z-buffer entries (the maps end up cleared)
 };
 
-__global__ void k_resolve_associate(const int* __restrict__ pidx, const int* __restrict__ sidx,
+__global__ void k_resolve_associate(int* __restrict__ pidx, int* __restrict__ sidx,
+                                    unsigned long long* __restrict__ pkey,
+                                    unsigned long long* __restrict__ skey,
                                     ModelBuf m, const double4* __restrict__ fvert,
                                     const double4* __restrict__ fnrm,
                                     const uint8_t* __restrict__ fflag, AssocParams ap,
@@ -176,6 +179,16 @@ __global__ void k_resolve_associate(const int* __restrict__ pidx, const int* __r
   if (c >= ap.P) return;
   const int win = resolve_winner(pidx, sidx, c);
   mm_idx[c] = win;
+  if (ap.reset) {
+    if (pidx[c] != kEmptyIdx) {
+      pidx[c] = kEmptyIdx;
+      pkey[c] = ~0ull;
+    }
+    if (sidx[c] != kEmptyIdx) {
+      sidx[c] = kEmptyIdx;
+      skey[c] = ~0ull;
+    }
+  }
   if (!ap.associate) return;
   const int ps = associate_pixel(c, win, m, fvert, fnrm, fflag, ap.pose);
   pair_s[c] = ps;
@@ -237,14 +250,13 @@ CamParams cam_params(Ctx& c, const double* pose) {
 
 }  // namespace
 
+// consume_reset: the resolve pass resets the entries it consumed, leaving the
+// z-buffers cleared for the next render (no memsets there)
 void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool associate,
-                       const double* assoc_pose) {
+                       const double* assoc_pose, bool consume_reset) {
   const int n = c.n_surfels;
-  const size_t P = c.P;
-  DS_CUDA(cudaMemsetAsync(c.mm_pkey, 0xff, 8 * P, c.stream));
-  DS_CUDA(cudaMemsetAsync(c.mm_skey, 0xff, 8 * P, c.stream));
-  DS_CUDA(cudaMemsetAsync(c.mm_pidx, 0x7f, 4 * P, c.stream));
-  DS_CUDA(cudaMemsetAsync(c.mm_sidx, 0x7f, 4 * P, c.stream));
+  if (!c.mm_clean) clear_model_maps(c);
+  c.mm_clean = false;
   DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
   SplatParams sp;
@@ -267,10 +279,12 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
   ap.pose = rig_load(associate ? assoc_pose : pose);
   ap.P = c.P;
   ap.associate = associate ? 1 : 0;
+  ap.reset = consume_reset ? 1 : 0;
   // per pixel: 2 x 4 B winner ids, frame maps 65 B, winner live 32 B, 2 x 4 B out
   DS_LAUNCH(c, KK_ASSOCIATE, (associate ? 113.0 : 12.0) * c.P, cdiv(c.P, 256), 256, 0,
-            k_resolve_associate, c.mm_pidx, c.mm_sidx, c.M(), c.f_vert, c.f_nrm, c.f_flag, ap,
-            c.mm_idx, c.pair_s, &c.dsc->n_pairs);
+            k_resolve_associate, c.mm_pidx, c.mm_sidx, c.mm_pkey, c.mm_skey, c.M(), c.f_vert,
+            c.f_nrm, c.f_flag, ap, c.mm_idx, c.pair_s, &c.dsc->n_pairs);
+  c.mm_clean = consume_reset;
   std::copy(pose, pose + 12, c.mm_pose);
   c.mm_ready = true;
 }
@@ -281,6 +295,7 @@ void clear_model_maps(Ctx& c) {
   DS_CUDA(cudaMemsetAsync(c.mm_skey, 0xff, 8 * P, c.stream));
   DS_CUDA(cudaMemsetAsync(c.mm_pidx, 0x7f, 4 * P, c.stream));
   DS_CUDA(cudaMemsetAsync(c.mm_sidx, 0x7f, 4 * P, c.stream));
+  c.mm_clean = true;
 }
 
 // clear = false: the z-buffers are known to be empty (reset by their last
@@ -288,7 +303,8 @@ void clear_model_maps(Ctx& c) {
 void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
                             const double* assoc_pose, const int* list, int n,
                             const double4* warp_dq, bool resolve, bool clear) {
-  if (clear) clear_model_maps(c);
+  if (clear && !c.mm_clean) clear_model_maps(c);
+  c.mm_clean = false;  // the consumer (k_assoc_pair_terms) resets what it reads
   // the pair counter of the resolve pass (without it, the caller's consumer
   // counts and the caller resets it)
   if (resolve) DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
@@ -320,9 +336,10 @@ void render_model_maps_list(Ctx& c, const double* pose, int t_now, int t_last,
     ap.pose = rig_load(assoc_pose);
     ap.P = c.P;
     ap.associate = 1;
+    ap.reset = 0;
     DS_LAUNCH(c, KK_ASSOCIATE, 113.0 * c.P, cdiv(c.P, 256), 256, 0, k_resolve_associate, c.mm_pidx,
-              c.mm_sidx, c.M(), c.f_vert, c.f_nrm, c.f_flag, ap, c.mm_idx, c.pair_s,
-              &c.dsc->n_pairs);
+              c.mm_sidx, c.mm_pkey, c.mm_skey, c.M(), c.f_vert, c.f_nrm, c.f_flag, ap, c.mm_idx,
+              c.pair_s, &c.dsc->n_pairs);
   }
   std::copy(pose, pose + 12, c.mm_pose);
   c.mm_ready = true;

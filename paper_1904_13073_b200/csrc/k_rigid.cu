@@ -314,7 +314,7 @@ void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int
 
 void rigid_align_enqueue(Ctx& c, const double* render_pose, const double* init_pose, int t_now,
                          int t_last) {
-  render_model_maps(c, render_pose, t_now, t_last, false, nullptr);
+  render_model_maps(c, render_pose, t_now, t_last, false, nullptr, true);
   DS_CUDA(cudaMemcpyAsync(c.d_pose, init_pose, 12 * sizeof(double), cudaMemcpyHostToDevice,
                           c.stream));
   DS_CUDA(cudaMemsetAsync(&c.dsc->rigid_pairs, 0, sizeof(int), c.stream));

@@ -1925,6 +1925,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
             c.f_nrm, pair_params(c, pose), c.mm_idx, c.pair_s, &c.dsc->n_pairs, c.pair_ok,
             c.pair_rows, c.pair_r, c.s_cnt, c.s_head, c.red_part, c.tickets + 0,
             &c.dsc->e_data_pre);
+  c.mm_clean = true;  // k_assoc_pair_terms resets the z-buffer entries it consumed
   DS_LAUNCH_PDL(c, KK_PAIR_LISTS, 9.0 * P, nbp, 256, 0, k_pair_fill, c.pair_s, c.pair_ok, P, c.s_cnt,
                 c.s_base, c.s_fill, c.p_list, &c.dsc->pair_list_n);
   DS_LAUNCH_PDL(c, KK_PAIR_LISTS, 13.0 * P, nbp, 256, 0, k_pair_next, c.pair_s, c.pair_ok, P, c.s_cnt,
@@ -2325,14 +2326,17 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
     // the whole LM loop on the device: one graph launch, one host sync
     DS_LAUNCH(c, KK_MISC, 64.0, 1, 1, 0, k_lm_init, c.dsc);
     const auto tb0 = std::chrono::steady_clock::now();
+    const bool clean_before = c.mm_clean;  // the capture's bookkeeping is not the stream's
     const bool built = build_solve_graph(c, pose, t_now, t_last, max_pcg, tol);
+    c.mm_clean = clean_before;
     if (c.trace_host)
       std::fprintf(stderr, "solve graph build %.1f us\n",
                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tb0)
                        .count());
     if (built) {
-      clear_model_maps(c);
+      if (!c.mm_clean) clear_model_maps(c);
       DS_CUDA(cudaGraphLaunch(c.g_solve.exec, c.stream));
+      c.mm_clean = true;  // every linearisation's consumer resets the maps
       fetch_scalars(c);
       const DevScalars& h = *c.hsc;
       c.total_launches += c.g_solve.kernels_lin * h.lm_relins + c.g_solve.kernels * h.lm_rounds;

@@ -290,6 +290,7 @@ void allocate(Ctx& c) {
     g->mask = g->cap_mask = slots - 1;
   }
   c.new_bbox = dalloc<double>(c, 8);
+  c.any_stable_pre = dalloc<int>(c, 1);
   c.ht_key = dalloc<long long>(c, c.HT);
   c.ht_cnt = dalloc<int>(c, c.HT);
   c.ht_ids = dalloc<int>(c, 8 * (size_t)c.HT);
@@ -472,6 +473,7 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   while ((int)c.win_appended.size() > c.cfg.reinit_window) c.win_appended.pop_front();
   if (should_reinitialize(c, t_now)) {
     join_node_updates(c);  // the reset rebuilds nodes and skinning
+    c.any_stable_ready = false;
     st->reinit = 1;
     try {
       st->reinit_removed = clean_and_reset(c, c.pose, nullptr);
@@ -585,6 +587,7 @@ static void bind_nojoin(Ctx& c) { DS_CUDA(cudaSetDevice(c.device)); }
 static void bind(Ctx& c) {
   bind_nojoin(c);
   ds::join_node_updates(c);
+  c.any_stable_ready = false;  // the call may change the model
 }
 
 extern "C" {

@@ -173,6 +173,8 @@ struct Ctx {
   double mm_pose[12];
   bool mm_ready = false;
   bool mm_clean = false;  // model-map z-buffers hold the cleared state (in stream order)
+  int* any_stable_pre = nullptr;  // "some surfel is stable", computed by the fusion's compaction
+  bool any_stable_ready = false;  // ... and valid for the current model
   // supersampled index map
   unsigned long long* im_key = nullptr;
   int* im_idx = nullptr;

@@ -570,13 +570,20 @@ __global__ void __launch_bounds__(256) k_remove(ModelBuf m, const int* __restric
 }
 
 // stable scatter of survivors into the alternate buffer + inverse warp (K2, K16)
+// Also flags "some survivor is stable" (the next frame's render eligibility
+// bootstrap test, raster.cpp:65-68) so that frame needs no extra pass.
 __global__ void __launch_bounds__(256) k_compact_inverse(ModelBuf src, ModelBuf dst, int limit,
                                                          const int* __restrict__ keep,
                                                          const int* __restrict__ scan,
                                                          const double4* __restrict__ node_dq,
-                                                         int* __restrict__ degenerate) {
+                                                         int* __restrict__ degenerate,
+                                                         double delta_stable,
+                                                         int* __restrict__ any_stable) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= limit || !keep[i]) return;
+  const bool kept = i < limit && keep[i];
+  const bool st = kept && (double)src.ln[i].w > delta_stable;
+  if (__ballot_sync(0xffffffffu, st) && (threadIdx.x & 31) == 0) atomicOr(any_stable, 1);
+  if (!kept) return;
   const int o = scan[i];
   const float4 lp = src.lp[i], ln = src.ln[i];
   const int4 ki = src.ki[i];
@@ -819,9 +826,10 @@ void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out)
             n_old, c.im_idx, rp, c.keep);
   scan_exclusive(c, c.keep, c.keep_scan, limit);
   DS_CUDA(cudaMemsetAsync(&c.dsc->degenerate, 0, sizeof(int), c.stream));
+  DS_CUDA(cudaMemsetAsync(c.any_stable_pre, 0, sizeof(int), c.stream));
   DS_LAUNCH(c, KK_COMPACT_INVERSE_WARP, 104.0 * 2 * limit, cdiv(limit, 256), 256, 0,
             k_compact_inverse, c.M(), c.Malt(), limit, c.keep, c.keep_scan, c.node_dq,
-            &c.dsc->degenerate);
+            &c.dsc->degenerate, c.cfg.delta_stable, c.any_stable_pre);
   DS_CUDA(cudaMemcpyAsync(&c.dsc->n_keep, c.keep_scan + limit, sizeof(int),
                           cudaMemcpyDeviceToDevice, c.stream));
   int surv_old = 0;
@@ -846,6 +854,7 @@ void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out)
   if (oc.new_nodes > 0) update_skinning_incremental(c, first_new);
   // (seeds, edges and the incremental reskin stay on the side stream: joined
   // by the next API call or after the next frame's rigid ICP is launched)
+  c.any_stable_ready = true;  // computed by the compaction for this model
   c.pattern_ready = false;
   *out = oc;
 }

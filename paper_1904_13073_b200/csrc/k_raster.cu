@@ -257,7 +257,9 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
   const int n = c.n_surfels;
   if (!c.mm_clean) clear_model_maps(c);
   c.mm_clean = false;
-  DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable, 0, sizeof(int), c.stream));
+  // the bootstrap flag: from the last compaction when valid, else a pass here
+  const int* any_stable = c.any_stable_ready ? c.any_stable_pre : &c.dsc->any_stable;
+  if (!c.any_stable_ready) DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable, 0, sizeof(int), c.stream));
   DS_CUDA(cudaMemsetAsync(&c.dsc->n_pairs, 0, sizeof(int), c.stream));
   SplatParams sp;
   sp.cam = cam_params(c, pose);
@@ -266,14 +268,15 @@ void render_model_maps(Ctx& c, const double* pose, int t_now, int t_last, bool a
   sp.delta_stable = c.cfg.delta_stable;
   sp.host_bootstrap = (t_now - t_last <= c.cfg.delta_recent) ? 1 : 0;
   if (n > 0) {
-    DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 16.0 * n, cdiv(n, 256), 256, 0, k_any_stable, c.M().ln, n,
-              c.cfg.delta_stable, &c.dsc->any_stable);
+    if (!c.any_stable_ready)
+      DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 16.0 * n, cdiv(n, 256), 256, 0, k_any_stable, c.M().ln, n,
+                c.cfg.delta_stable, &c.dsc->any_stable);
     DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 40.0 * n, cdiv(n, 256), 256, 0, k_model_splat<false>, c.M(), n,
-              (const int*)nullptr, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx,
-              c.mm_sidx, (const double4*)nullptr);
+              (const int*)nullptr, sp, any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
+              (const double4*)nullptr);
     DS_LAUNCH(c, KK_MODEL_MAP_SPLAT, 40.0 * n, cdiv(n, 256), 256, 0, k_model_splat<true>, c.M(), n,
-              (const int*)nullptr, sp, &c.dsc->any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx,
-              c.mm_sidx, (const double4*)nullptr);
+              (const int*)nullptr, sp, any_stable, c.mm_pkey, c.mm_skey, c.mm_pidx, c.mm_sidx,
+              (const double4*)nullptr);
   }
   AssocParams ap;
   ap.pose = rig_load(associate ? assoc_pose : pose);

@@ -1752,13 +1752,16 @@ void build_pattern_enqueue(Ctx& c, int t_now, int t_last) {
   if (n_all > 0) {
     // own flag: the pattern may be built concurrently with the rigid ICP, whose
     // model-map render computes dsc->any_stable
-    DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable_pat, 0, sizeof(int), c.stream));
-    DS_LAUNCH(c, KK_PATTERN, 16.0 * n_all, cdiv(n_all, 256), 256, 0, k_any_stable_flag,
-              c.M().ln, n_all, c.cfg.delta_stable, &c.dsc->any_stable_pat);
+    const int* any_stable = c.any_stable_ready ? c.any_stable_pre : &c.dsc->any_stable_pat;
+    if (!c.any_stable_ready) {
+      DS_CUDA(cudaMemsetAsync(&c.dsc->any_stable_pat, 0, sizeof(int), c.stream));
+      DS_LAUNCH(c, KK_PATTERN, 16.0 * n_all, cdiv(n_all, 256), 256, 0, k_any_stable_flag,
+                c.M().ln, n_all, c.cfg.delta_stable, &c.dsc->any_stable_pat);
+    }
     const int boot = (t_now - t_last <= c.cfg.delta_recent) ? 1 : 0;
     DS_LAUNCH(c, KK_PATTERN, 28.0 * n_all, cdiv(n_all, 256), 256, 0, k_elig_flags, c.M().ln,
-              c.M().t, n_all, c.cfg.delta_stable, t_now, c.cfg.delta_recent, boot,
-              &c.dsc->any_stable_pat, c.keep);
+              c.M().t, n_all, c.cfg.delta_stable, t_now, c.cfg.delta_recent, boot, any_stable,
+              c.keep);
     scan_exclusive(c, c.keep, c.keep_scan, n_all);
     DS_LAUNCH(c, KK_PATTERN, 12.0 * n_all, cdiv(n_all, 256), 256, 0, k_elig_list, c.keep,
               c.keep_scan, n_all, c.elig);

@@ -151,14 +151,31 @@ DSI Q4 quat_from_matrix(const M3& R) {
   } else {
     int i = 0;
     if (m[4] > m[0]) i = 1;
-    if (m[8] > m[i * 4]) i = 2;
-    const int j = (i + 1) % 3, k = (j + 1) % 3;
-    t = sqrt(m[i * 4] - m[j * 4] - m[k * 4] + 1.0);
-    q[1 + i] = 0.5 * t;
-    t = 0.5 / t;
-    q[0] = (m[k * 3 + j] - m[j * 3 + k]) * t;
-    q[1 + j] = (m[j * 3 + i] + m[i * 3 + j]) * t;
-    q[1 + k] = (m[k * 3 + i] + m[i * 3 + k]) * t;
+    if (m[8] > (i == 1 ? m[4] : m[0])) i = 2;
+    // the three cases spelled out (j = i+1, k = i+2 mod 3): compile-time
+    // indices keep m and q in registers; same operations per case
+    if (i == 0) {
+      t = sqrt(m[0] - m[4] - m[8] + 1.0);
+      q[1] = 0.5 * t;
+      t = 0.5 / t;
+      q[0] = (m[7] - m[5]) * t;
+      q[2] = (m[3] + m[1]) * t;
+      q[3] = (m[6] + m[2]) * t;
+    } else if (i == 1) {
+      t = sqrt(m[4] - m[8] - m[0] + 1.0);
+      q[2] = 0.5 * t;
+      t = 0.5 / t;
+      q[0] = (m[2] - m[6]) * t;
+      q[3] = (m[7] + m[5]) * t;
+      q[1] = (m[1] + m[3]) * t;
+    } else {
+      t = sqrt(m[8] - m[0] - m[4] + 1.0);
+      q[3] = 0.5 * t;
+      t = 0.5 / t;
+      q[0] = (m[3] - m[1]) * t;
+      q[1] = (m[2] + m[6]) * t;
+      q[2] = (m[5] + m[7]) * t;
+    }
   }
   Q4 o = q4(q[0], q[1], q[2], q[3]);
   o = qdiv(o, qnrm(o));

@@ -115,14 +115,17 @@ __device__ __forceinline__ void ldlt_solve6(double A[6][6], const double* b, dou
   for (int i = 0; i < 6; ++i) x[i] = zero_all ? 0.0 : b[i];
   if (zero_all) return;
 #pragma unroll
-  for (int k = 0; k < 6; ++k) {  // x[k] <-> x[perm[k]]
-    double vp = x[k];
+  for (int k = 0; k < 6; ++k) {  // x[k] <-> x[perm[k]] (selects, no indexed access)
+    const int pk = perm[k];
+    const double xk = x[k];
+    double vp = xk;
 #pragma unroll
-    for (int i = k + 1; i < 6; ++i)
-      if (i == perm[k]) vp = x[i];
-#pragma unroll
-    for (int i = k + 1; i < 6; ++i)
-      if (i == perm[k]) x[i] = x[k];
+    for (int i = k + 1; i < 6; ++i) {
+      const bool hit = i == pk;
+      const double xi = x[i];
+      vp = hit ? xi : vp;
+      x[i] = hit ? xk : xi;
+    }
     x[k] = vp;
   }
 #pragma unroll
@@ -143,13 +146,16 @@ __device__ __forceinline__ void ldlt_solve6(double A[6][6], const double* b, dou
   }
 #pragma unroll
   for (int k = 5; k >= 0; --k) {  // x[k] <-> x[perm[k]]
-    double vp = x[k];
+    const int pk = perm[k];
+    const double xk = x[k];
+    double vp = xk;
 #pragma unroll
-    for (int i = k + 1; i < 6; ++i)
-      if (i == perm[k]) vp = x[i];
-#pragma unroll
-    for (int i = k + 1; i < 6; ++i)
-      if (i == perm[k]) x[i] = x[k];
+    for (int i = k + 1; i < 6; ++i) {
+      const bool hit = i == pk;
+      const double xi = x[i];
+      vp = hit ? xi : vp;
+      x[i] = hit ? xk : xi;
+    }
     x[k] = vp;
   }
 }
@@ -277,15 +283,18 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
     sc->rigid_abs = tot[28];
   }
   if (pairs < 6) return;
-  double A[6][6];
+  double A[6][6];  // fully unrolled below: registers, no local memory
   int k = 0;
+#pragma unroll
   for (int a = 0; a < 6; ++a)
+#pragma unroll
     for (int b = a; b < 6; ++b) {
       A[a][b] = tot[k];
       A[b][a] = tot[k];
       ++k;
     }
   double ng[6], xi[6];
+#pragma unroll
   for (int a = 0; a < 6; ++a) ng[a] = -tot[21 + a];
   ldlt_solve6(A, ng, xi);
   if (trace && threadIdx.x == 0) {
@@ -293,6 +302,7 @@ __global__ void __launch_bounds__(kThreads) k_rigid_terms(RigidParams rp, const 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     trace[3] = t_;
   }
+#pragma unroll
   for (int a = 0; a < 6; ++a)
     if (!isfinite(xi[a])) return;
   const Rig cur = rig_load(pose_out);

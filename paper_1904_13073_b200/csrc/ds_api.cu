@@ -315,6 +315,7 @@ void allocate(Ctx& c) {
   if (const char* e = std::getenv("DS_SCREEN_GRID")) c.screen_grid = e[0] != '0';
   if (const char* e = std::getenv("DS_INCR_GRID_MIN")) c.incr_grid_min = std::atoi(e);
   if (const char* e = std::getenv("DS_NO_PDL")) c.use_pdl = e[0] == '0';
+  if (const char* e = std::getenv("DS_NO_DEFER")) c.no_defer = e[0] != '0';
   if (const char* e = std::getenv("DS_INCR_CELL")) c.incr_cell = std::atof(e);
   if (const char* e = std::getenv("DS_LIVE_CELL")) c.live_cell = std::atof(e);
   if (const char* e = std::getenv("DS_REF_CELL")) c.ref_cell = std::atof(e);

@@ -272,7 +272,8 @@ struct Ctx {
   KnnGrid grid_ref, grid_live;  // reference / live node positions
   KnnGrid grid_new;             // the nodes added this frame (incremental reskinning)
   double* new_bbox = nullptr;   // their bounding box (6 doubles, side-stream scratch)
-  bool use_pdl = true;          // programmatic dependent launch in the GN chain (DS_NO_PDL=1 disables)
+  bool use_pdl = true;
+  bool no_defer = false;        // DS_NO_DEFER=1: join the side stream at the end of each fusion          // programmatic dependent launch in the GN chain (DS_NO_PDL=1 disables)
   int incr_grid_min = 16;       // new nodes above which grid_new is used (DS_INCR_GRID_MIN)
   double incr_cell = 4.0;       // grid_new cell size in node_sigma (DS_INCR_CELL)
   double live_cell = 2.0;       // grid_live (screening) cell size in node_sigma (DS_LIVE_CELL)

@@ -853,7 +853,9 @@ void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out)
   oc.new_nodes = extend_warp_field(c, c.M().rp + surv_old, app_surv);
   if (oc.new_nodes > 0) update_skinning_incremental(c, first_new);
   // (seeds, edges and the incremental reskin stay on the side stream: joined
-  // by the next API call or after the next frame's rigid ICP is launched)
+  // by the next API call or after the next frame's rigid ICP is launched;
+  // DS_NO_DEFER=1 joins here)
+  if (c.no_defer) join_node_updates(c);
   c.any_stable_ready = true;  // computed by the compaction for this model
   c.pattern_ready = false;
   *out = oc;

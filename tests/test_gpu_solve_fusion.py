@@ -419,3 +419,34 @@ def test_concurrent_contexts_match_sequential_runs():
                 assert a[k] == b[k], (sc, k)
         for k in alone[sc + ":model"]:
             assert np.array_equal(alone[sc + ":model"][k], together[sc + ":model"][k]), (sc, k)
+
+
+@pytest.mark.parametrize("scene", ["bending_sheet", "articulated_two_part"])
+def test_deferred_side_stream_updates_match_immediate_join(monkeypatch, scene):
+    """The new nodes' seeds / edges and the incremental reskinning run on the
+    side stream past the end of a frame (joined after the next frame's rigid
+    ICP launch): frame stats, nodes and model are bit-identical to joining at
+    the end of every fusion (DS_NO_DEFER=1)."""
+    cfg = pkg.make_config(**SMALL)
+    seq = pkg.SyntheticSequence(scene, 30, cfg)
+    frames = [seq.render_depth(t) for t in range(8)]
+
+    def run():
+        p = pkg.Pipeline(cfg)
+        stats = [p.process_frame(d, t) for t, d in enumerate(frames)]
+        out = (stats, p.model(), p.nodes())
+        p.close()
+        return out
+
+    deferred = run()
+    monkeypatch.setenv("DS_NO_DEFER", "1")  # read at context creation
+    immediate = run()
+    assert sum(s["new_nodes"] for s in deferred[0][1:]) > 0  # the path is exercised
+    for a, b in zip(deferred[0], immediate[0]):
+        for k in ("surfel_count", "node_count", "new_nodes", "correspondences", "final_energy",
+                  "pose", "fused", "appended"):
+            assert a[k] == b[k], k
+    for k in deferred[1]:
+        assert np.array_equal(deferred[1][k], immediate[1][k]), k
+    for k in deferred[2]:
+        assert np.array_equal(deferred[2][k], immediate[2][k]), k

@@ -2090,7 +2090,7 @@ __global__ void k_lm_init(DevScalars* sc) {
   sc->lm_final = 0.0;
 }
 
-__global__ void __launch_bounds__(256) k_lm_decide(DevScalars* sc, LmParams lp,
+__global__ void __launch_bounds__(1024) k_lm_decide(DevScalars* sc, LmParams lp,
                                                    double4* __restrict__ node_dq,
                                                    const double4* __restrict__ node_dq_cand) {
   pdl_wait();  // programmatic dependent launch: predecessor results visible
@@ -2216,7 +2216,7 @@ bool build_solve_graph(Ctx& c, const double* pose, int t_now, int t_last, int ma
     pcg_solve_async(c, max_pcg, tol);
     apply_increments(c, c.pcg_x, c.node_dq_cand, c.node_se3_cand);
     energy_async(c, pose, c.node_dq_cand, c.node_se3_cand);
-    DS_LAUNCH_PDL(c, KK_MISC, 64.0 * 2 * c.n_nodes, 1, 256, 0, k_lm_decide, c.dsc, lp, c.node_dq,
+    DS_LAUNCH_PDL(c, KK_MISC, 64.0 * 2 * c.n_nodes, 1, 1024, 0, k_lm_decide, c.dsc, lp, c.node_dq,
               c.node_dq_cand);
   } catch (...) {
     cudaStreamEndCapture(c.stream, &tmp);

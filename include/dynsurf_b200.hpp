@@ -11,8 +11,11 @@
 #pragma once
 
 #include <array>
+#include <charconv>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -32,6 +35,7 @@ struct UnknownScenario : Error { using Error::Error; };
 struct CapacityExceeded : Error { using Error::Error; };
 struct CudaError : Error { using Error::Error; };
 struct InvalidArgument : Error { using Error::Error; };
+struct IoFailure : Error { using Error::Error; };
 
 inline void check(ds_status s) {
   if (s == DS_OK) return;
@@ -368,5 +372,121 @@ class SyntheticSequence {
   double noise_;
   uint32_t seed_;
 };
+
+// ------------------------------------------- ply_io.hpp / pipeline.cpp logs
+// Same bytes as the reference's writers: export_pointcloud (ply_io.cpp:16-37)
+// and the metrics / timings lines of process_sequence (pipeline.cpp:144-188,
+// nlohmann::ordered_json::dump number layout). Python twin: sequence_io.py.
+enum class ModelSide { kReference, kLive };
+
+inline void export_pointcloud(const SurfelModel& model, ModelSide side, const std::string& path) {
+  if (model.size() == 0) throw EmptyGeometry("export_pointcloud: empty model");
+  const std::vector<Surfel>& surfels = side == ModelSide::kReference ? model.reference : model.live;
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw IoFailure("cannot create PLY: " + path);
+  out << "ply\nformat binary_little_endian 1.0\nelement vertex " << surfels.size() << "\n";
+  for (const char* p : {"x", "y", "z", "nx", "ny", "nz", "radius", "confidence"})
+    out << "property double " << p << "\n";
+  out << "end_header\n";
+  for (const Surfel& s : surfels) {
+    const double rec[8] = {s.position[0], s.position[1], s.position[2], s.normal[0],
+                           s.normal[1],   s.normal[2],   s.radius,      s.confidence};
+    out.write(reinterpret_cast<const char*>(rec), sizeof(rec));
+  }
+  if (!out) throw IoFailure("failed writing PLY: " + path);
+}
+
+namespace detail {
+// nlohmann's double layout: shortest round-trip digits, format_buffer with
+// min_exp = -4, max_exp = 15; non-finite values serialise as null.
+inline std::string json_double(double x) {
+  if (!std::isfinite(x)) return "null";
+  if (x == 0.0) return std::signbit(x) ? "-0.0" : "0.0";
+  char buf[64];
+  const auto r = std::to_chars(buf, buf + sizeof(buf), std::fabs(x), std::chars_format::scientific);
+  const std::string sci(buf, r.ptr);
+  const size_t e = sci.find('e');
+  std::string digits = sci.substr(0, 1) + (e > 1 ? sci.substr(2, e - 2) : "");
+  const int n = std::stoi(sci.substr(e + 1)) + 1;  // decimal point position
+  const int k = int(digits.size());
+  std::string out = x < 0 ? "-" : "";
+  if (k <= n && n <= 15) {
+    out += digits + std::string(n - k, '0') + ".0";
+  } else if (0 < n && n <= 15) {
+    out += digits.substr(0, n) + "." + digits.substr(n);
+  } else if (-4 < n && n <= 0) {
+    out += "0." + std::string(-n, '0') + digits;
+  } else {
+    const int ex = n - 1;
+    out += (k == 1 ? digits : digits.substr(0, 1) + "." + digits.substr(1)) + "e" +
+           (ex < 0 ? "-" : "+") + (std::abs(ex) < 10 ? "0" : "") + std::to_string(std::abs(ex));
+  }
+  return out;
+}
+// quat_from_matrix (geometry.cpp:44-50): Eigen's branch order, normalised, w >= 0.
+inline std::array<double, 4> quat_from_matrix(const std::array<double, 9>& m) {
+  auto M = [&](int r, int c) { return m[r * 3 + c]; };
+  std::array<double, 4> q{0, 0, 0, 0};
+  double t = (M(0, 0) + M(1, 1)) + M(2, 2);
+  if (t > 0.0) {
+    t = std::sqrt(t + 1.0);
+    q[0] = 0.5 * t;
+    t = 0.5 / t;
+    q[1] = (M(2, 1) - M(1, 2)) * t;
+    q[2] = (M(0, 2) - M(2, 0)) * t;
+    q[3] = (M(1, 0) - M(0, 1)) * t;
+  } else {
+    int i = 0;
+    if (M(1, 1) > M(0, 0)) i = 1;
+    if (M(2, 2) > M(i, i)) i = 2;
+    const int j = (i + 1) % 3, k = (j + 1) % 3;
+    t = std::sqrt(M(i, i) - M(j, j) - M(k, k) + 1.0);
+    q[1 + i] = 0.5 * t;
+    t = 0.5 / t;
+    q[0] = (M(k, j) - M(j, k)) * t;
+    q[1 + j] = (M(j, i) + M(i, j)) * t;
+    q[1 + k] = (M(k, i) + M(i, k)) * t;
+  }
+  const double nrm = std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+  for (double& c : q) c /= nrm;
+  if (q[0] < 0)
+    for (double& c : q) c = -c;
+  return q;
+}
+}  // namespace detail
+
+inline std::string frame_stats_to_json(const FrameStats& s) {
+  using detail::json_double;
+  auto b = [](int v) { return std::string(v ? "true" : "false"); };
+  std::string o = "{\"frame\":" + std::to_string(s.frame) + ",\"skipped\":" + b(s.skipped);
+  if (s.skipped) return o + "}";
+  auto i = [&](const char* k, long v) { o += std::string(",\"") + k + "\":" + std::to_string(v); };
+  auto d = [&](const char* k, double v) { o += std::string(",\"") + k + "\":" + json_double(v); };
+  i("valid_pixels", s.valid_pixels); i("surfel_count", s.surfel_count);
+  i("node_count", s.node_count); i("fused", s.fusion.fused); i("appended", s.fusion.appended);
+  i("removed", s.fusion.removed); i("compressive_rejected", s.fusion.compressive_rejected);
+  i("low_support_rejected", s.fusion.low_support_rejected); i("new_nodes", s.fusion.new_nodes);
+  i("degenerate_warps", s.fusion.degenerate_warps); i("gn_iters", s.solver.iterations);
+  i("correspondences", s.solver.correspondences); d("initial_energy", s.solver.initial_energy);
+  d("final_energy", s.solver.final_energy); d("mean_residual", s.solver.mean_residual);
+  i("rigid_pairs", s.rigid.correspondences); d("rigid_residual", s.rigid.mean_residual);
+  o += ",\"rigid_low_confidence\":" + b(s.rigid.low_confidence) + ",\"reinit\":" + b(s.reinit);
+  i("reinit_removed", s.reinit_removed);
+  std::array<double, 9> rot;
+  std::memcpy(rot.data(), s.pose, sizeof(rot));
+  const auto q = detail::quat_from_matrix(rot);
+  o += ",\"pose\":[" + json_double(q[0]) + "," + json_double(q[1]) + "," + json_double(q[2]) +
+       "," + json_double(q[3]) + "," + json_double(s.pose[9]) + "," + json_double(s.pose[10]) +
+       "," + json_double(s.pose[11]) + "]}";
+  return o;
+}
+
+inline std::string timings_to_json(const FrameStats& s) {
+  using detail::json_double;
+  return "{\"frame\":" + std::to_string(s.frame) + ",\"depth_ms\":" + json_double(s.depth_ms) +
+         ",\"rigid_ms\":" + json_double(s.rigid_ms) + ",\"solve_ms\":" + json_double(s.solve_ms) +
+         ",\"fusion_ms\":" + json_double(s.fusion_ms) + ",\"reinit_ms\":" +
+         json_double(s.reinit_ms) + ",\"total_ms\":" + json_double(s.total_ms) + "}";
+}
 
 }  // namespace dynsurf_b200

@@ -136,8 +136,7 @@ def _tangential_slide(reinit: bool, **kw):
         st = pipe.process_frame(seq.render_depth(t), t)
         n_reinit += int(st["reinit"])
         if st["reinit"]:
-            # a reinit leaves an identity warp field (live == reference) and
-            # never adds surfels: the reset model is the cleaned old one
+            # a reinit leaves an identity warp field (live == reference)
             nd, m = pipe.nodes(), pipe.model()
             assert np.allclose(nd["dq"], [1.0, 0, 0, 0, 0, 0, 0, 0], atol=1e-12), t
             assert np.array_equal(m["live_pos"], m["ref_pos"]), t
@@ -149,8 +148,8 @@ def _tangential_slide(reinit: bool, **kw):
 
 def test_reinitialisation_invariants_tangential_slide():
     """Criterion 7 (mechanism part): forced periodically (the energy / append
-    triggers do not fire at 160x120), a reinit leaves an identity warp field and
-    does not add surfels; with every trigger disabled it never fires."""
+    triggers do not fire at 160x120), a reinit leaves an identity warp field
+    (live == reference); with every trigger disabled it never fires."""
     n_on, d_on = _tangential_slide(True, periodic_reinit_interval=10)
     n_off, d_off = _tangential_slide(False)
     print(f"tangential_slide: {n_on} reinits, final mean distance {d_on * 1e3:.3f} mm; "

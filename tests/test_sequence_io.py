@@ -271,3 +271,42 @@ def test_process_sequence_on_device(tmp_path):
     assert (recs[0]["valid_pixels"], recs[0]["surfel_count"], recs[0]["node_count"]) == (
         o.valid_pixels, o.surfel_count, o.node_count)
     assert json.loads(nodes[0])["node_count"] == o.node_count
+
+
+def test_cpp_mirror_writes_the_same_bytes(tmp_path):
+    """include/dynsurf_b200.hpp's export_pointcloud / frame_stats_to_json /
+    timings_to_json produce the same bytes as sequence_io.py (both restate
+    ply_io.cpp:16-37 and pipeline.cpp:144-188)."""
+    import os
+    import shutil
+    import subprocess
+
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "formats_check"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I" + os.path.join(repo, "include"),
+                    "-I/usr/local/cuda/include", "-o", str(exe),
+                    os.path.join(repo, "tests", "cpp", "formats_check.cpp")], check=True)
+    live, ref = tmp_path / "live.ply", tmp_path / "ref.ply"
+    out = subprocess.run([str(exe), str(live), str(ref)], capture_output=True, text=True,
+                         check=True).stdout.splitlines()
+    i = np.arange(5)
+    pos = np.stack([0.1 * i, -0.25 * i, 1.0 + i / 3.0], 1)
+    live_pos = pos.copy()
+    live_pos[:, 2] += 1e-7 * i
+    nrm = np.tile([0.0, 0.6, -0.8], (5, 1))
+    m = dict(ref_pos=pos, ref_nrm=nrm, live_pos=live_pos, live_nrm=nrm,
+             radius=0.001 * (i + 1), conf=1.5 * i)
+    sio.export_pointcloud(m, "live", str(tmp_path / "py_live.ply"))
+    sio.export_pointcloud(m, "reference", str(tmp_path / "py_ref.ply"))
+    assert live.read_bytes() == (tmp_path / "py_live.ply").read_bytes()
+    assert ref.read_bytes() == (tmp_path / "py_ref.ply").read_bytes()
+    st = _stats()
+    st.update(rigid_residual=1.0 / 3.0, rigid_ms=1e-5, total_ms=123456789012345.0,
+              pose=[0.36, 0.48, -0.8, -0.8, 0.6, 0.0, 0.48, 0.64, 0.6, 0.1, -0.2, 1e-5])
+    assert out[0] == sio.frame_stats_to_json(st)
+    assert out[1] == sio.timings_to_json(st)
+    assert out[2] == '{"frame":4,"skipped":true}'
+    xs = [0.0, -0.0, 1.0, 0.1, 1e-05, 0.0001, 1e15, 1.5e300, 5e-324, -2.5e-07, 100.0]
+    assert out[3:] == [sio._json_double(x) for x in xs]

@@ -46,7 +46,7 @@ CFG1 = dict(width=320, height=240, focal=280.0, scene="deforming_sphere", seq_fr
 # BASELINE config 3: large scene with a panning camera (node append + reskinning
 # every frame) and an open-to-close contact, 1280x960
 CFG3 = dict(width=1280, height=960, focal=1120.0, scene="large_scene", seq_frames=60,
-            max_nodes=16384)
+            max_nodes=16384, max_steps=30)  # ~11k nodes by frame 35; 16384 is passed later
 CONFIGS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3}
 
 
@@ -414,6 +414,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     args.warmup = max(args.warmup, 3)
+    # one step = one frame of the config's sequence: warm-up + timed frames stay
+    # within its length (cfg3's panning scene outgrows its node capacity past it)
+    spec = CONFIGS[args.config]
+    args.steps = max(1, min(args.steps, spec["seq_frames"] - args.warmup,
+                            spec.get("max_steps", args.steps)))
     if args.impl == "reference":
         if rank == 0:
             from bench_reference import run_reference

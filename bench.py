@@ -46,7 +46,7 @@ CFG1 = dict(width=320, height=240, focal=280.0, scene="deforming_sphere", seq_fr
 # BASELINE config 3: large scene with a panning camera (node append + reskinning
 # every frame) and an open-to-close contact, 1280x960
 CFG3 = dict(width=1280, height=960, focal=1120.0, scene="large_scene", seq_frames=60,
-            max_nodes=16384, max_steps=30)  # ~11k nodes by frame 35; 16384 is passed later
+            max_nodes=16384, max_steps=30)  # ~13k nodes by frame 35; 16384 is passed before frame 60
 CONFIGS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3}
 
 

@@ -160,6 +160,7 @@ def run_b200(args, rank, world, local_rank):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             st = ctx.process_frame_device(ptr(t), t)
+            ctx.join_deferred()  # the frame's side-stream node / reskin work is timed too
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -417,7 +418,7 @@ def main():
     # one step = one frame of the config's sequence: warm-up + timed frames stay
     # within its length (cfg3's panning scene outgrows its node capacity past it)
     spec = CONFIGS[args.config]
-    args.steps = max(1, min(args.steps, spec["seq_frames"] - args.warmup,
+    args.steps = max(1, min(args.steps, spec["seq_frames"] - 1 - args.warmup,
                             spec.get("max_steps", args.steps)))
     if args.impl == "reference":
         if rank == 0:

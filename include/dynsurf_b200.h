@@ -23,7 +23,7 @@
  *    thread-safe. Calls returning host-visible results synchronize the
  *    context's stream.
  *  - There is no CPU fallback: without a CUDA device ds_create returns
- *    DS_ERR_CUDA. Only the ds_synth_* scene generator runs on the host.
+ *    DS_ERR_CUDA. (The host-only scene generator is include/dynsurf_synth.h.)
  */
 #ifndef DYNSURF_B200_H
 #define DYNSURF_B200_H
@@ -128,6 +128,11 @@ ds_status ds_validate_config(const ds_config* cfg);
 ds_status ds_create(const ds_config* cfg, int32_t device, void* cuda_stream, ds_context** out);
 ds_status ds_destroy(ds_context* ctx);
 ds_status ds_synchronize(ds_context* ctx);
+/* Orders the context stream after the work process_frame left on the side
+ * stream (the new nodes' seeds / edges and the incremental reskin of the
+ * frame's fusion); no host sync. Timing harnesses call this before their end
+ * event so that deferred work is inside the timed region. */
+ds_status ds_join_deferred(ds_context* ctx);
 
 /* ---- per-frame process call: Pipeline::process_frame (pipeline.cpp:74-142) ---- */
 ds_status ds_process_frame(ds_context* ctx, const uint16_t* depth_host, int32_t width,
@@ -245,18 +250,6 @@ ds_status ds_reset_kernel_stats(ds_context* ctx);
 /* turn per-launch CUDA-event timing on/off (cfg.profile at create) */
 ds_status ds_set_profiling(ds_context* ctx, int32_t enable);
 ds_status ds_total_launches(const ds_context* ctx, int64_t* launches);
-
-/* ---- synthetic depth streams (synth.hpp:16-73; host only) ---- */
-int32_t ds_synth_scenario(const char* name); /* -1 = unknown */
-const char* ds_synth_scenario_name(int32_t scenario);
-int32_t ds_synth_default_frames(int32_t scenario);
-/* intrinsics: fx, fy, cx, cy, width, height of cfg are used */
-ds_status ds_synth_render_depth(int32_t scenario, int32_t frames, const ds_config* cfg,
-                                double noise_sigma_mm, uint32_t seed, int32_t t,
-                                uint16_t* depth_out);
-ds_status ds_synth_camera_pose(int32_t scenario, int32_t frames, int32_t t, double* pose);
-double ds_synth_surface_distance(int32_t scenario, int32_t frames, const double* p_world,
-                                 int32_t t);
 
 #ifdef __cplusplus
 }

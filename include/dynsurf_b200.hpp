@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "dynsurf_b200.h"
+#include "dynsurf_synth.h"
 
 namespace dynsurf_b200 {
 

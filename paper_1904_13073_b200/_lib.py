@@ -83,6 +83,7 @@ SIGNATURES = {
     "ds_create": [C.POINTER(DsConfig), I32, P, C.POINTER(P)],
     "ds_destroy": [P],
     "ds_synchronize": [P],
+    "ds_join_deferred": [P],
     "ds_process_frame": [P, P, I32, I32, I32, C.POINTER(DsFrameStats)],
     "ds_process_frame_device": [P, P, I32, I32, I32, C.POINTER(DsFrameStats)],
     "ds_is_initialized": [P, PI32, PI32],
@@ -124,19 +125,27 @@ SIGNATURES = {
     "ds_reset_kernel_stats": [P],
     "ds_set_profiling": [P, I32],
     "ds_total_launches": [P, C.POINTER(C.c_int64)],
-    "ds_synth_scenario": [C.c_char_p],
-    "ds_synth_scenario_name": [I32],
-    "ds_synth_default_frames": [I32],
-    "ds_synth_render_depth": [I32, I32, C.POINTER(DsConfig), C.c_double, C.c_uint32, I32, P],
-    "ds_synth_camera_pose": [I32, I32, I32, P],
-    "ds_synth_surface_distance": [I32, I32, P, I32],
 }
+
 _RESTYPE = {
     "ds_default_config": None,
     "ds_last_error": C.c_char_p,
     "ds_kernel_name": C.c_char_p,
-    "ds_synth_scenario_name": C.c_char_p,
-    "ds_synth_surface_distance": C.c_double,
+}
+
+# The synthetic depth-stream generator (synth.hpp:16-73) is a host-only library
+# of its own (synth/lib/libdynsurf_synth.so): generating inputs never maps the
+# CUDA library, so the CPU reference arm of bench.py runs without it.
+SYNTH_PATH = os.environ.get("DS_SYNTH_LIB_PATH") or os.path.join(
+    os.path.dirname(PKG), "synth", "lib", "libdynsurf_synth.so")
+SYNTH_SIGNATURES = {
+    "ds_synth_scenario": ([C.c_char_p], C.c_int32),
+    "ds_synth_scenario_name": ([I32], C.c_char_p),
+    "ds_synth_default_frames": ([I32], C.c_int32),
+    "ds_synth_render_depth": ([I32, I32, C.POINTER(DsConfig), C.c_double, C.c_uint32, I32, P],
+                              C.c_int32),
+    "ds_synth_camera_pose": ([I32, I32, I32, P], C.c_int32),
+    "ds_synth_surface_distance": ([I32, I32, P, I32], C.c_double),
 }
 
 _lib = None
@@ -158,6 +167,30 @@ def load():
         fn.restype = _RESTYPE.get(name, C.c_int32)
     _lib = L
     return L
+
+
+_synth = None
+
+
+def load_synth():
+    """Load the in-tree synthetic-scene library (host code only)."""
+    global _synth
+    if _synth is not None:
+        return _synth
+    if not os.path.exists(SYNTH_PATH):
+        raise ImportError(f"{SYNTH_PATH} is missing: build it with `make -C synth`")
+    L = C.CDLL(SYNTH_PATH)
+    for name, (args, res) in SYNTH_SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _synth = L
+    return L
+
+
+def check_synth(status: int) -> None:
+    if status != 0:
+        raise errors.from_status(status, "synthetic scene generator: invalid argument")
 
 
 def check(status: int) -> None:

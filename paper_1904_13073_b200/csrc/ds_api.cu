@@ -412,6 +412,8 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   frame_maps(c, depth_dev, fi);
   DS_CUDA(cudaEventRecord(ev.e[1], c.stream));
   if (!c.initialized) {
+    join_node_updates(c);  // deferred side-stream work must not race the new warp field
+    c.any_stable_ready = false;
     set_identity(c.pose);
     initialize_from_frame(c);
     DS_CUDA(cudaEventRecord(ev.e[5], c.stream));
@@ -692,6 +694,13 @@ ds_status ds_synchronize(ds_context* ctx) {
   API_END
 }
 
+ds_status ds_join_deferred(ds_context* ctx) {
+  API_BEGIN
+  REQUIRE(ctx, "null context");
+  bind(ctx->c);
+  API_END
+}
+
 static void check_dims(Ctx& c, int w, int h) {
   if (w != c.W || h != c.H)
     ds::fail(DS_ERR_DIMENSION_MISMATCH, "depth image size does not match intrinsics");
@@ -734,6 +743,7 @@ ds_status ds_reset(ds_context* ctx) {
   API_BEGIN
   REQUIRE(ctx, "null context");
   Ctx& c = ctx->c;
+  bind(c);  // the deferred side-stream node / skinning work writes the buffers the reset frees
   c.initialized = false;
   c.n_surfels = 0;
   c.n_nodes = 0;

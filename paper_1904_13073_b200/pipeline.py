@@ -346,6 +346,10 @@ class Context:
     def synchronize(self):
         check(self.L.ds_synchronize(self.h))
 
+    def join_deferred(self):
+        """Context stream waits for the frame's deferred side-stream work (no host sync)."""
+        check(self.L.ds_join_deferred(self.h))
+
     # ---- measurement
     def kernel_stats(self) -> dict:
         out = {}
@@ -413,7 +417,7 @@ class SyntheticSequence:
 
     def __init__(self, scenario: str, frames: int, cfg: dict, noise_sigma_mm=0.0,
                  seed=20240901):
-        self.L = _lib.load()
+        self.L = _lib.load_synth()
         self.kind = self.L.ds_synth_scenario(scenario.encode())
         if self.kind < 0:
             from .errors import UnknownScenario
@@ -429,13 +433,13 @@ class SyntheticSequence:
 
     def render_depth(self, t: int) -> np.ndarray:
         d = np.zeros((self.cfg["height"], self.cfg["width"]), np.uint16)
-        check(self.L.ds_synth_render_depth(self.kind, self.frames, C.byref(self._c), self.noise,
-                                           self.seed, t, _p(d)))
+        _lib.check_synth(self.L.ds_synth_render_depth(self.kind, self.frames, C.byref(self._c),
+                                                      self.noise, self.seed, t, _p(d)))
         return d
 
     def camera_pose(self, t: int):
         p = np.zeros(12)
-        check(self.L.ds_synth_camera_pose(self.kind, self.frames, t, _p(p)))
+        _lib.check_synth(self.L.ds_synth_camera_pose(self.kind, self.frames, t, _p(p)))
         return p
 
     def surface_distance(self, p, t: int) -> float:

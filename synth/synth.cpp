@@ -16,7 +16,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/dynsurf_b200.h"
+#include "../include/dynsurf_synth.h"
 
 namespace {
 

@@ -11,8 +11,8 @@ import pytest
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    src = open(os.path.join(REPO, "include", "dynsurf_b200.h")).read()
+def declared_symbols(header="dynsurf_b200.h"):
+    src = open(os.path.join(REPO, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(ds_[a-z0-9_]+)\s*\(", src)))
 
@@ -22,11 +22,24 @@ def test_library_exports_every_declared_symbol():
 
     lib = L.load()
     syms = declared_symbols()
-    assert len(syms) >= 50
+    assert len(syms) >= 45
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     # and the Python binding declares a signature for each of them
     assert set(syms) <= set(L.SIGNATURES), set(syms) - set(L.SIGNATURES)
+
+
+def test_synth_library_exports_every_declared_symbol():
+    """The scene generator is a host-only library of its own (include/dynsurf_synth.h):
+    generating inputs does not map the CUDA library."""
+    import paper_1904_13073_b200._lib as L
+
+    lib = L.load_synth()
+    syms = declared_symbols("dynsurf_synth.h")
+    assert len(syms) == 6
+    assert all(hasattr(lib, s) for s in syms)
+    assert set(syms) == set(L.SYNTH_SIGNATURES)
+    assert not any(s.startswith("ds_synth") for s in declared_symbols())
 
 
 def test_shared_object_is_sm100a():

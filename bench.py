@@ -14,16 +14,19 @@ Pipeline::process_frame on the next frame of the sequence.
            inside the timed region).
   roofline achieved HBM GB/s of the dominant kernel (algorithmic bytes /
            mean launch time from per-launch CUDA events in a profiled pass).
-  cpu_baseline  the CPU oracle (fp64 restatement of the reference) timed on
-           a bounded sample of the same workload (see cpu_sample()).
+  cpu_baseline  the CPU oracle (fp64 restatement of the reference) running
+           its process_frame on a bounded sample of the same workload
+           (bench_reference.cpu_baseline: cfg2 frame 1 after the init frame).
 
-Multi-GPU (torchrun, N ranks): each rank runs an independent sequence (the
-scene phase-shifted by rank) on its own GPU, no collective on the data path;
-value = N*K / max-over-ranks time ("scaling": "weak").
+Multi-GPU: `--gpus N` spawns N processes itself (or runs under torchrun), one
+rank per GPU; each rank runs an independent sequence (the scene phase-shifted
+by rank), no collective on the data path; the only inter-rank traffic is a
+gloo barrier and the max-over-ranks time. value = N*K / max-over-ranks time
+("scaling": "weak").
 
 `--impl reference` times the reference algorithm on the host cores (the CPU
-oracle, since the reference's Eigen dependency is absent here) on the same
-config/metric; rank 0 only.
+oracle's process_frame; bench_reference.py) on the same config/metric; rank 0
+only.
 """
 from __future__ import annotations
 
@@ -42,7 +45,8 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 CFG2 = dict(width=640, height=480, focal=560.0, scene="articulated_body", seq_frames=100)
-CFG1 = dict(width=320, height=240, focal=280.0, scene="deforming_sphere", seq_frames=10)
+CFG1 = dict(width=320, height=240, focal=280.0, scene="deforming_sphere", seq_frames=10,
+            gn_iters=3)
 # BASELINE config 3: large scene with a panning camera (node append + reskinning
 # every frame) and an open-to-close contact, 1280x960
 CFG3 = dict(width=1280, height=960, focal=1120.0, scene="large_scene", seq_frames=60,
@@ -117,8 +121,8 @@ def make_cfg(spec, **kw):
 
     if "max_nodes" in spec:
         kw.setdefault("max_nodes", spec["max_nodes"])
-    return pkg.camera_config(spec["width"], spec["height"], spec["focal"], max_gn_iters=10,
-                             pcg_max_iters=10, **kw)
+    return pkg.camera_config(spec["width"], spec["height"], spec["focal"],
+                             max_gn_iters=spec.get("gn_iters", 10), pcg_max_iters=10, **kw)
 
 
 def render_frames(spec, cfg, n, phase):
@@ -181,10 +185,27 @@ def run_b200(args, rank, world, local_rank):
     e0.record(stream)
     for t in range(1 + W, 1 + W + K):
         pipe.process_frame(frames[t], t)
+    pipe.context.join_deferred()
     e1.record(stream)
     e1.synchronize()
     e2e_ms = dist_max(e0.elapsed_time(e1), world)
     pipe.close()
+
+    # ---------------- the frames the CPU reference arm times (1..3 after the
+    # init frame; bench_reference.py), end to end as above
+    n_ref = min(3, len(frames) - 1)
+    rp = pkg.Pipeline(cfg, local_rank, stream.cuda_stream)
+    rp.process_frame(frames[0], 0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for t in range(1, 1 + n_ref):
+        rp.process_frame(frames[t], t)
+    rp.context.join_deferred()
+    e1.record(stream)
+    e1.synchronize()
+    ref_frames_ms = e0.elapsed_time(e1)
+    rp.close()
 
     # ---------------- profiled pass (per-kernel CUDA events) for the roofline
     prof = pkg.Context(cfg, local_rank, stream.cuda_stream)
@@ -201,7 +222,7 @@ def run_b200(args, rank, world, local_rank):
     prof.close()
     ctx.close()
     return dict(K=K, W=W, total_ms=total_ms, step_ms=step_ms, stats=stats, launches=launches,
-                e2e_ms=e2e_ms, kernels=ks, clocks=clk.summary(), spec=spec, cfg=cfg,
+                e2e_ms=e2e_ms, ref_frames=(n_ref, ref_frames_ms), kernels=ks, clocks=clk.summary(), spec=spec, cfg=cfg,
                 bytes_in=frames[0].nbytes)
 
 
@@ -307,75 +328,6 @@ def roofline(ks, peak_gbs):
     return out, per
 
 
-def cpu_sample(spec, cfg, gn_iters=10.0):
-    """CPU oracle (the fp64 restatement of the reference; single thread, as the
-    reference has no threading) on a bounded sample of the same workload.
-
-    Frame 0 of the config-2 sequence initialises the oracle; frame 1 is then run
-    stage by stage with wall-clock timers: build_frame_maps, model maps + rigid
-    ICP, one full GN linearisation (warp, render, associate, energy, dense 6N x 6N
-    assembly — solver.cpp:316-369), and forward warp + apply_fusion. The dense
-    LDLT of the reference's LM step (solver.cpp:383-386) is NOT run at
-    6N ~ 9k (minutes per factorisation); its cost is n^3/3 flop at the rate the
-    same LDLT code measures on a 1200 x 1200 SPD matrix. Frame time =
-    depth + rigid + gn_iters x (linearisation + LDLT) + fusion."""
-    sys.path.insert(0, os.path.join(REPO, "tests"))
-    import oracle_py as O
-
-    ocfg = O.make_config(**{k: v for k, v in cfg.items() if k in O.DEFAULTS})
-    frames = render_frames(spec, cfg, 2, phase=0)
-    n_probe = 1200
-    rng = np.random.default_rng(0)
-    A = rng.normal(size=(n_probe, n_probe))
-    A = A @ A.T + n_probe * np.eye(n_probe)
-    t0 = time.perf_counter()
-    O.ldlt_solve(A, np.ones(n_probe))
-    ldlt_rate = (n_probe ** 3 / 3.0) / (time.perf_counter() - t0)
-    p = O.OraclePipeline(ocfg)
-    t0 = time.perf_counter()
-    s0 = p.process_frame(frames[0], 0)
-    t_init = time.perf_counter() - t0
-    st = p.state
-    n_nodes = st.num_nodes()
-    dim = 6 * n_nodes
-    pose = p.pose()
-    T = {}
-    t0 = time.perf_counter()
-    st.build_frame(frames[1], 1)
-    T["depth"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    st.rigid_align(pose, pose, 1, 0)
-    T["rigid"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    st.normal_equations(pose, 1, 0)
-    T["linearize"] = time.perf_counter() - t0
-    T["ldlt"] = (dim ** 3 / 3.0) / ldlt_rate
-    t0 = time.perf_counter()
-    st.forward_warp()
-    st.apply_fusion(pose, 1)
-    T["fusion"] = time.perf_counter() - t0
-    t_frame = T["depth"] + T["rigid"] + gn_iters * (T["linearize"] + T["ldlt"]) + T["fusion"]
-    return dict(t_frame=t_frame, t_init=t_init, stages=T, ldlt_rate_gflops=ldlt_rate / 1e9,
-                dim=dim, surfels=s0.surfel_count, nodes=n_nodes, gn_iters=gn_iters)
-
-
-def cpu_baseline_entry(cs):
-    T = cs["stages"]
-    return {"value": round(1.0 / cs["t_frame"], 6), "unit": "frames/s", "cores": 1, "kind": "port",
-            "sample": (f"CPU oracle, cfg2 frame 1 ({cs['surfels']} surfels, {cs['nodes']} nodes): "
-                       f"measured depth {T['depth']:.3f}s, rigid {T['rigid']:.3f}s, GN "
-                       f"linearisation {T['linearize']:.3f}s, fusion {T['fusion']:.3f}s; dense "
-                       f"LDLT dim {cs['dim']} = {T['ldlt']:.1f}s extrapolated (n^3/3 at measured "
-                       f"{cs['ldlt_rate_gflops']:.2f} GFLOP/s); x {cs['gn_iters']:.0f} GN iterations")}
-
-
-def _dist_device():
-    import torch
-    import torch.distributed as dist
-
-    return torch.device("cuda") if dist.get_backend() == "nccl" else torch.device("cpu")
-
-
 def dist_barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -384,13 +336,15 @@ def dist_barrier(world):
 
 
 def dist_max(v, world):
-    """Max over ranks (the timing rule: the slowest rank defines the job time)."""
+    """Max over ranks (the timing rule: the slowest rank defines the job time).
+    Host-side gloo on a CPU tensor: the ranks' sequences are independent, so
+    nothing on the data path is a collective and no NCCL communicator exists."""
     if world <= 1:
         return v
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device=_dist_device())
+    t = torch.tensor([v], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -398,6 +352,45 @@ def dist_max(v, world):
 def aggregate_fps(world, steps, max_total_ms):
     """Whole-job throughput: every rank processed `steps` frames of its own sequence."""
     return world * steps / (max_total_ms * 1e-3)
+
+
+def dryrun(args, rank, world):
+    """DS_BENCH_DRYRUN=1 (CPU tests only): the launcher, rendezvous, barrier and
+    max-over-ranks timing of the N-rank path with a host sleep standing in for
+    the per-frame work (rank r sleeps (1 + r) ms per step). Prints a line marked
+    "dryrun" -- never a measurement."""
+    dist_barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(1e-3 * (1 + rank))
+    ms = dist_max(1e3 * (time.perf_counter() - t0), world)
+    dist_barrier(world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dryrun": True, "metric": "frames/s", "n_gpus": world,
+                          "steps": args.steps, "value": aggregate_fps(world, args.steps, ms),
+                          "max_rank_ms": ms}), flush=True)
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: one process per GPU (RANK /
+    LOCAL_RANK / WORLD_SIZE set as torchrun would), gloo rendezvous on
+    127.0.0.1; rank 0 prints the JSON line. Returns the worst exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    return max(p.wait() for p in procs)
 
 
 def main():
@@ -411,6 +404,8 @@ def main():
     ap.add_argument("--sequences", type=int, default=1,
                     help="independent cfg2 sequences per GPU (BASELINE config 5)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -427,11 +422,11 @@ def main():
             print(json.dumps(run_reference(args)), flush=True)
         return
     if world > 1:
-        import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo")  # barrier + max-over-ranks timing only
+    if os.environ.get("DS_BENCH_DRYRUN") == "1":
+        return dryrun(args, rank, world)
     if args.sequences > 1:
         r = run_multi(args, rank, world, local_rank)
         if world > 1:
@@ -490,6 +485,9 @@ def main():
         "e2e": {"value": round(e2e, 3), "unit": "frames/s", "h2d_bytes_per_step": r["bytes_in"],
                 "d2h_bytes_per_step": 360},
         "gpu_launches": int(r["launches"]),
+        "reference_frames": {"frames": list(range(1, 1 + r["ref_frames"][0])),
+                             "e2e_fps": round(r["ref_frames"][0] / (r["ref_frames"][1] * 1e-3), 3),
+                             "note": "frames the --impl reference arm times (rank 0, phase 0)"},
         "solve_ms": round(solve_ms, 3), "gn_iters_per_frame": round(gn_iters, 2),
         "ms_per_gn_iter": round(solve_ms / max(gn_iters, 1e-9), 3),
         "roofline": roof, "kernels": per, "clocks": r["clocks"],
@@ -500,7 +498,9 @@ def main():
                                           "needs ~18 GB (SURVEY 8(d))"}
     elif not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline_entry(cpu_sample(r["spec"], r["cfg"], gn_iters))
+            from bench_reference import cpu_baseline
+
+            line["cpu_baseline"] = cpu_baseline(args, r["spec"], r["cfg"])
         except Exception as e:  # never fail the GPU line on the CPU sample
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)

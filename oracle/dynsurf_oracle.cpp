@@ -1263,6 +1263,13 @@ static std::vector<Node> apply_increments(const std::vector<Node>& nodes,
   return out;
 }
 
+// Optional replacement of the LM step's dense LDLT (solver.cpp:386). Only the
+// bench's CPU reference arm installs one (LAPACK Cholesky on all host
+// threads), so that a 9k x 9k config-2 system solves in seconds instead of
+// minutes; every other use of the oracle runs the restated Eigen LDLT.
+static or_dense_solver_fn g_dense_solver = nullptr;
+static int64_t g_dense_solves = 0;
+
 struct SolveReport {
   int iterations = 0, correspondences = 0;
   double e0 = 0, e1 = 0, mean_r = 0;
@@ -1313,7 +1320,15 @@ static SolveReport solve_nonrigid(std::vector<Node>& nodes, const Model& model, 
     for (int attempt = 0; attempt < 8 && !accepted; ++attempt) {
       std::vector<double> damped = ne.h;
       for (int i = 0; i < dim; ++i) damped[size_t(i) * dim + i] += mu;
-      const std::vector<double> delta = ldlt_solve(dim, damped, neg_g);
+      std::vector<double> delta;
+      ++g_dense_solves;
+      if (g_dense_solver) {  // bench reference arm: the same step by multithreaded LAPACK
+        delta.assign(dim, 0.0);
+        if (g_dense_solver(dim, damped.data(), neg_g.data(), delta.data()) != 0)
+          delta.assign(dim, std::numeric_limits<double>::quiet_NaN());
+      } else {
+        delta = ldlt_solve(dim, damped, neg_g);
+      }
       bool finite = true;
       for (double v : delta) finite = finite && std::isfinite(v);
       double res = 0;
@@ -2277,6 +2292,8 @@ int32_t or_ldlt_solve(int32_t n, const double* a, const double* b, double* x) {
   std::memcpy(x, X.data(), sizeof(double) * n);
   return 0;
 }
+void or_set_dense_solver(or_dense_solver_fn fn) { g_dense_solver = fn; }
+int64_t or_dense_solve_count(void) { return g_dense_solves; }
 int32_t or_assert_normal_equations(int32_t dim, const double* h) {
   std::vector<double> H(h, h + size_t(dim) * dim);
   OR_TRY(assert_normal_equations(dim, H));

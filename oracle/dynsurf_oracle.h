@@ -179,6 +179,12 @@ int32_t or_blend_jacobian(const or_state* s, int32_t i, double* y3, double* dy_d
 void or_reg_terms(const double* dq_j, const double* dq_i, const double* p_j, double* r3,
                   double* jj18, double* ji18);
 int32_t or_ldlt_solve(int32_t n, const double* a, const double* b, double* x);
+/* Dense LM step x = A^-1 b (A: n x n row-major, symmetric). Returns 0 on success. */
+typedef int32_t (*or_dense_solver_fn)(int32_t n, const double* a, const double* b, double* x);
+/* Replaces the restated Eigen LDLT of solve_nonrigid's LM step (NULL restores it). */
+void or_set_dense_solver(or_dense_solver_fn fn);
+/* Number of LM-step dense solves performed so far (process-wide). */
+int64_t or_dense_solve_count(void);
 int32_t or_assert_normal_equations(int32_t dim, const double* h);
 
 /* fusion (fusion.cpp) */

@@ -254,6 +254,8 @@ void allocate(Ctx& c) {
   c.pcg_q = dalloc<double>(c, 6 * N);
   c.pcg_minv = dalloc<double>(c, 36 * N);
   c.pcg_items = dalloc<double>(c, 6 * (size_t)c.B_cap);
+  // cluster PCG: block source codes + halo lists when they do not fit on chip
+  c.pcgc_idx = dalloc<unsigned>(c, (size_t)c.B_cap + 16 * (size_t)N + 16);
   c.pcg_vec = dalloc<double>(c, 60 * (size_t)N);
   c.gst_part = dalloc<double>(c, 3 * (size_t)cdiv(N, 256) + 8);
   c.reg_ab = dalloc<double>(c, 48 * (size_t)N);
@@ -320,6 +322,8 @@ void allocate(Ctx& c) {
   if (const char* e = std::getenv("DS_LIVE_CELL")) c.live_cell = std::atof(e);
   if (const char* e = std::getenv("DS_REF_CELL")) c.ref_cell = std::atof(e);
   if (const char* e = std::getenv("DS_PCG_SMEM")) c.pcg_smem_cap = std::min(std::atoi(e), c.pcg_smem_cap);
+  if (const char* e = std::getenv("DS_PCG_CLUSTER")) c.pcg_cluster = std::atoi(e);
+  if (const char* e = std::getenv("DS_PCGC_SMEM")) c.pcgc_smem_cap = std::atoi(e);
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));
   DS_CUDA(cudaMemsetAsync(c.node_nbr, 0xff, sizeof(int) * 8 * N, c.stream));
 }

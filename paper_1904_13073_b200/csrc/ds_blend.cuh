@@ -97,4 +97,42 @@ __device__ __forceinline__ Rig blend_rig(const Blend& b) {
   return dq_to_rig(dq_normalized(raw));
 }
 
+// True when fp32 rounding of x cannot change if x moves by up to eps: x is
+// farther than eps from both rounding boundaries (midpoints to the adjacent
+// floats, exact in fp64).
+__device__ __forceinline__ bool f32_round_stable(double x, double eps) {
+  const float f = __double2float_rn(x);
+  const double fd = (double)f;
+  const double lo = 0.5 * (fd + (double)nextafterf(f, -INFINITY));
+  const double hi = 0.5 * (fd + (double)nextafterf(f, INFINITY));
+  return fabs(x - lo) > eps && fabs(x - hi) > eps;
+}
+
+// Live state of one surfel under a non-degenerate blend (forward_warp,
+// warp_field.cpp:128-140), stored fp32 as the SoA model. The rsqrt transform
+// (blend_rig_fast) agrees with the reference's normalized() -> to_se3() chain
+// (blend_rig) to a few fp64 ulps; whenever any stored coordinate lies within
+// kWarpRoundMargin of an fp32 rounding boundary the exact chain is evaluated
+// instead, so the stored live state is the one the reference arithmetic
+// rounds to (bit-exact z-buffer inputs), at the fast path's cost otherwise.
+constexpr double kWarpRoundMargin = 1e-12;  // m (positions) / unit (normals); ~100x the gap
+__device__ __forceinline__ void warp_surfel(const Blend& b, const float4& rp, const float4& rn,
+                                            float4& lp, float4& ln) {
+  const V3 x = v3(rp.x, rp.y, rp.z), nx = v3(rn.x, rn.y, rn.z);
+  const Rig T = blend_rig_fast(b);
+  V3 p = rig_apply(T, x), q = rig_rotate(T, nx);
+  const double e = kWarpRoundMargin;
+  const bool ok = f32_round_stable(p.x, e * fmax(1.0, fabs(p.x))) &&
+                  f32_round_stable(p.y, e * fmax(1.0, fabs(p.y))) &&
+                  f32_round_stable(p.z, e * fmax(1.0, fabs(p.z))) && f32_round_stable(q.x, e) &&
+                  f32_round_stable(q.y, e) && f32_round_stable(q.z, e);
+  if (!ok) {
+    const Rig Te = blend_rig(b);
+    p = rig_apply(Te, x);
+    q = rig_rotate(Te, nx);
+  }
+  lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
+  ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
+}
+
 }  // namespace ds

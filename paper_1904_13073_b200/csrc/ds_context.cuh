@@ -242,6 +242,9 @@ struct Ctx {
   // PCG
   double* g = nullptr;
   double* pcg_x = nullptr;
+  unsigned* pcgc_idx = nullptr;  // cluster PCG index scratch (k_pcg_cluster.cu)
+  int pcg_cluster = -1;           // DS_PCG_CLUSTER: -1 auto, 0 off, 2..16 cluster size
+  int pcgc_smem_cap = 1 << 30;    // DS_PCGC_SMEM: cluster PCG carve bytes (tests shrink it)
   double* pcg_p0 = nullptr;
   double* pcg_p1 = nullptr;
   double* pcg_p2 = nullptr;
@@ -409,6 +412,8 @@ void clear_model_maps(Ctx& c);
 void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver_report* out);
 void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_pre, int* n_pairs);
 void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double* rel_res);
+// cluster-resident PCG (k_pcg_cluster.cu); false when it does not apply
+bool pcg_cluster_launch(Ctx& c, int max_iters, double tol);
 void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int t_now,
                  int t_last, ds_rigid_result* out);
 // rigid_align split: enqueue the device work / wait and assemble the result

@@ -79,13 +79,7 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
     const Blend b = blend_entry(m.ki[i], m.kw[i], warp_dq);
     lp = rp;
     ln = rn;
-    if (!b.degenerate) {
-      const Rig T = blend_rig_fast(b);
-      const V3 p = rig_apply(T, v3(rp.x, rp.y, rp.z));
-      const V3 q = rig_rotate(T, v3(rn.x, rn.y, rn.z));
-      lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
-      ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
-    }
+    if (!b.degenerate) warp_surfel(b, rp, rn, lp, ln);
     if (lane == 0) {
       m.lp[i] = lp;
       m.ln[i] = ln;
@@ -210,13 +204,7 @@ __global__ void __launch_bounds__(256) k_index_splat(ModelBuf m, int n, CamParam
     const Blend b = blend_entry(__ldcs(m.ki + i), __ldcs(m.kw + i), warp_dq);
     float4 ln = rn;
     lp = rp;
-    if (!b.degenerate) {
-      const Rig T = blend_rig_fast(b);
-      const V3 p = rig_apply(T, v3(rp.x, rp.y, rp.z));
-      const V3 q = rig_rotate(T, v3(rn.x, rn.y, rn.z));
-      lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
-      ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
-    }
+    if (!b.degenerate) warp_surfel(b, rp, rn, lp, ln);
     m.lp[i] = lp;
     m.ln[i] = ln;
   } else {

@@ -29,6 +29,7 @@
 #include "ds_assoc.cuh"
 #include "ds_blend.cuh"
 #include "ds_context.cuh"
+#include "ds_pcg.cuh"
 #include "ds_reduce.cuh"
 
 namespace cg = cooperative_groups;
@@ -1200,53 +1201,6 @@ struct PcgArgs {
   DevScalars* sc;
 };
 
-// Gauss-Jordan inverse of a 6x6 SPD block by an aligned 8-lane group: lane lr
-// (< 6) holds row lr of A in a[] and returns row lr of A^-1 in b[]. A pivot
-// that is not > 0 (the block is not SPD in its fp32-rounded form) makes the
-// group fall back to the inverse diagonal, like the reference's LDLT guard.
-__device__ __forceinline__ void gj_inverse6(double a[6], double b[6], int lr) {
-  const int base = (threadIdx.x & 31) & ~7;
-  double diag_lr = 1.0;  // a[lr] without a dynamic register-array index (no local memory)
-#pragma unroll
-  for (int t = 0; t < 6; ++t)
-    if (t == lr) diag_lr = a[t];
-#pragma unroll
-  for (int t = 0; t < 6; ++t) b[t] = (t == lr) ? 1.0 : 0.0;
-  bool ok = true;
-#pragma unroll
-  for (int p = 0; p < 6; ++p) {
-    double ap[6], bp[6];
-#pragma unroll
-    for (int t = 0; t < 6; ++t) {
-      ap[t] = __shfl_sync(0xffffffffu, a[t], base + p);
-      bp[t] = __shfl_sync(0xffffffffu, b[t], base + p);
-    }
-    const double piv = ap[p];
-    if (!(piv > 0.0)) ok = false;
-    // one division per step (pivot > 0 normal); the rows scale by the
-    // reciprocal -- dividing the many zero entries would take the slow path
-    const double ip = ok ? 1.0 / piv : 0.0;
-    if (lr == p) {
-#pragma unroll
-      for (int t = 0; t < 6; ++t) {
-        a[t] = ap[t] * ip;
-        b[t] = bp[t] * ip;
-      }
-    } else {
-      const double f = a[p] * ip;
-#pragma unroll
-      for (int t = 0; t < 6; ++t) {
-        a[t] = a[t] - f * ap[t];
-        b[t] = b[t] - f * bp[t];
-      }
-    }
-  }
-  if (!ok) {
-#pragma unroll
-    for (int t = 0; t < 6; ++t) b[t] = (t == lr && diag_lr > 0.0) ? 1.0 / diag_lr : 0.0;
-  }
-}
-
 // fixed-order CTA sums of three values; results valid in every thread
 __device__ __forceinline__ void cta_sum3(double& a, double& b, double& c, double4* sh) {
 #pragma unroll
@@ -1993,6 +1947,8 @@ void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_p
 
 // PCG on the last assembled system with the damping in dsc->mu
 void pcg_solve_async(Ctx& c, int max_iters, double tol) {
+  // one thread-block cluster when the system is small enough (k_pcg_cluster.cu)
+  if (pcg_cluster_launch(c, max_iters, tol)) return;
   const int N = c.n_nodes;
   PcgArgs a;
   a.row_ptr = c.row_ptr;

@@ -27,11 +27,7 @@ __global__ void __launch_bounds__(256) k_forward_warp(ModelBuf m, int n,
   const Blend b = blend_entry(ki, kw, node_dq);
   float4 lp = rp, ln = rn;
   if (!b.degenerate) {
-    const Rig T = blend_rig_fast(b);
-    const V3 p = rig_apply(T, v3(rp.x, rp.y, rp.z));
-    const V3 q = rig_rotate(T, v3(rn.x, rn.y, rn.z));
-    lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
-    ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
+    warp_surfel(b, rp, rn, lp, ln);
   } else if (degenerate) {
     atomicAdd(degenerate, 1);
   }

@@ -114,11 +114,15 @@ def test_forward_warp_matches():
     model, _ = frame_model(cfg, seq.render_depth(0))
     ctx, st = _init_both(cfg, model)
     _random_field(ctx, st, np.random.default_rng(3))
+    # the device's fp32 skinning weights on both sides (mirror input)
+    st.set_model(Hh.device_to_oracle_model(ctx.download_model()))
     assert ctx.forward_warp() == st.forward_warp() == 0
     g, o = ctx.download_model(), st.get_model()
-    # fp64 arithmetic, fp32 store: <= 0.5 ulp(fp32) of |x| <~ 1.5 m
-    assert np.abs(g["live_pos"] - o["live_pos"]).max() < 2e-7
-    assert np.abs(g["live_nrm"] - o["live_nrm"]).max() < 2e-7
+    # fp64 arithmetic rounded to the fp32 store: the stored live state is the
+    # one the reference chain rounds to (ds_blend.cuh warp_surfel)
+    f32 = lambda a: np.asarray(a).astype(np.float32).astype(np.float64)  # noqa: E731
+    assert np.array_equal(g["live_pos"], f32(o["live_pos"]))
+    assert np.array_equal(g["live_nrm"], f32(o["live_nrm"]))
     ctx.close()
 
 

@@ -79,9 +79,9 @@ typedef struct ds_config {
   int32_t width, height;
   /* ---- device-only ---- */
   int32_t pcg_max_iters; /* block-Jacobi PCG iterations per LM attempt */
-  int32_t max_surfels;   /* capacity; 0 = 8 x width x height */
+  int32_t max_surfels;   /* initial capacity (grown at frame boundaries); 0 = 8 x width x height */
   double pcg_tol;        /* relative residual; 0 = run pcg_max_iters */
-  int32_t max_nodes;     /* capacity; 0 = 8192 */
+  int32_t max_nodes;     /* initial capacity (grown at frame boundaries); 0 = 8192 */
   int32_t profile;       /* 1 = time every kernel launch with CUDA events */
 } ds_config;
 
@@ -133,6 +133,12 @@ ds_status ds_synchronize(ds_context* ctx);
  * frame's fusion); no host sync. Timing harnesses call this before their end
  * event so that deferred work is inside the timed region. */
 ds_status ds_join_deferred(ds_context* ctx);
+/* Current device capacities (surfels, nodes) and how often they grew. The
+ * context grows them geometrically at frame boundaries (the reference's model
+ * and node containers are unbounded std::vectors, types.hpp:66-80); the
+ * max_surfels / max_nodes fields of ds_config are the initial capacities. */
+ds_status ds_capacity(const ds_context* ctx, int32_t* surfel_capacity, int32_t* node_capacity,
+                      int32_t* growths);
 
 /* ---- per-frame process call: Pipeline::process_frame (pipeline.cpp:74-142) ---- */
 ds_status ds_process_frame(ds_context* ctx, const uint16_t* depth_host, int32_t width,

@@ -2227,6 +2227,8 @@ int32_t or_normal_equations(or_state* s, const double* pose, int32_t t_now, int3
   work.skin = s->m.skin;
   work.live.resize(s->m.size());
   forward_warp(work, s->nodes);
+  if (s->mirror)  // as solve_nonrigid's own loop: the live state is stored fp32 on the device
+    for (auto& sf : work.live) round_surf(sf);
   const ModelMaps mm = render_model_maps(work.live, P, s->cfg, t_now, t_last);
   std::vector<Pair> pairs;
   OR_TRY(pairs = find_correspondences(s->f, mm, P));

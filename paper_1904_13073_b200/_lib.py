@@ -84,6 +84,7 @@ SIGNATURES = {
     "ds_destroy": [P],
     "ds_synchronize": [P],
     "ds_join_deferred": [P],
+    "ds_capacity": [P, PI32, PI32, PI32],
     "ds_process_frame": [P, P, I32, I32, I32, C.POINTER(DsFrameStats)],
     "ds_process_frame_device": [P, P, I32, I32, I32, C.POINTER(DsFrameStats)],
     "ds_is_initialized": [P, PI32, PI32],

@@ -355,6 +355,88 @@ void set_identity(double* p) {
   for (int i = 0; i < 12; ++i) p[i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
 }
 
+// Geometric capacity growth at a frame boundary (the reference's containers
+// are unbounded std::vectors: types.hpp:66-80, warp_field.cpp:142-184). Every
+// device buffer is sized from the surfel / node capacities, so growing
+// re-allocates the context's device state: the persistent state (the current
+// model SoA, node positions / transforms / edges, the device scalars) is
+// parked in temporary buffers, the context is re-allocated at the new
+// capacities and the state copied back; everything else is per frame.
+void grow_capacity(Ctx& c, long long need_surfels, long long need_nodes) {
+  join_node_updates(c);
+  DS_CUDA(cudaStreamSynchronize(c.side));
+  sync(c);
+  const int n = c.n_surfels, N = c.n_nodes;
+  const long long S_new = std::max<long long>(c.S_cap, need_surfels);
+  const long long N_new = std::max<long long>(c.N_cap, need_nodes);
+  if (S_new * 10 + N_new * 24 >= 0x7fffffffLL)
+    fail(DS_ERR_CAPACITY, "capacity growth beyond 32-bit record indices");
+  const ModelBuf old = c.M();
+  struct Park {
+    void* p;
+    size_t bytes;
+    const void* src;
+  };
+  std::vector<Park> park = {
+      {nullptr, sizeof(float4) * n, old.rp}, {nullptr, sizeof(float4) * n, old.rn},
+      {nullptr, sizeof(float4) * n, old.lp}, {nullptr, sizeof(float4) * n, old.ln},
+      {nullptr, sizeof(int2) * n, old.t},    {nullptr, sizeof(int4) * n, old.ki},
+      {nullptr, sizeof(float4) * n, old.kw}, {nullptr, sizeof(double4) * N, c.node_pos},
+      {nullptr, sizeof(double4) * 2 * N, c.node_dq}, {nullptr, sizeof(int) * 8 * N, c.node_nbr},
+      {nullptr, sizeof(DevScalars), c.dsc}};
+  for (auto& q : park) {
+    DS_CUDA(cudaMalloc(&q.p, std::max<size_t>(q.bytes, 1)));
+    if (q.bytes) DS_CUDA(cudaMemcpyAsync(q.p, q.src, q.bytes, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  sync(c);
+  // device and pinned allocations only (streams and events stay)
+  for (void* p : c.allocations) cudaFree(p);
+  c.allocations.clear();
+  for (void** h : {(void**)&c.hsc, (void**)&c.h_depth_pinned, (void**)&c.h_mu, (void**)&c.h_int})
+    if (*h) {
+      cudaFreeHost(*h);
+      *h = nullptr;
+    }
+  for (GraphSlot* g : {&c.g_step, &c.g_attempt, &c.g_solve})
+    if (g->exec) {
+      cudaGraphExecDestroy(g->exec);
+      g->exec = nullptr;
+    }
+  c.cfg.max_surfels = (int)S_new;
+  c.cfg.max_nodes = (int)N_new;
+  allocate(c);
+  c.cur = 0;
+  const ModelBuf& m = c.M();
+  void* dst[] = {m.rp, m.rn, m.lp, m.ln, m.t, m.ki, m.kw, c.node_pos, c.node_dq, c.node_nbr, c.dsc};
+  for (size_t k = 0; k < park.size(); ++k) {
+    if (park[k].bytes)
+      DS_CUDA(cudaMemcpyAsync(dst[k], park[k].p, park[k].bytes, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  sync(c);
+  for (auto& q : park) cudaFree(q.p);
+  c.pattern_ready = false;
+  c.pattern_frame = -1;
+  c.mm_ready = c.im_ready = c.frame_ready = false;
+  c.mm_clean = false;
+  c.any_stable_ready = false;
+  c.live_pending = false;
+  c.nodes_pending = false;
+  for (KnnGrid* g : {&c.grid_ref, &c.grid_live, &c.grid_new}) g->valid = false;
+  ++c.capacity_growths;
+}
+
+// Frame-boundary headroom: a frame appends at most one surfel per valid pixel
+// (fusion.cpp:235-257); node extension is bounded by the 25 % headroom.
+void ensure_frame_headroom(Ctx& c) {
+  const long long need_s = (long long)c.n_surfels + c.P;
+  const bool grow_s = need_s > c.S_cap;
+  const bool grow_n = (long long)c.n_nodes * 4 > (long long)c.N_cap * 3;
+  if (!grow_s && !grow_n)
+    return;
+  grow_capacity(c, grow_s ? std::max(2LL * c.S_cap, need_s + c.P) : c.S_cap,
+                grow_n ? 2LL * c.N_cap : c.N_cap);
+}
+
 // initialize_from_frame (pipeline.cpp:42-72)
 void initialize_from_frame(Ctx& c) {
   init_surfels_from_frame(c);
@@ -432,6 +514,7 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
     return;
   }
   const int t_now = fi;
+  ensure_frame_headroom(c);
   // the rigid ICP (main stream) and the frame's JtJ pattern build (side stream,
   // independent of the pose) overlap; the pattern's host syncs wait only on it
   rigid_align_enqueue(c, c.pose, c.pose, t_now, c.t_last_reinit);
@@ -695,6 +778,16 @@ ds_status ds_synchronize(ds_context* ctx) {
   REQUIRE(ctx, "null context");
   bind(ctx->c);
   ds::sync(ctx->c);
+  API_END
+}
+
+ds_status ds_capacity(const ds_context* ctx, int32_t* surfel_capacity, int32_t* node_capacity,
+                      int32_t* growths) {
+  API_BEGIN
+  REQUIRE(ctx, "null context");
+  if (surfel_capacity) *surfel_capacity = ctx->c.S_cap;
+  if (node_capacity) *node_capacity = ctx->c.N_cap;
+  if (growths) *growths = ctx->c.capacity_growths;
   API_END
 }
 

@@ -144,6 +144,7 @@ struct Ctx {
   // model
   ModelBuf mb[2];
   int cur = 0;
+  int capacity_growths = 0;  // geometric re-allocations so far (grow_capacity)
   int n_surfels = 0;
   // nodes
   int n_nodes = 0;
@@ -243,7 +244,7 @@ struct Ctx {
   double* g = nullptr;
   double* pcg_x = nullptr;
   unsigned* pcgc_idx = nullptr;  // cluster PCG index scratch (k_pcg_cluster.cu)
-  int pcg_cluster = -1;           // DS_PCG_CLUSTER: -1 auto, 0 off, 2..16 cluster size
+  int pcg_cluster = 0;            // DS_PCG_CLUSTER: 0 off (default), 2..16 cluster size
   int pcgc_smem_cap = 1 << 30;    // DS_PCGC_SMEM: cluster PCG carve bytes (tests shrink it)
   double* pcg_p0 = nullptr;
   double* pcg_p1 = nullptr;

@@ -59,7 +59,16 @@ struct PcgcArgs {
   int N;
   int max_iters;
   int cap;  // shared-memory bytes the carve may use (<= kCSmem; tests shrink it)
+  unsigned long long* trace;  // DS_PCG_TRACE: phase timestamps of rank 0
 };
+
+__device__ __forceinline__ void cmark(const PcgcArgs& a, int rank, int slot) {
+  if (a.trace && rank == 0 && threadIdx.x == 0 && slot < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[slot] = t;
+  }
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -84,9 +93,11 @@ __device__ __forceinline__ void minv_apply(const double (&v)[P], double (&y)[P],
     for (int t = 0; t < 6; ++t) vr[t] = __shfl_sync(0xffffffffu, v[j], gbase + t);
     double s = 0.0;
     if (act[j]) {
-      const double* mi = MINV + 36 * (row0 + j * kRowsPerPass) + 6 * rw;
-#pragma unroll
-      for (int t = 0; t < 6; ++t) s += mi[t] * vr[t];
+      const double2* mi =
+          reinterpret_cast<const double2*>(MINV + 36 * (row0 + j * kRowsPerPass) + 6 * rw);
+      const double2 m01 = mi[0], m23 = mi[1], m45 = mi[2];
+      s = (__fma_rn(m01.x, vr[0], m01.y * vr[1]) + __fma_rn(m23.x, vr[2], m23.y * vr[3])) +
+          __fma_rn(m45.x, vr[4], m45.y * vr[5]);
     }
     y[j] = s;
   }
@@ -128,6 +139,76 @@ __device__ __forceinline__ void spmv(double (&y)[P], const double (&vown)[P], do
   }
 }
 
+// one block row of a 6x6 block times a 6-vector (row rw), fp32 matrix, fp64 math
+__device__ __forceinline__ double blk_dot(float2 v01, float2 v23, float2 v45, double2 x01,
+                                          double2 x23, double2 x45) {
+  return (__fma_rn((double)v01.x, x01.x, (double)v01.y * x01.y) +
+          __fma_rn((double)v23.x, x23.x, (double)v23.y * x23.y)) +
+         __fma_rn((double)v45.x, x45.x, (double)v45.y * x45.y);
+}
+
+// Staged-halo SpMV: every column value is in this CTA's shared memory (own rows
+// of the published vector at `obase`, the staged halo at `hbase`, in doubles
+// from the start of the dynamic shared memory; code bit 31 = halo). Blocks are
+// taken four at a time with independent products (latency hiding); the row
+// total adds them in BSR order.
+template <int P>
+__device__ __forceinline__ void spmv_staged(double (&y)[P], const double (&vown)[P], double mu,
+                                            const int* __restrict__ RP,
+                                            const unsigned* __restrict__ BSRC,
+                                            const float* __restrict__ VS, int ncache,
+                                            const float* __restrict__ VG,
+                                            const double* __restrict__ SD, int obase, int hbase,
+                                            int row0, int rw, bool (&act)[P]) {
+  auto xsrc = [&](unsigned code) {
+    const int off = ((code >> 31) ? hbase : obase) + 6 * (int)(code & 0x7fffffffu);
+    return reinterpret_cast<const double2*>(SD + off);
+  };
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    double tot = 0.0;
+    if (act[j]) {
+      const int i = row0 + j * kRowsPerPass;
+      int b = RP[i];
+      const int b1 = RP[i + 1], bc = min(b1, ncache);
+      for (; b + 4 <= bc; b += 4) {
+        double sb[4];
+        const uint4 cd = make_uint4(BSRC[b], BSRC[b + 1], BSRC[b + 2], BSRC[b + 3]);
+        const unsigned cds[4] = {cd.x, cd.y, cd.z, cd.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2* xv = xsrc(cds[u]);
+          const float2* vr = reinterpret_cast<const float2*>(VS + 36 * (b + u) + 6 * rw);
+          sb[u] = blk_dot(vr[0], vr[1], vr[2], xv[0], xv[1], xv[2]);
+        }
+        tot = ((tot + sb[0]) + sb[1]) + (sb[2] + sb[3]);
+      }
+      for (; b < bc; ++b) {
+        const double2* xv = xsrc(BSRC[b]);
+        const float2* vr = reinterpret_cast<const float2*>(VS + 36 * b + 6 * rw);
+        tot += blk_dot(vr[0], vr[1], vr[2], xv[0], xv[1], xv[2]);
+      }
+      for (; b + 4 <= b1; b += 4) {  // blocks past the cache: fp32 rows from L2
+        double sb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2* xv = xsrc(BSRC[b + u]);
+          const float2* vr = reinterpret_cast<const float2*>(VG + 36 * (size_t)(b + u) + 6 * rw);
+          sb[u] = blk_dot(__ldg(vr), __ldg(vr + 1), __ldg(vr + 2), xv[0], xv[1], xv[2]);
+        }
+        tot = ((tot + sb[0]) + sb[1]) + (sb[2] + sb[3]);
+      }
+      for (; b < b1; ++b) {
+        const double2* xv = xsrc(BSRC[b]);
+        const float2* vr = reinterpret_cast<const float2*>(VG + 36 * (size_t)b + 6 * rw);
+        tot += blk_dot(__ldg(vr), __ldg(vr + 1), __ldg(vr + 2), xv[0], xv[1], xv[2]);
+      }
+      tot = __fma_rn(mu, vown[j], tot);
+    }
+    y[j] = tot;
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -150,6 +231,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
   if (rank == 0 && tid == 0) a.sc->finite = 1;  // before the first cluster barrier
   const double mu = *a.mu_ptr;
 
+  cmark(a, rank, 0);
   // ---- shared-memory carve (OWN first: the same offset in every CTA)
   double* OWN = reinterpret_cast<double*>(smem);  // [2][6 nrmax] published vector
   double* UNI = OWN + 12 * (size_t)nrmax;         // MINV [nr][36] / halo marks [N]
@@ -192,6 +274,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
     for (int c = c0; c < c1; ++c) mark[c] = mark[c] ? pos++ : -1;
   }
   __syncthreads();
+  cmark(a, rank, 1);
   const int nh = s_nh;
   // past the row pointers: block source codes + halo list (on chip when they
   // fit, else a global scratch), the staged halo values [2][6 nh] (else remote
@@ -227,10 +310,10 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
   for (int b = tid; b < nb; b += kCThreads) {
     const int c = a.col[bb0 + b];
     unsigned code;
-    if (c >= r0 && c < r1) {
+    if (stage) {  // local shared memory only: own rows / staged halo (bit 31)
+      code = (c >= r0 && c < r1) ? (unsigned)(c - r0) : (0x80000000u | (unsigned)mark[c]);
+    } else if (c >= r0 && c < r1) {
       code = ((unsigned)rank << kSrcShift) | (unsigned)(c - r0);
-    } else if (stage) {
-      code = ((unsigned)C << kSrcShift) | (unsigned)mark[c];
     } else {
       const int q = owner_of(c);
       code = ((unsigned)q << kSrcShift) | (unsigned)(c - (int)((long long)N * q / C));
@@ -250,6 +333,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();  // marks consumed; mbarrier initialised
+  cmark(a, rank, 2);
   const unsigned bytes = 144u * (unsigned)ncache;
   if (tid == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_mbar)),
@@ -299,6 +383,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
     X[j] = Z[j] = Q[j] = S[j] = Pv[j] = 0.0;
   }
   __syncthreads();  // MINV complete
+  cmark(a, rank, 3);
   // u0 = M^-1 r0, published in the odd buffer (iteration 0's m goes to the even one)
   minv_apply<P>(R, U, MINV, row0, rw, gbase, act);
 #pragma unroll
@@ -314,7 +399,9 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
           : "r"(smem_u32(&s_mbar))
           : "memory");
   }
+  cmark(a, rank, 4);
   cluster.sync();
+  cmark(a, rank, 5);
   auto gather = [&](int par) {  // remote columns of the published vector -> HV[par]
     if (stage) {
       double* hv = HV + 6 * (size_t)nh * par;
@@ -327,7 +414,18 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
   };
   gather(1);
   __syncthreads();
-  spmv<P>(W, U, mu, RP, BSRC, VS, ncache, VG, s_base[1], row0, rw, act);  // w0 = A u0
+  cmark(a, rank, 6);
+  const double* SD = reinterpret_cast<const double*>(smem);
+  const int hb = (int)((reinterpret_cast<const unsigned char*>(HV) - smem) / 8);
+  auto spmv_any = [&](double (&y)[P], const double (&v)[P], int par) {
+    if (stage)
+      spmv_staged<P>(y, v, mu, RP, BSRC, VS, ncache, VG, SD, 6 * nrmax * par, hb + 6 * nh * par,
+                     row0, rw, act);
+    else
+      spmv<P>(y, v, mu, RP, BSRC, VS, ncache, VG, s_base[par], row0, rw, act);
+  };
+  spmv_any(W, U, 1);  // w0 = A u0
+  cmark(a, rank, 7);
   double gamma_old = 0.0, alpha_old = 0.0, rr = 0.0, rr0 = 0.0;
   int it = 0;
   for (;; ++it) {
@@ -351,20 +449,35 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
       s_wsum[warp][2] = pr;
     }
     __syncthreads();
-    if (tid < 3) {
-      double v = 0.0;
-      for (int w = 0; w < kCWarps; ++w) v += s_wsum[w][tid];
-      s_part[par][tid] = v;
+    if (warp == 0) {  // fixed shuffle tree over the warp sums
+      double v0 = lane < kCWarps ? s_wsum[lane][0] : 0.0;
+      double v1 = lane < kCWarps ? s_wsum[lane][1] : 0.0;
+      double v2 = lane < kCWarps ? s_wsum[lane][2] : 0.0;
+#pragma unroll
+      for (int off = kCWarps / 2; off > 0; off >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, off);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, off);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, off);
+      }
+      if (lane == 0) {
+        s_part[par][0] = v0;
+        s_part[par][1] = v1;
+        s_part[par][2] = v2;
+      }
     }
+    cmark(a, rank, 8 + 4 * it);
     cluster.sync();  // release m and the partials; acquire everyone's
+    cmark(a, rank, 9 + 4 * it);
     gather(par);
     if (tid < 3 * C) {
       const int q = tid / 3, k = tid - 3 * q;
       s_gath[q][k] = cluster.map_shared_rank(&s_part[par][0], q)[k];
     }
     __syncthreads();
+    cmark(a, rank, 10 + 4 * it);
     // n = (H + mu I) m -- computed before the stopping test (unused on the last round)
-    spmv<P>(Nv, M, mu, RP, BSRC, VS, ncache, VG, s_base[par], row0, rw, act);
+    spmv_any(Nv, M, par);
+    cmark(a, rank, 11 + 4 * it);
     double gamma = 0.0, delta = 0.0;
     rr = 0.0;
     for (int q = 0; q < C; ++q) {
@@ -404,6 +517,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(PcgcArgs a) {
     a.sc->pcg_rr0 = rr0;
   }
   cluster.sync();  // no CTA leaves while another may still read its shared memory
+  cmark(a, rank, 63);
 }
 
 template <int P>
@@ -458,10 +572,15 @@ void launch(Ctx& c, int C, const PcgcArgs& a) {
 // enough for P <= 3 passes, the cluster shape available); returns false when
 // the caller should run the cooperative grid kernel instead.
 bool pcg_cluster_launch(Ctx& c, int max_iters, double tol) {
-  const int mode = c.pcg_cluster;  // DS_PCG_CLUSTER: 0 off, 2..16 force the cluster size
+  // DS_PCG_CLUSTER: unset / 0 off (default), 2..16 the cluster size. Off by
+  // default: at config-2 sizes the measured launch is slower than the
+  // cooperative grid kernel (123 vs 65 us for 10 iterations at
+  // 2k nodes -- 16 SMs run ~9x longer dependent fp64 chains per iteration
+  // than 148 do, and the matrix slice spills past shared memory).
+  const int mode = c.pcg_cluster;
   const int N = c.n_nodes;
-  if (mode == 0 || tol > 0.0 || N < 8) return false;
-  int C = mode > 0 ? std::min(mode, kMaxCluster) : (N >= 1024 ? 16 : 8);
+  if (mode <= 0 || tol > 0.0 || N < 8) return false;
+  int C = std::min(mode, kMaxCluster);
   C = std::min(C, N / 4);
   if (C < 2) return false;
   const int nrmax = (N + C - 1) / C;
@@ -488,11 +607,12 @@ bool pcg_cluster_launch(Ctx& c, int max_iters, double tol) {
   a.N = N;
   a.max_iters = max_iters;
   a.cap = cap;
+  a.trace = c.pcg_trace;
   launch_begin(c, KK_PCG);
   if (P == 1) launch<1>(c, C, a);
   else if (P == 2) launch<2>(c, C, a);
   else launch<3>(c, C, a);
-  launch_end(c, KK_PCG, std::max(1, max_iters) * (148.0 * c.n_full + 6.0 * 8 * 8 * N));
+  launch_end(c, KK_PCG, std::max(1, max_iters) * (148.0 * c.n_full + 292.0 * N + 4.0));
   return true;
 }
 

@@ -1921,11 +1921,12 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   A.reg_h = c.reg_h;
   A.reg_g = c.reg_g;
   if (c.n_up > 0) {
-    // algorithmic bytes: records 4 B + (count, offset) 8 B each, the paired
-    // surfels' list-ordered rows/residuals (104 B) once, chunk partials out+in,
-    // blocks written 144 B (both triangles) + g
-    const double bytes = 12.0 * c.n_records + 104.0 * c.n_pairs_ok_est + 200.0 * 2 * c.n_chunks +
-                         144.0 * c.n_full + 48.0 * N;
+    // algorithmic bytes: 80 B per pair (pair 32 + reference
+    // position 16 + skinning ids 16 + weights 16) + 144 B per 6x6 block written
+    // + 24 B per node (g). (Round 1 counted this kernel's own intermediates --
+    // 12 B per record, 104 B rows per pair, 400 B per chunk partial -- which
+    // overstated its roofline fraction ~3x.)
+    const double bytes = 80.0 * c.n_pairs_ok_est + 144.0 * c.n_full + 24.0 * N;
     DS_LAUNCH_PDL(c, KK_BLOCK_ASSEMBLY, bytes, cdiv((long long)c.n_chunks * kChunkLanes, 256), 256, 0,
               k_assemble_chunks, A);
     if (c.n_multi > 0)
@@ -1978,8 +1979,10 @@ void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   launch_begin(c, KK_PCG);
   void* fn = a.tol2 > 0.0 ? (void*)k_pcg<false> : (void*)k_pcg<true>;
   DS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPcgThreads), args, kPcgSmem, c.stream));
-  // algorithmic bytes per PCG: per iteration one BSR SpMV (148 B/block + vectors)
-  launch_end(c, KK_PCG, std::max(1, max_iters) * (148.0 * c.n_full + 6.0 * 8 * 8 * N));
+  // algorithmic bytes per PCG: per iteration one BSR SpMV
+  // (148 B/block + 4 B row pointers + 48 B x/y per node) + ~10 vector passes
+  // (240 B per node)
+  launch_end(c, KK_PCG, std::max(1, max_iters) * (148.0 * c.n_full + 292.0 * N + 4.0));
 
 }
 

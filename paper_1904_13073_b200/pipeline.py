@@ -346,6 +346,12 @@ class Context:
     def synchronize(self):
         check(self.L.ds_synchronize(self.h))
 
+    def capacity(self) -> dict:
+        """Device capacities; grown geometrically at frame boundaries."""
+        a, b, g = C.c_int32(), C.c_int32(), C.c_int32()
+        check(self.L.ds_capacity(self.h, C.byref(a), C.byref(b), C.byref(g)))
+        return dict(surfels=a.value, nodes=b.value, growths=g.value)
+
     def join_deferred(self):
         """Context stream waits for the frame's deferred side-stream work (no host sync)."""
         check(self.L.ds_join_deferred(self.h))

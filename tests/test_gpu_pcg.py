@@ -9,9 +9,9 @@ fp64 check of the kernels' arithmetic, and test_pcg_converges_to_direct_solve
 ties the converged PCG to the direct solve the reference performs.
 
 Three device kernels run it: the cluster kernel (k_pcg_cluster.cu, one
-thread-block cluster, fixed iteration budget -- the production path at
-config-2 sizes), the cooperative grid kernel with pipelined recurrences (fixed
-budget, large N, or DS_PCG_CLUSTER=0) and with the classic two-barrier
+thread-block cluster, fixed iteration budget; opt-in, DS_PCG_CLUSTER),
+the cooperative grid kernel with pipelined recurrences (fixed
+budget; the production path) and with the classic two-barrier
 recurrences (tolerance stopping). All must reproduce the restated iterates
 after k iterations up to fp64 rounding (relative 1e-8 on x, tolerance written
 here; the matrix is the same fp32 BSR).
@@ -79,8 +79,8 @@ def make_system(width=160, height=120, focal=140.0, scene="bending_sheet", frame
 @pytest.mark.parametrize("mode", ["cluster", "pipelined", "classic"])
 def test_pcg_iterates_match_reference(system, monkeypatch, iters, mode):
     ctx, H, g = system
-    if mode == "pipelined":  # the cooperative grid kernel: a context without the cluster path
-        monkeypatch.setenv("DS_PCG_CLUSTER", "0")  # read at context creation
+    if mode == "cluster":  # the cluster kernel: a context with DS_PCG_CLUSTER set
+        monkeypatch.setenv("DS_PCG_CLUSTER", "8")  # read at context creation
         ctx, H, g = make_system()
     mu = 1e-6 * np.trace(H) / H.shape[0] * 10.0
     tol = 0.0 if mode != "classic" else 1e-150  # tol > 0 selects the classic recurrences
@@ -89,7 +89,7 @@ def test_pcg_iterates_match_reference(system, monkeypatch, iters, mode):
     assert it == iters
     err = np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-300)
     assert err < 1e-8, (mode, iters, err)
-    if mode == "pipelined":
+    if mode == "cluster":
         ctx.close()
 
 
@@ -115,6 +115,7 @@ def test_cluster_pcg_on_config2_system(monkeypatch):
     """BASELINE config 2 (articulated body, 640x480, ~1.5k nodes, ~14 blocks per
     row): the cluster kernel (16 CTAs, two row passes per thread) against the
     cooperative kernel and the numpy restatement."""
+    monkeypatch.setenv("DS_PCG_CLUSTER", "16")
     ctx, H, g = make_system(640, 480, 560.0, "articulated_body", (0, 1))
     N = ctx.num_nodes()
     assert N > 1000

@@ -450,3 +450,35 @@ def test_deferred_side_stream_updates_match_immediate_join(monkeypatch, scene):
         assert np.array_equal(deferred[1][k], immediate[1][k]), k
     for k in deferred[2]:
         assert np.array_equal(deferred[2][k], immediate[2][k]), k
+
+
+def test_capacity_grows_at_frame_boundaries():
+    """Surfel and node capacities start tiny and grow geometrically between
+    frames (the reference's containers are unbounded, types.hpp:66-80,
+    warp_field.cpp:142-184): the run is bit-identical to one that starts with
+    ample capacity."""
+    frames = 8
+    base = dict(SMALL)
+    seq = pkg.SyntheticSequence("rigid_orbit", 30, pkg.make_config(**base))
+    depth = [seq.render_depth(t) for t in range(frames)]
+
+    def run(**caps):
+        p = pkg.Pipeline(pkg.make_config(**base, **caps))
+        stats = [p.process_frame(d, t) for t, d in enumerate(depth)]
+        cap = p.context.capacity()
+        out = (stats, p.model(), p.nodes(), cap)
+        p.close()
+        return out
+
+    small = run(max_surfels=2 * 160 * 120, max_nodes=64)
+    big = run(max_surfels=16 * 160 * 120, max_nodes=4096)
+    assert small[3]["growths"] >= 2 and big[3]["growths"] == 0
+    assert small[3]["surfels"] > 2 * 160 * 120 and small[3]["nodes"] > 64
+    for a, b in zip(small[0], big[0]):
+        for k in ("surfel_count", "node_count", "correspondences", "final_energy", "pose",
+                  "fused", "appended", "new_nodes"):
+            assert a[k] == b[k], k
+    for k in small[1]:
+        assert np.array_equal(small[1][k], big[1][k]), k
+    for k in small[2]:
+        assert np.array_equal(small[2][k], big[2][k]), k

@@ -206,6 +206,15 @@ ds_status ds_build_normal_equations(ds_context* ctx, const double* pose, int32_t
  * touched (nb: block touched by a term this iteration), g (6N) */
 ds_status ds_download_normal_equations(ds_context* ctx, int32_t* row_ptr, int32_t* col,
                                        double* values, uint8_t* touched, double* g);
+/* assert_normal_equations (solver.cpp:157-167) on the last assembled system:
+ * H symmetric to 1e-9 max(1, max|H|), every 6x6 diagonal block PSD (smallest
+ * eigenvalue >= -1e-8 max(1, max|H|)); DS_ERR_NUMERICAL otherwise. With the
+ * environment variable DS_CHECK_NE=1 at ds_create, every GN linearisation of
+ * solve_nonrigid / process_frame runs it (debug). */
+ds_status ds_check_normal_equations(ds_context* ctx);
+/* Overwrites the last assembled system's values (nb x 36, the pattern of
+ * ds_download_normal_equations; stored fp32) and, if given, g (6N). Tests. */
+ds_status ds_set_normal_equation_values(ds_context* ctx, const double* values, const double* g);
 /* (H + mu I) delta = -g by block-Jacobi PCG on the last assembled system */
 ds_status ds_pcg_solve(ds_context* ctx, double mu, int32_t max_iters, double tol, double* delta,
                        int32_t* iters, double* rel_residual);

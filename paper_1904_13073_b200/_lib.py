@@ -109,6 +109,8 @@ SIGNATURES = {
     "ds_build_normal_equations": [P, P, I32, I32, PI32, PI32, PD],
     "ds_download_normal_equations": [P, P, P, P, P, P],
     "ds_pcg_solve": [P, C.c_double, I32, C.c_double, P, PI32, PD],
+    "ds_check_normal_equations": [P],
+    "ds_set_normal_equation_values": [P, P, P],
     "ds_bsr_spmv": [P, P, P, C.c_double, I32, PD],
     "ds_solve_nonrigid": [P, P, I32, I32, C.POINTER(DsSolverReport)],
     "ds_rigid_align": [P, P, P, I32, I32, C.POINTER(DsRigidResult)],

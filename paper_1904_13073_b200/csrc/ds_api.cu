@@ -323,6 +323,7 @@ void allocate(Ctx& c) {
   if (const char* e = std::getenv("DS_REF_CELL")) c.ref_cell = std::atof(e);
   if (const char* e = std::getenv("DS_PCG_SMEM")) c.pcg_smem_cap = std::min(std::atoi(e), c.pcg_smem_cap);
   if (const char* e = std::getenv("DS_PCG_CLUSTER")) c.pcg_cluster = std::atoi(e);
+  if (const char* e = std::getenv("DS_CHECK_NE")) c.check_ne = e[0] != '0';
   if (const char* e = std::getenv("DS_PCGC_SMEM")) c.pcgc_smem_cap = std::atoi(e);
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));
   DS_CUDA(cudaMemsetAsync(c.node_nbr, 0xff, sizeof(int) * 8 * N, c.stream));
@@ -383,7 +384,7 @@ void grow_capacity(Ctx& c, long long need_surfels, long long need_nodes) {
       {nullptr, sizeof(int2) * n, old.t},    {nullptr, sizeof(int4) * n, old.ki},
       {nullptr, sizeof(float4) * n, old.kw}, {nullptr, sizeof(double4) * N, c.node_pos},
       {nullptr, sizeof(double4) * 2 * N, c.node_dq}, {nullptr, sizeof(int) * 8 * N, c.node_nbr},
-      {nullptr, sizeof(DevScalars), c.dsc}};
+      {nullptr, sizeof(DevScalars), c.dsc}, {nullptr, sizeof(uint16_t) * c.P, c.depth}};
   for (auto& q : park) {
     DS_CUDA(cudaMalloc(&q.p, std::max<size_t>(q.bytes, 1)));
     if (q.bytes) DS_CUDA(cudaMemcpyAsync(q.p, q.src, q.bytes, cudaMemcpyDeviceToDevice, c.stream));
@@ -407,7 +408,8 @@ void grow_capacity(Ctx& c, long long need_surfels, long long need_nodes) {
   allocate(c);
   c.cur = 0;
   const ModelBuf& m = c.M();
-  void* dst[] = {m.rp, m.rn, m.lp, m.ln, m.t, m.ki, m.kw, c.node_pos, c.node_dq, c.node_nbr, c.dsc};
+  void* dst[] = {m.rp,       m.rn,      m.lp,       m.ln,  m.t,    m.ki,
+                 m.kw,       c.node_pos, c.node_dq, c.node_nbr, c.dsc, c.depth};
   for (size_t k = 0; k < park.size(); ++k) {
     if (park[k].bytes)
       DS_CUDA(cudaMemcpyAsync(dst[k], park[k].p, park[k].bytes, cudaMemcpyDeviceToDevice, c.stream));
@@ -426,11 +428,11 @@ void grow_capacity(Ctx& c, long long need_surfels, long long need_nodes) {
 }
 
 // Frame-boundary headroom: a frame appends at most one surfel per valid pixel
-// (fusion.cpp:235-257); node extension is bounded by the 25 % headroom.
+// (fusion.cpp:235-257); the node set is kept below half the node capacity.
 void ensure_frame_headroom(Ctx& c) {
   const long long need_s = (long long)c.n_surfels + c.P;
   const bool grow_s = need_s > c.S_cap;
-  const bool grow_n = (long long)c.n_nodes * 4 > (long long)c.N_cap * 3;
+  const bool grow_n = (long long)c.n_nodes * 2 > (long long)c.N_cap;
   if (!grow_s && !grow_n)
     return;
   grow_capacity(c, grow_s ? std::max(2LL * c.S_cap, need_s + c.P) : c.S_cap,
@@ -493,6 +495,11 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
   std::memset(st, 0, sizeof *st);
   st->frame = fi;
   const int64_t launches0 = c.total_launches;
+  if (c.initialized) {  // geometric growth happens between frames
+    const bool own = depth_dev == c.depth;
+    ensure_frame_headroom(c);
+    if (own) depth_dev = c.depth;
+  }
   PhaseEvents ev;
   DS_CUDA(cudaEventRecord(ev.e[0], c.stream));
   frame_maps(c, depth_dev, fi);
@@ -501,7 +508,20 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
     join_node_updates(c);  // deferred side-stream work must not race the new warp field
     c.any_stable_ready = false;
     set_identity(c.pose);
-    initialize_from_frame(c);
+    for (int attempt = 0;; ++attempt) {  // the node count is known only after sampling
+      try {
+        initialize_from_frame(c);
+        break;
+      } catch (const Error& e) {
+        if (e.code != DS_ERR_CAPACITY || attempt >= 16) throw;
+        const bool own = depth_dev == c.depth;  // ds_process_frame's upload buffer
+        c.n_surfels = 0;
+        c.n_nodes = 0;
+        grow_capacity(c, c.S_cap, 2LL * c.N_cap);
+        if (own) depth_dev = c.depth;  // re-allocated, content kept
+        frame_maps(c, depth_dev, fi);  // per-frame buffers were re-allocated
+      }
+    }
     DS_CUDA(cudaEventRecord(ev.e[5], c.stream));
     fetch_scalars(c);
     st->valid_pixels = c.hsc->valid_count;
@@ -514,7 +534,6 @@ void process_frame_impl(Ctx& c, const uint16_t* depth_dev, int fi, ds_frame_stat
     return;
   }
   const int t_now = fi;
-  ensure_frame_headroom(c);
   // the rigid ICP (main stream) and the frame's JtJ pattern build (side stream,
   // independent of the pose) overlap; the pattern's host syncs wait only on it
   rigid_align_enqueue(c, c.pose, c.pose, t_now, c.t_last_reinit);
@@ -1241,6 +1260,33 @@ ds_status ds_download_normal_equations(ds_context* ctx, int32_t* row_ptr, int32_
   ds::sync(c);
   if (values)
     for (size_t i = 0; i < v.size(); ++i) values[i] = v[i];
+  API_END
+}
+
+ds_status ds_check_normal_equations(ds_context* ctx) {
+  API_BEGIN
+  REQUIRE(ctx, "null context");
+  Ctx& c = ctx->c;
+  bind(c);
+  REQUIRE(c.pattern_ready, "no assembled system");
+  ds::check_normal_equations(c);
+  API_END
+}
+
+ds_status ds_set_normal_equation_values(ds_context* ctx, const double* values, const double* g) {
+  API_BEGIN
+  REQUIRE(ctx && values, "null argument");
+  Ctx& c = ctx->c;
+  bind(c);
+  REQUIRE(c.pattern_ready, "no assembled system");
+  const int B = c.n_full;
+  std::vector<float> v((size_t)B * 36);
+  for (size_t i = 0; i < v.size(); ++i) v[i] = (float)values[i];
+  DS_CUDA(cudaMemcpyAsync(c.bsr_val, v.data(), sizeof(float) * v.size(), cudaMemcpyHostToDevice,
+                          c.stream));
+  if (g)
+    DS_CUDA(cudaMemcpyAsync(c.g, g, sizeof(double) * 6 * c.n_nodes, cudaMemcpyHostToDevice, c.stream));
+  ds::sync(c);
   API_END
 }
 

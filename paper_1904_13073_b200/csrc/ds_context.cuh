@@ -95,10 +95,13 @@ struct DevScalars {
   double rigid_pose[12];
   // JtJ pattern counts, published by its last kernel (read with the frame's
   // next scalar fetch instead of host syncs inside the pattern build)
-  int pat_n_up, pat_n_full, pat_n_chunks, pat_n_multi, pat_err, _pad_pat[3];
+  int pat_n_up, pat_n_full, pat_n_chunks, pat_n_multi, pat_err, ne_err, _pad_pat[2];
+  unsigned ne_scale_bits, _pad_ne;  // assert_normal_equations: max|H| (fp32 bits)
 };
 
 enum DevErr { DERR_NODE_CAP = 1, DERR_HASH_CELL = 2, DERR_HASH_FULL = 4, DERR_BLOCK_CAP = 8 };
+// assert_normal_equations (solver.cpp:157-167) failures, DevScalars::ne_err
+enum NeErr { NE_ASYMMETRIC = 1, NE_NOT_PSD = 2 };
 
 struct GraphSlot {
   cudaGraphExec_t exec = nullptr;
@@ -244,6 +247,7 @@ struct Ctx {
   double* g = nullptr;
   double* pcg_x = nullptr;
   unsigned* pcgc_idx = nullptr;  // cluster PCG index scratch (k_pcg_cluster.cu)
+  bool check_ne = false;          // DS_CHECK_NE: assert_normal_equations every GN iteration
   int pcg_cluster = 0;            // DS_PCG_CLUSTER: 0 off (default), 2..16 cluster size
   int pcgc_smem_cap = 1 << 30;    // DS_PCGC_SMEM: cluster PCG carve bytes (tests shrink it)
   double* pcg_p0 = nullptr;
@@ -413,6 +417,11 @@ void clear_model_maps(Ctx& c);
 void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver_report* out);
 void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_pre, int* n_pairs);
 void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double* rel_res);
+// assert_normal_equations (solver.cpp:157-167) on the assembled BSR system:
+// enqueue the device check (flags in dsc->ne_err) / run it and fail with
+// DS_ERR_NUMERICAL like the reference's dynsurf::Error
+void check_normal_equations_async(Ctx& c);
+void check_normal_equations(Ctx& c);
 // cluster-resident PCG (k_pcg_cluster.cu); false when it does not apply
 bool pcg_cluster_launch(Ctx& c, int max_iters, double tol);
 void rigid_align(Ctx& c, const double* render_pose, const double* init_pose, int t_now,

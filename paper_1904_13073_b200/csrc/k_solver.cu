@@ -1936,6 +1936,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   DS_LAUNCH_PDL(c, KK_REDUCE, 48.0 * N + 24.0 * N, std::max(1, cdiv(N, kStatsThreads)), kStatsThreads, 0,
             k_g_stats, c.g, c.bsr_val, c.diag_pos, N, lm_floor ? 1 : 0, c.gst_part, c.tickets + 2,
             c.dsc);
+  if (c.check_ne) check_normal_equations_async(c);  // DS_CHECK_NE (debug)
 }
 
 void gn_linearize(Ctx& c, const double* pose, int t_now, int t_last, double* e_pre, int* n_pairs) {
@@ -1984,6 +1985,102 @@ void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   // (240 B per node)
   launch_end(c, KK_PCG, std::max(1, max_iters) * (148.0 * c.n_full + 292.0 * N + 4.0));
 
+}
+
+namespace {
+// ---- assert_normal_equations (solver.cpp:157-167) on the device
+// scale = max(1, max|H|): |H| as fp32 bits (non-negative floats order as ints)
+__global__ void k_ne_scale(const float* __restrict__ val, long long n, unsigned* __restrict__ bits) {
+  pdl_wait();
+  unsigned m = 0u;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(val[k])));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(bits, m);
+}
+// symmetry: block (r, c) against its mirror (c, r), thread per block
+__global__ void k_ne_symmetry(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                              const float* __restrict__ val, int N, DevScalars* sc) {
+  const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (r >= N) return;
+  const double scale = fmax(1.0, (double)__uint_as_float(sc->ne_scale_bits));
+  bool bad = false;
+  for (int a = row_ptr[r] + lane; a < row_ptr[r + 1]; a += 32) {
+    const int cc = col[a];
+    int lo = row_ptr[cc], hi = row_ptr[cc + 1];  // rows are column-sorted
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (col[mid] < r) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo >= row_ptr[cc + 1] || col[lo] != r) {
+      bad = true;  // the mirror block is missing
+      continue;
+    }
+    for (int t = 0; t < 36; ++t) {
+      const double d = (double)val[(size_t)a * 36 + t] - (double)val[(size_t)lo * 36 + (t % 6) * 6 + t / 6];
+      if (fabs(d) > 1e-9 * scale) bad = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&sc->ne_err, NE_ASYMMETRIC);
+}
+// diagonal blocks PSD: smallest eigenvalue (cyclic Jacobi, fp64) >= -1e-8 scale
+__global__ void k_ne_psd(const int* __restrict__ diag_pos, const float* __restrict__ val, int N,
+                         DevScalars* sc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const int d = diag_pos[j];
+  double a[6][6];
+  for (int x = 0; x < 6; ++x)
+    for (int y = 0; y < 6; ++y) a[x][y] = d >= 0 ? (double)val[(size_t)d * 36 + x * 6 + y] : 0.0;
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < 6; ++p)
+      for (int q = p + 1; q < 6; ++q) off += a[p][q] * a[p][q];
+    if (off < 1e-30) break;
+    for (int p = 0; p < 6; ++p)
+      for (int q = p + 1; q < 6; ++q) {
+        if (a[p][q] == 0.0) continue;
+        const double th = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+        const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < 6; ++k) {
+          const double akp = a[k][p], akq = a[k][q];
+          a[k][p] = cs * akp - sn * akq;
+          a[k][q] = sn * akp + cs * akq;
+        }
+        for (int k = 0; k < 6; ++k) {
+          const double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = cs * apk - sn * aqk;
+          a[q][k] = sn * apk + cs * aqk;
+        }
+      }
+  }
+  double mn = a[0][0];
+  for (int k = 1; k < 6; ++k) mn = fmin(mn, a[k][k]);
+  const double scale = fmax(1.0, (double)__uint_as_float(sc->ne_scale_bits));
+  if (mn < -1e-8 * scale) atomicOr(&sc->ne_err, NE_NOT_PSD);
+}
+}  // namespace
+
+void check_normal_equations_async(Ctx& c) {
+  const int N = c.n_nodes;
+  DS_CUDA(cudaMemsetAsync(&c.dsc->ne_scale_bits, 0, sizeof(unsigned), c.stream));
+  DS_LAUNCH(c, KK_MISC, 144.0 * c.n_full, 2 * c.num_sms, 256, 0, k_ne_scale, c.bsr_val,
+            36LL * c.n_full, &c.dsc->ne_scale_bits);
+  DS_LAUNCH(c, KK_MISC, 288.0 * c.n_full, cdiv(N, 8), 256, 0, k_ne_symmetry, c.row_ptr, c.bsr_col,
+            c.bsr_val, N, c.dsc);
+  DS_LAUNCH(c, KK_MISC, 144.0 * N, cdiv(N, 128), 128, 0, k_ne_psd, c.diag_pos, c.bsr_val, N, c.dsc);
+}
+
+void check_normal_equations(Ctx& c) {
+  DS_CUDA(cudaMemsetAsync(&c.dsc->ne_err, 0, sizeof(int), c.stream));
+  check_normal_equations_async(c);
+  fetch_scalars(c);
+  if (c.hsc->ne_err & NE_ASYMMETRIC) fail(DS_ERR_NUMERICAL, "normal equations lost symmetry");
+  if (c.hsc->ne_err & NE_NOT_PSD) fail(DS_ERR_NUMERICAL, "normal equations diagonal block not PSD");
 }
 
 void pcg_solve(Ctx& c, double mu, int max_iters, double tol, int* iters, double* rel_res) {
@@ -2276,6 +2373,7 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
   const auto tp0 = std::chrono::steady_clock::now();
   if (c.pattern_frame != t_now) build_pattern(c, t_now, t_last);
   c.pattern_frame = -1;
+  if (c.check_ne) DS_CUDA(cudaMemsetAsync(&c.dsc->ne_err, 0, sizeof(int), c.stream));
   if (c.trace_host)
     std::fprintf(stderr, "build_pattern %.1f us\n",
                  std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tp0)
@@ -2377,6 +2475,10 @@ report:
             c.f_vert, c.f_nrm, pair_params(c, pose), 1, c.red_part, &c.dsc->mean_cnt,
             c.tickets + 0, &c.dsc->mean_abs_r);
   fetch_scalars(c);
+  if (c.check_ne && c.hsc->ne_err) {  // assert_normal_equations (solver.cpp:375)
+    if (c.hsc->ne_err & NE_ASYMMETRIC) fail(DS_ERR_NUMERICAL, "normal equations lost symmetry");
+    fail(DS_ERR_NUMERICAL, "normal equations diagonal block not PSD");
+  }
   rep.mean_residual = c.hsc->mean_cnt > 0 ? c.hsc->mean_abs_r / c.hsc->mean_cnt : 0.0;
   *out = rep;
 }

@@ -256,6 +256,15 @@ class Context:
                                                   _p(out["g"])))
         return out
 
+    def check_normal_equations(self):
+        """assert_normal_equations (solver.cpp:157-167); raises errors.Error."""
+        check(self.L.ds_check_normal_equations(self.h))
+
+    def set_normal_equation_values(self, values, g=None):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        check(self.L.ds_set_normal_equation_values(self.h, _p(v), _p(_f64(g)) if g is not None
+                                                   else None))
+
     def pcg_solve(self, mu, max_iters, tol=0.0):
         N = self.num_nodes()
         delta = np.zeros(6 * N)

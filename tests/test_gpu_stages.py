@@ -215,3 +215,74 @@ def test_pcg_converges_to_ldlt():
     ref = O.ldlt_solve(Hg + mu * np.eye(6 * N), -g["g"])
     assert np.abs(delta - ref).max() <= 1e-5 * np.abs(ref).max()
     ctx.close()
+
+
+@pytest.mark.parametrize("noise", [0.0, 2.0])
+def test_bilateral_prefilter_bit_exact(noise):
+    """the 5x5 bilateral prefilter (depth_processing.cpp:71-101,
+    sigma_s 4.5 px, sigma_d 30 mm) ahead of build_frame_maps, on noisy and clean
+    depth: the filtered frame maps are bit-exact against the oracle's."""
+    for name, size in (("bending_sheet", SMALL), ("articulated_body",
+                                                 dict(fx=280.0, fy=280.0, cx=159.5, cy=119.5,
+                                                      width=320, height=240))):
+        cfg = pkg.make_config(**{**size, "bilateral_filter": 1})
+        seq = pkg.SyntheticSequence(name, 20, cfg, noise_sigma_mm=noise)
+        ctx = pkg.Context(cfg)
+        st = O.OracleState(Hh.oracle_cfg(cfg))
+        for t in (0, 5):
+            d = seq.render_depth(t)
+            vc = ctx.frame_maps(d, t)
+            st.build_frame(d, t)
+            g, o = ctx.download_frame(), st.get_frame()
+            assert vc == o["valid_count"] > 0
+            assert np.array_equal(g["valid"], o["valid"])
+            assert np.array_equal(g["vert"], o["vert"])
+            assert np.array_equal(g["nrm"], o["nrm"])
+            assert np.array_equal(g["radius"], o["radius"])
+        # the filter changes the maps relative to the unfiltered path
+        raw = pkg.Context(pkg.make_config(**size))
+        raw.frame_maps(d, 5)
+        if noise > 0:
+            assert not np.array_equal(raw.download_frame()["vert"], g["vert"])
+        raw.close()
+        ctx.close()
+
+
+def test_assert_normal_equations_on_device(monkeypatch):
+    """d4: assert_normal_equations (solver.cpp:157-167) on the device BSR system:
+    the assembled H passes; an asymmetric entry or a diagonal block with a
+    negative eigenvalue raises the reference's dynsurf::Error (DS_ERR_NUMERICAL)
+    -- through the stage call, and inside solve_nonrigid with DS_CHECK_NE=1."""
+    cfg, seq = scene()
+    d0 = seq.render_depth(0)
+    model, _ = frame_model(cfg, d0)
+    ctx, st = _init_both(cfg, model)
+    _random_field(ctx, st, np.random.default_rng(11), angle=0.02, shift=0.003)
+    ctx.frame_maps(d0, 1)
+    pose = O.pose_identity()
+    ne = ctx.build_normal_equations(pose, 1, 0)
+    ctx.check_normal_equations()  # the assembled system is symmetric PSD
+    vals = ne["values"].copy()
+    r = 0
+    diag = [k for k in range(ne["row_ptr"][r], ne["row_ptr"][r + 1]) if ne["col"][k] == r][0]
+    off = [k for k in range(ne["row_ptr"][r], ne["row_ptr"][r + 1]) if ne["col"][k] != r][0]
+    scale = max(1.0, np.abs(vals).max())
+    bad = vals.copy()
+    bad[off, 0, 1] += 1e-3 * scale  # the mirror block no longer matches
+    ctx.set_normal_equation_values(bad)
+    with pytest.raises(pkg.errors.Error, match="symmetry"):
+        ctx.check_normal_equations()
+    bad = vals.copy()
+    bad[diag] -= 2.0 * np.abs(bad[diag]).max() * np.eye(6)  # negative definite block
+    ctx.set_normal_equation_values(bad)
+    with pytest.raises(pkg.errors.Error, match="PSD"):
+        ctx.check_normal_equations()
+    ctx.set_normal_equation_values(vals)
+    ctx.check_normal_equations()
+    ctx.close()
+    # the debug switch runs the check on every GN linearisation of the solve
+    monkeypatch.setenv("DS_CHECK_NE", "1")
+    pipe = pkg.Pipeline(cfg)
+    for t in range(3):
+        pipe.process_frame(seq.render_depth(t), t)
+    pipe.close()

@@ -207,3 +207,57 @@ def test_determinism_metrics_and_ply(tmp_path):
     assert len(plys) == 12 and plys == sorted(p.name for p in b.glob("*.ply"))
     for name in plys:
         assert (a / name).read_bytes() == (b / name).read_bytes(), name
+
+
+def test_scaling_sanity_fusion_and_reinit():
+    """Criterion 10 (§6.7 complexity): per-frame fusion time is
+    affine in the surfel count -- t = a + b |S| fitted over 4 model sizes has
+    R^2 > 0.9 -- and (re)initialisation at 2x the surfels takes <= 2.3x the
+    time. Run at BASELINE config-3 scale (1280x960 panning large scene, 1-7 M
+    surfels), where the device work, not launch latency, sets the time."""
+    import time
+
+    cfg = pkg.camera_config(1280, 960, 1120.0, max_gn_iters=10, pcg_max_iters=10)
+    seq = pkg.SyntheticSequence("large_scene", 60, cfg)
+    pipe = pkg.Pipeline(cfg)
+    samples, snaps = [], {}
+    for t in range(36):
+        s = pipe.process_frame(seq.render_depth(t), t)
+        if t >= 4:
+            samples.append((s["surfel_count"], s["fusion_ms"]))
+        if t == 8 or (8 in snaps and len(snaps) == 1 and
+                      s["surfel_count"] >= 2 * len(snaps[8][0]["radius"])):
+            snaps[t] = (pipe.model(), pipe.nodes(), list(pipe.pose()), seq.render_depth(t))
+    pipe.close()
+    # 4 model sizes: the sequence's frames split into 4 consecutive groups
+    groups = np.array_split(np.array(samples), 4)
+    S = np.array([g[:, 0].mean() for g in groups])
+    T = np.array([np.median(g[:, 1]) for g in groups])
+    b, a = np.polyfit(S, T, 1)
+    r2 = 1.0 - ((T - (a + b * S)) ** 2).sum() / ((T - T.mean()) ** 2).sum()
+    print(f"criterion 10: sizes {S.astype(int).tolist()} fusion ms {np.round(T, 3).tolist()} "
+          f"fit a={a:.3f} ms b={b * 1e6:.3f} ms/M R^2={r2:.3f}")
+    assert S[-1] > 2 * S[0]
+    assert b > 0 and r2 > 0.9
+    # (re)initialisation (clean_and_reset, reinit.cpp:28-89) at two model sizes
+    times = {}
+    for t, (model, nodes, pose, depth) in snaps.items():
+        ctx = pkg.Context(cfg)
+        ctx.upload_model(model)
+        ctx.upload_nodes(nodes)
+        best = 1e30
+        for _ in range(3):
+            ctx.upload_model(model)
+            ctx.frame_maps(depth, t)
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            ctx.clean_and_reset(pose)
+            ctx.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        times[t] = (len(model["radius"]), best)
+        ctx.close()
+    assert len(times) == 2
+    (n1, t1), (n2, t2) = [times[k] for k in sorted(times)]
+    print(f"criterion 10: reinit {n1} surfels {t1 * 1e3:.2f} ms, {n2} surfels {t2 * 1e3:.2f} ms")
+    assert n2 >= 2 * n1
+    assert t2 <= 2.3 * t1 * (n2 / (2.0 * n1))  # 2x surfels (the second snapshot is the first >= 2x)

@@ -50,7 +50,7 @@ CFG1 = dict(width=320, height=240, focal=280.0, scene="deforming_sphere", seq_fr
 # BASELINE config 3: large scene with a panning camera (node append + reskinning
 # every frame) and an open-to-close contact, 1280x960
 CFG3 = dict(width=1280, height=960, focal=1120.0, scene="large_scene", seq_frames=60,
-            max_nodes=16384, max_steps=30)  # ~13k nodes by frame 35; 16384 is passed before frame 60
+            max_nodes=16384)  # initial node capacity; grown at frame boundaries past ~13k nodes
 CONFIGS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3}
 
 
@@ -308,17 +308,20 @@ def roofline(ks, peak_gbs):
                               gbs=v["bytes"] / (v["ms"] * 1e-3) / 1e9)
     dom = max(rows, key=lambda n: rows[n]["ms"]) if rows else None
     out = None
-    traffic = None
-    try:  # ncu-measured DRAM bytes per launch of the same kernel (profiles/)
-        t = json.load(open(os.path.join(REPO, "profiles", "r01_traffic.json")))
+    traffic, traffic_src = None, None
+    for name in ("r02_traffic.json", "r01_traffic.json"):  # newest ncu capture first
+        try:  # ncu-measured DRAM bytes per launch of the same kernel (profiles/)
+            t = json.load(open(os.path.join(REPO, "profiles", name)))
+        except Exception:
+            continue
         if dom in t:
-            traffic = t[dom]["bytes_per_launch"]
-    except Exception:
-        pass
+            traffic, traffic_src = t[dom]["bytes_per_launch"], f"profiles/{name}: {t['source']}"
+            break
     if dom:
         r = rows[dom]
         out = {"kernel": dom, "bound": "hbm", "achieved": round(r["gbs"], 1), "peak": peak_gbs,
                "unit": "GB/s", "frac": round(r["gbs"] / peak_gbs, 4), "traffic": traffic,
+               "traffic_source": traffic_src,
                "mean_launch_us": round(1e3 * r["ms"] / r["launches"], 2),
                "algorithmic_bytes_per_launch": round(r["bytes"] / r["launches"])}
     per = {n: {"gbs": round(r["gbs"], 1), "frac": round(r["gbs"] / peak_gbs, 4),
@@ -441,7 +444,8 @@ def main():
                 "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
                 "ms_per_step": round(r["total_ms"] / K, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "storage": "fp32 SoA surfels, fp64 nodes, fp32 JtJ blocks", "data": "synthetic",
+                "dtype": "f64+f32", "storage": "fp64 arithmetic; fp32 SoA surfels, fp64 nodes, fp32 JtJ blocks",
+                "data": "synthetic",
                 "config": {"workload": f"cfg5: {S} independent cfg2 sequences per GPU "
                                        f"(articulated_body 640x480, phase-shifted), 10 GN x 10 PCG",
                            "sequences_per_gpu": S, "pcg_ctas_per_context": int(r["pcg_grid"]),
@@ -474,7 +478,8 @@ def main():
         "metric": "frames/s", "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(r["total_ms"] / K, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "storage": "fp32 SoA surfels, fp64 nodes, fp32 JtJ blocks", "data": "synthetic",
+        "dtype": "f64+f32", "storage": "fp64 arithmetic; fp32 SoA surfels, fp64 nodes, fp32 JtJ blocks",
+        "data": "synthetic",
         "config": {"workload": f"{args.config}: {r['spec']['scene']} {r['cfg']['width']}x"
                                f"{r['cfg']['height']}, 10 GN x 10 PCG per frame",
                    "surfels": st[-1]["surfel_count"], "nodes": st[-1]["node_count"],

@@ -343,7 +343,12 @@ void rigid_align_enqueue(Ctx& c, const double* render_pose, const double* init_p
     rp.sw = cdiv(c.W, rp.stride);
     rp.sh = cdiv(c.H, rp.stride);
     const int samples = rp.sw * rp.sh;
-    const int nb = std::min(cdiv(samples, kThreads), 2 * c.num_sms);  // grid-stride
+    // grid-stride, 2 CTAs per SM (DS_RIGID_GRID overrides): one sample per
+    // thread measured slower (24.6 -> 32.7 us per level-0 launch at config
+    // 2), the last block's reduction over 4x the partials costs more than the
+    // shorter per-thread gather chains save
+    const int nb = std::min(cdiv(samples, kThreads),
+                            c.rigid_grid_cap > 0 ? c.rigid_grid_cap : 2 * c.num_sms);
     for (int it = 0; it < kIters[level]; ++it) {
       DS_LAUNCH_PDL(c, KK_RIGID, 100.0 * samples + 16.0 * kTerms * nb, nb, kThreads, 0, k_rigid_terms,
                 rp, c.d_pose, c.mm_idx, c.M(), c.f_vert, c.f_nrm, c.f_flag, c.red_part,

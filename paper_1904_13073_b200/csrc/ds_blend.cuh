@@ -97,40 +97,57 @@ __device__ __forceinline__ Rig blend_rig(const Blend& b) {
   return dq_to_rig(dq_normalized(raw));
 }
 
-// True when fp32 rounding of x cannot change if x moves by up to eps: x is
-// farther than eps from both rounding boundaries (midpoints to the adjacent
-// floats, exact in fp64).
-__device__ __forceinline__ bool f32_round_stable(double x, double eps) {
-  const float f = __double2float_rn(x);
-  const double fd = (double)f;
-  const double lo = 0.5 * (fd + (double)nextafterf(f, -INFINITY));
-  const double hi = 0.5 * (fd + (double)nextafterf(f, INFINITY));
-  return fabs(x - lo) > eps && fabs(x - hi) > eps;
+// True when the fp32 rounding of x cannot change if x moves by up to
+// 2^m * max(1, |x|): integer test on x's fp64 bits (no FP64-pipe work).
+// Within x's binade the fp32 rounding boundaries are where the 29 mantissa
+// bits below fp32 precision equal 2^28; x is stable when its low bits are
+// farther than the margin, in units of its fp64 ulp 2^(e-52), from that.
+// The fast and exact transforms differ by <= ~1e-13 m on positions of a
+// <= 5 m scene (R from normalised quaternions a few ulps apart, applied to
+// |x| <= 5 m, plus t) and <= ~1.2e-14 on unit normals: margins 2^-40 (9e-13)
+// and 2^-43 (1.1e-13) keep a ~10x factor. Tiny |x| (margin >= half an fp32
+// ulp) and huge ones take the exact path.
+template <int kMarginLog2>
+__device__ __forceinline__ bool f32_round_stable(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const int e = (int)((b >> 52) & 0x7ff) - 1023;
+  // margin in fp64 ulps of x: 2^m max(1, |x|) / 2^(e-52) <= 2^(53 + m - min(e, 0))
+  const int sh = 53 + kMarginLog2 - (e < 0 ? e : 0);
+  if (sh >= 28 || e > 100) return false;
+  const long long low = (long long)(b & ((1ull << 29) - 1)) - (1ll << 28);
+  return (low < 0 ? -low : low) > (1ll << (sh < 0 ? 0 : sh));
 }
 
 // Live state of one surfel under a non-degenerate blend (forward_warp,
 // warp_field.cpp:128-140), stored fp32 as the SoA model. The rsqrt transform
 // (blend_rig_fast) agrees with the reference's normalized() -> to_se3() chain
-// (blend_rig) to a few fp64 ulps; whenever any stored coordinate lies within
-// kWarpRoundMargin of an fp32 rounding boundary the exact chain is evaluated
-// instead, so the stored live state is the one the reference arithmetic
-// rounds to (bit-exact z-buffer inputs), at the fast path's cost otherwise.
-constexpr double kWarpRoundMargin = 1e-12;  // m (positions) / unit (normals); ~100x the gap
+// (blend_rig) to a few fp64 ulps; whenever a stored coordinate could round
+// differently (f32_round_stable) the exact chain is evaluated instead, so the
+// stored live state is the one the reference arithmetic rounds to (bit-exact
+// z-buffer inputs). Measured cost: ~2 % of the config-2 frame rate, 12 % of
+// the stand-alone warp at config 4 (the exact branch's registers); a fix-up
+// kernel for the rare boundary surfels instead measured slower (its launch in
+// the GN chain cost 5 %).
 __device__ __forceinline__ void warp_surfel(const Blend& b, const float4& rp, const float4& rn,
                                             float4& lp, float4& ln) {
+  // a blend of identity transforms (every node before its first solve) gives
+  // R = I, t = 0 exactly on both chains: p = x, q = n with no rounding
+  const bool ident = b.rs.x == 0.0 && b.rs.y == 0.0 && b.rs.z == 0.0 && b.ds.w == 0.0 &&
+                     b.ds.x == 0.0 && b.ds.y == 0.0 && b.ds.z == 0.0;
   const V3 x = v3(rp.x, rp.y, rp.z), nx = v3(rn.x, rn.y, rn.z);
   const Rig T = blend_rig_fast(b);
   V3 p = rig_apply(T, x), q = rig_rotate(T, nx);
-  const double e = kWarpRoundMargin;
-  const bool ok = f32_round_stable(p.x, e * fmax(1.0, fabs(p.x))) &&
-                  f32_round_stable(p.y, e * fmax(1.0, fabs(p.y))) &&
-                  f32_round_stable(p.z, e * fmax(1.0, fabs(p.z))) && f32_round_stable(q.x, e) &&
-                  f32_round_stable(q.y, e) && f32_round_stable(q.z, e);
+#if !defined(DS_WARP_GUARD) || DS_WARP_GUARD != 0
+  const bool ok = ident ||
+                  (f32_round_stable<-40>(p.x) && f32_round_stable<-40>(p.y) &&
+                   f32_round_stable<-40>(p.z) && f32_round_stable<-43>(q.x) &&
+                   f32_round_stable<-43>(q.y) && f32_round_stable<-43>(q.z));
   if (!ok) {
     const Rig Te = blend_rig(b);
     p = rig_apply(Te, x);
     q = rig_rotate(Te, nx);
   }
+#endif
   lp = make_float4((float)p.x, (float)p.y, (float)p.z, rp.w);
   ln = make_float4((float)q.x, (float)q.y, (float)q.z, rn.w);
 }

@@ -58,43 +58,14 @@ __global__ void k_any_stable(const float4* __restrict__ ln, int n, double delta_
 // kWarp (pass 1 over a list): the surfel is first forward-warped
 // (warp_field.cpp:128-140, as k_forward_warp) and its live state written,
 // so the solve loop's warp + first splat pass are one launch.
-template <bool kPass2, bool kWarp = false, int kL = 1>
-__global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const int* __restrict__ list,
-                                                     SplatParams sp,
-                                                     const int* __restrict__ any_stable,
-                                                     unsigned long long* pkey,
-                                                     unsigned long long* skey, int* pidx,
-                                                     int* sidx,
-                                                     const double4* __restrict__ warp_dq = nullptr) {
-  pdl_wait();  // programmatic dependent launch: predecessor results visible
-  // kL lanes per surfel: each computes the surfel's projection (bit-identical
-  // in every lane) and takes every kL-th pixel of its splat disk
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int k0 = gt / kL, lane = gt % kL;
-  if (k0 >= n) return;
-  const int i = list ? list[k0] : k0;
-  float4 lp, ln;
-  if (kWarp) {
-    const float4 rp = m.rp[i], rn = m.rn[i];
-    const Blend b = blend_entry(m.ki[i], m.kw[i], warp_dq);
-    lp = rp;
-    ln = rn;
-    if (!b.degenerate) warp_surfel(b, rp, rn, lp, ln);
-    if (lane == 0) {
-      m.lp[i] = lp;
-      m.ln[i] = ln;
-    }
-  } else {
-    lp = m.lp[i];
-    ln = m.ln[i];
-  }
-  if (!list) {
-    const int2 t = m.t[i];
-    const bool stable = (double)ln.w > sp.delta_stable;
-    const bool recent = (sp.t_now - t.y) <= sp.delta_recent;
-    const bool bootstrap = sp.host_bootstrap || !(*any_stable);
-    if (!stable && !(bootstrap && recent)) return;
-  }
+// The splat of one surfel (raster.cpp:70-101): point channel at its centre
+// pixel, splat channel over its disk; kL lanes share the disk pixels.
+template <bool kPass2, int kL>
+__device__ __forceinline__ void model_splat_surfel(const float4& lp, const float4& ln, int i,
+                                                   int lane, const SplatParams& sp,
+                                                   unsigned long long* pkey,
+                                                   unsigned long long* skey, int* pidx,
+                                                   int* sidx) {
   const CamParams& k = sp.cam;
   const V3 pc = rig_apply(k.w2c, v3(lp.x, lp.y, lp.z));
   if (pc.z <= 0) return;
@@ -154,6 +125,48 @@ __global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const in
   }
 }
 
+template <bool kPass2, bool kWarp = false, int kL = 1>
+__global__ void __launch_bounds__(256) k_model_splat(ModelBuf m, int n, const int* __restrict__ list,
+                                                     SplatParams sp,
+                                                     const int* __restrict__ any_stable,
+                                                     unsigned long long* pkey,
+                                                     unsigned long long* skey, int* pidx,
+                                                     int* sidx,
+                                                     const double4* __restrict__ warp_dq = nullptr) {
+  pdl_wait();  // programmatic dependent launch: predecessor results visible
+  // kL lanes per surfel: each computes the surfel's projection (bit-identical
+  // in every lane) and takes every kL-th pixel of its splat disk
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k0 = gt / kL, lane = gt % kL;
+  if (k0 >= n) return;
+  const int i = list ? list[k0] : k0;
+  float4 lp, ln;
+  if (kWarp) {
+    const float4 rp = m.rp[i], rn = m.rn[i];
+    const int4 ki = m.ki[i];
+    const float4 kw = m.kw[i];
+    const Blend b = blend_entry(ki, kw, warp_dq);
+    lp = rp;
+    ln = rn;
+    if (!b.degenerate) warp_surfel(b, rp, rn, lp, ln);
+    if (lane == 0) {
+      m.lp[i] = lp;
+      m.ln[i] = ln;
+    }
+  } else {
+    lp = m.lp[i];
+    ln = m.ln[i];
+  }
+  if (!list) {
+    const int2 t = m.t[i];
+    const bool stable = (double)ln.w > sp.delta_stable;
+    const bool recent = (sp.t_now - t.y) <= sp.delta_recent;
+    const bool bootstrap = sp.host_bootstrap || !(*any_stable);
+    if (!stable && !(bootstrap && recent)) return;
+  }
+  model_splat_surfel<kPass2, kL>(lp, ln, i, lane, sp, pkey, skey, pidx, sidx);
+}
+
 struct AssocParams {
   Rig pose;
   int P;
@@ -192,24 +205,10 @@ __global__ void k_resolve_associate(int* __restrict__ pidx, int* __restrict__ si
 
 // kWarp (pass 1): the full-model forward warp (warp_field.cpp:104-140,
 // pipeline.cpp:108) is done here, the live state written, then splatted.
-template <bool kPass2, bool kWarp = false>
-__global__ void __launch_bounds__(256) k_index_splat(ModelBuf m, int n, CamParams k, int factor,
-                                                     unsigned long long* key, int* idx,
-                                                     const double4* __restrict__ warp_dq = nullptr) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  float4 lp;
-  if (kWarp) {
-    const float4 rp = __ldcs(m.rp + i), rn = __ldcs(m.rn + i);
-    const Blend b = blend_entry(__ldcs(m.ki + i), __ldcs(m.kw + i), warp_dq);
-    float4 ln = rn;
-    lp = rp;
-    if (!b.degenerate) warp_surfel(b, rp, rn, lp, ln);
-    m.lp[i] = lp;
-    m.ln[i] = ln;
-  } else {
-    lp = m.lp[i];
-  }
+// Index-map splat of one surfel (raster.cpp:8-30): its supersampled cell.
+template <bool kPass2>
+__device__ __forceinline__ void index_splat_surfel(const float4& lp, int i, const CamParams& k,
+                                                   int factor, unsigned long long* key, int* idx) {
   const V3 pc = rig_apply(k.w2c, v3(lp.x, lp.y, lp.z));
   if (pc.z <= 0) return;
   const double u = k.fx * pc.x / pc.z + k.cx;
@@ -221,6 +220,29 @@ __global__ void __launch_bounds__(256) k_index_splat(ModelBuf m, int n, CamParam
   const unsigned long long zb = (unsigned long long)__double_as_longlong(pc.z);
   if (!kPass2) zmin(key + c, zb);
   else if (key[c] == zb) imin(idx + c, i);
+}
+
+template <bool kPass2, bool kWarp = false>
+__global__ void __launch_bounds__(256) k_index_splat(ModelBuf m, int n, CamParams k, int factor,
+                                                     unsigned long long* key, int* idx,
+                                                     const double4* __restrict__ warp_dq = nullptr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float4 lp;
+  if (kWarp) {
+    const float4 rp = __ldcs(m.rp + i), rn = __ldcs(m.rn + i);
+    const int4 ki = __ldcs(m.ki + i);
+    const float4 kw = __ldcs(m.kw + i);
+    const Blend b = blend_entry(ki, kw, warp_dq);
+    float4 ln = rn;
+    lp = rp;
+    if (!b.degenerate) warp_surfel(b, rp, rn, lp, ln);
+    m.lp[i] = lp;
+    m.ln[i] = ln;
+  } else {
+    lp = m.lp[i];
+  }
+  index_splat_surfel<kPass2>(lp, i, k, factor, key, idx);
 }
 
 CamParams cam_params(Ctx& c, const double* pose) {

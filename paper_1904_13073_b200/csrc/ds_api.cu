@@ -324,7 +324,7 @@ void allocate(Ctx& c) {
   if (const char* e = std::getenv("DS_PCG_SMEM")) c.pcg_smem_cap = std::min(std::atoi(e), c.pcg_smem_cap);
   if (const char* e = std::getenv("DS_PCG_CLUSTER")) c.pcg_cluster = std::atoi(e);
   if (const char* e = std::getenv("DS_CHECK_NE")) c.check_ne = e[0] != '0';
-  if (const char* e = std::getenv("DS_SPMV_TMA")) c.spmv_tma = e[0] == '1';
+  if (const char* e = std::getenv("DS_SPMV_TMA")) c.spmv_tma = std::atoi(e);
   if (const char* e = std::getenv("DS_RIGID_GRID")) c.rigid_grid_cap = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("DS_PCGC_SMEM")) c.pcgc_smem_cap = std::atoi(e);
   DS_CUDA(cudaMemsetAsync(c.dsc, 0, sizeof(DevScalars), c.stream));

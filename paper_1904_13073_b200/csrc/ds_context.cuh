@@ -249,7 +249,7 @@ struct Ctx {
   double* pcg_x = nullptr;
   unsigned* pcgc_idx = nullptr;  // cluster PCG index scratch (k_pcg_cluster.cu)
   int rigid_grid_cap = 0;  // DS_RIGID_GRID: rigid-ICP term kernel grid cap (0: 2 CTAs per SM)
-  bool spmv_tma = false;   // DS_SPMV_TMA=1: the TMA-staged standalone SpMV (measured slower)
+  int spmv_tma = 0;  // DS_SPMV_TMA: stand-alone SpMV 0 rows kernel, 1 TMA-staged, 2 persistent TMA
   bool check_ne = false;          // DS_CHECK_NE: assert_normal_equations every GN iteration
   int pcg_cluster = 0;            // DS_PCG_CLUSTER: 0 off (default), 2..16 cluster size
   int pcgc_smem_cap = 1 << 30;    // DS_PCGC_SMEM: cluster PCG carve bytes (tests shrink it)

@@ -1,9 +1,11 @@
 """GPU parity of the solve, rigid alignment and fusion stages, and of whole
 sequences, against the oracle on identical inputs.
 
-Tolerances (fp32 surfel storage, fp32 JtJ blocks, PCG instead of dense LDLT):
-  node transforms after the full GN solve: <= 1e-4 (absolute on unit DQ parts)
-  warped positions after the solve: <= 1e-4 m
+Tolerances (fp32 surfel storage, fp32 JtJ blocks, PCG to 1e-12 instead of the
+dense LDLT), about 4x the gaps measured on B200:
+  iterations and correspondences of the full GN solve: equal
+  final energy: 1e-4 of the initial energy; node transforms: 5e-4 (unit DQ parts)
+  warped positions after the solve: 5e-5 m
   fusion outcome counts: exact on a shared state
 """
 import numpy as np
@@ -68,20 +70,24 @@ def test_solve_nonrigid_matches_oracle(scene, t_frame):
     pose = O.pose_identity()
     g = ctx.solve_nonrigid(pose, t_frame, 0)
     o = st.solve_nonrigid(pose, t_frame, 0)
-    assert g.correspondences == o.correspondences or g.iterations != o.iterations
-    assert abs(g.initial_energy - o.initial_energy) <= 1e-6 * o.initial_energy + 1e-15
+    # measured (round 2, B200): equal iterations and pairs, E_0 within 9e-15,
+    # E_final within 1.5e-5 E_0, node DQs within 1.2e-4, warped surfels within
+    # 1.2e-5 m, mean residual within 1e-7 (scripts/r02/solve_gaps.py)
+    assert g.iterations == o.iterations
+    assert g.correspondences == o.correspondences
+    assert abs(g.initial_energy - o.initial_energy) <= 1e-12 * o.initial_energy + 1e-18
     assert g.final_energy <= g.initial_energy
-    assert abs(g.final_energy - o.final_energy) <= 2e-2 * o.initial_energy + 1e-14
+    assert abs(g.final_energy - o.final_energy) <= 1e-4 * o.initial_energy + 1e-14
     gn, on = ctx.download_nodes(), st.get_nodes()
     # weakly observed nodes carry gauge freedom (solver.cpp:375-377): node-level
     # agreement is looser than the warped-surfel agreement below
-    assert dq_close(gn["dq"], on["dq"]) < 1e-3
+    assert dq_close(gn["dq"], on["dq"]) < 5e-4
     # warped surfels under both node sets
     ctx.forward_warp()
     st.forward_warp()
     gm, om = ctx.download_model(), st.get_model()
-    assert np.abs(gm["live_pos"] - om["live_pos"]).max() < 1e-4
-    assert abs(g.mean_residual - o.mean_residual) < 1e-4
+    assert np.abs(gm["live_pos"] - om["live_pos"]).max() < 5e-5
+    assert abs(g.mean_residual - o.mean_residual) < 1e-6
 
 
 def test_solve_tracks_small_deformation():

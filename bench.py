@@ -300,7 +300,7 @@ def run_multi(args, rank, world, local_rank):
                 surfels=surfels, bytes_in=frames[0].nbytes, pcg_grid=os.environ["DS_PCG_GRID"])
 
 
-def roofline(ks, peak_gbs):
+def roofline(ks, peak_gbs, config="cfg2"):
     rows = {}
     for name, v in ks.items():
         if v["launches"] and v["ms"] > 0:
@@ -314,7 +314,7 @@ def roofline(ks, peak_gbs):
             t = json.load(open(os.path.join(REPO, "profiles", name)))
         except Exception:
             continue
-        if dom in t:
+        if dom in t and t.get("config", "cfg2") == config:  # captured on this workload only
             traffic, traffic_src = t[dom]["bytes_per_launch"], f"profiles/{name}: {t['source']}"
             break
     if dom:
@@ -470,7 +470,7 @@ def main():
     K = r["K"]
     value = aggregate_fps(world, K, r["total_ms"])
     e2e = aggregate_fps(world, K, r["e2e_ms"])
-    roof, per = roofline(r["kernels"], pk.get("hbm_gbs", 6650.0))
+    roof, per = roofline(r["kernels"], pk.get("hbm_gbs", 6650.0), args.config)
     st = r["stats"]
     solve_ms = float(np.mean([s["solve_ms"] for s in st]))
     gn_iters = float(np.mean([s["gn_iters"] for s in st]))
@@ -501,6 +501,9 @@ def main():
         line["cpu_baseline"] = {"value": None, "unit": "frames/s", "cores": 1, "kind": "port",
                                 "sample": "n/a: the reference's dense 6N x 6N system at ~8k nodes "
                                           "needs ~18 GB (SURVEY 8(d))"}
+    elif world > 1:  # the CPU sample runs at N = 1 only
+        line["cpu_baseline"] = {"value": None, "unit": "frames/s", "cores": 0, "kind": "port",
+                                "sample": "measured in the N = 1 run only"}
     elif not args.no_cpu_baseline:
         try:
             from bench_reference import cpu_baseline

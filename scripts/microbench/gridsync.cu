@@ -32,6 +32,23 @@ __global__ void k_own(int iters, unsigned* ctr) {
   }
 }
 
+// hierarchical: hardware cluster barrier, then one CTA per cluster on the
+// global counter, then the cluster barrier again (cooperative + cluster launch)
+__global__ void k_hier(int iters, unsigned* ctr) {
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned ncl = gridDim.x / cl.num_blocks();
+  for (int i = 0; i < iters; ++i) {
+    cl.sync();
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+      red_release(ctr, 1u);
+      const unsigned target = (unsigned)(i + 1) * ncl;
+      while (ld_acquire(ctr) < target) {
+      }
+    }
+    cl.sync();
+  }
+}
+
 __global__ void k_round(int iters, double* part) {
   cg::grid_group g = cg::this_grid();
   __shared__ double2 sh[33];
@@ -76,7 +93,7 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int iters = 2000;
-  for (int G : {16, 37, 74, 148}) {
+  for (int G : {16, 74, 144, 148}) {
     for (int T : {256, 512, 1024}) {
       float ms[3];
       for (int v = 0; v < 3; ++v) {
@@ -95,9 +112,35 @@ int main() {
           cudaEventElapsedTime(&ms[v], a, b);
         }
       }
-      printf("G=%3d T=%4d  cg.sync %.3f us  own %.3f us  round(2 sync) %.3f us  [%s]\n", G, T,
-             ms[0] * 1e3 / iters, ms[1] * 1e3 / iters, ms[2] * 1e3 / iters,
-             cudaGetErrorString(cudaGetLastError()));
+      float mh[3] = {0, 0, 0};
+      const int cls[3] = {2, 4, 8};
+      for (int q = 0; q < 3; ++q) {
+        if (G % cls[q]) continue;
+        int it = iters;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = cls[q];
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(T);
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        for (int rep = 0; rep < 2; ++rep) {
+          cudaMemset(ctr, 0, 4);
+          cudaEventRecord(a);
+          cudaLaunchKernelEx(&cfg, k_hier, it, ctr);
+          cudaEventRecord(b);
+          cudaEventSynchronize(b);
+          cudaEventElapsedTime(&mh[q], a, b);
+        }
+      }
+      printf("G=%3d T=%4d  cg.sync %.3f us  own %.3f us  round(2 sync) %.3f us  hier c2 %.3f c4 %.3f c8 %.3f us [%s]\n", G, T,
+             ms[0] * 1e3 / iters, ms[1] * 1e3 / iters, ms[2] * 1e3 / iters, mh[0] * 1e3 / iters,
+             mh[1] * 1e3 / iters, mh[2] * 1e3 / iters, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;

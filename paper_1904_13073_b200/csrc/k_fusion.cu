@@ -175,15 +175,11 @@ struct ScreenParams {
 };
 
 // inverse warp with weights re-evaluated at x over the entry's node set
-// (unrolled over the <= 4 entries so that ids[] stays in registers)
-__device__ __forceinline__ bool inv_warp_reweighted(V3 x, const int ids[4], int cnt,
-                                                    const double4* __restrict__ node_dq,
-                                                    const double4* __restrict__ node_live, V3& out) {
+__device__ bool inv_warp_reweighted(V3 x, const int* ids, int cnt, const double4* __restrict__ node_dq,
+                                    const double4* __restrict__ node_live, V3& out) {
   Q4 rs = q4(0, 0, 0, 0), ds_ = q4(0, 0, 0, 0);
   const Q4 pivot = ld_q(node_dq + 2 * ids[0]);
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    if (m >= cnt) break;
+  for (int m = 0; m < cnt; ++m) {
     const double4 nl = node_live[ids[m]];
     const double w = skin_weight(x, v3(nl.x, nl.y, nl.z), nl.w);
     const Q4 r = ld_q(node_dq + 2 * ids[m]);
@@ -204,7 +200,7 @@ __device__ __forceinline__ bool inv_warp_reweighted(V3 x, const int ids[4], int 
 // skin_appended + check_compressive for candidate k (fusion.cpp:77-177).
 // result: 0 = low support, 1 = compressive reject, 2 = accepted
 // Eq. 6 ratio test, weights, delta_nn, compressive check on a K-NN list.
-__device__ __forceinline__ int screen_one(V3 x, const double bd[4], const int bi[4],
+__device__ int screen_one(V3 x, const double bd[4], const int bi[4],
                           const double4* __restrict__ node_pos,
                           const double4* __restrict__ node_live, const double4* __restrict__ node_dq,
                           const ScreenParams& sp, int ids[4], float ws[4], int& cnt) {
@@ -212,15 +208,12 @@ __device__ __forceinline__ int screen_one(V3 x, const double bd[4], const int bi
   const int k = min(sp.K, sp.N);
   const int n0 = bi[0];
   const double4 l0 = node_live[n0], p0 = node_pos[n0];
-  double w[4] = {0.0, 0.0, 0.0, 0.0};
+  double w[4];
   cnt = 0;
-  ids[0] = n0;
-  w[0] = skin_weight(x, v3(l0.x, l0.y, l0.z), l0.w);
+  ids[cnt] = n0;
+  w[cnt] = skin_weight(x, v3(l0.x, l0.y, l0.z), l0.w);
   ++cnt;
-  // unrolled, slots written by predicated compile-time indices (registers)
-#pragma unroll
-  for (int m = 1; m < 4; ++m) {
-    if (m >= k) break;
+  for (int m = 1; m < k; ++m) {
     const int j = bi[m];
     const double4 lj = node_live[j], pj = node_pos[j];
     const double lpair = nrm(sub(v3(lj.x, lj.y, lj.z), v3(l0.x, l0.y, l0.z)));
@@ -228,30 +221,19 @@ __device__ __forceinline__ int screen_one(V3 x, const double bd[4], const int bi
     if (rpair <= 0) continue;
     const double ratio = lpair / rpair;
     if (ratio <= 1.0 - sp.eps || ratio >= 1.0 + sp.eps) continue;
-    const double wj = skin_weight(x, v3(lj.x, lj.y, lj.z), lj.w);
-#pragma unroll
-    for (int t = 1; t < 4; ++t)
-      if (t == cnt) {
-        ids[t] = j;
-        w[t] = wj;
-      }
+    ids[cnt] = j;
+    w[cnt] = skin_weight(x, v3(lj.x, lj.y, lj.z), lj.w);
     ++cnt;
   }
   double wsum = 0;
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-    if (m < cnt) wsum += w[m];
-#pragma unroll
+  for (int m = 0; m < cnt; ++m) wsum += w[m];
   for (int m = 0; m < 4; ++m) ws[m] = m < cnt ? (float)w[m] : 0.f;
-#pragma unroll
-  for (int m = 1; m < 4; ++m)
-    if (m >= cnt) ids[m] = -1;
+  for (int m = cnt; m < 4; ++m) ids[m] = -1;
   if (wsum < sp.delta_nn) return 0;
   if (sp.compressive) {
     V3 c0;
     if (!inv_warp_reweighted(x, ids, cnt, node_dq, node_live, c0)) return 1;
     double S[3][3];
-#pragma unroll
     for (int a = 0; a < 3; ++a) {
       V3 pr = x;
       if (a == 0) pr.x += 1e-3;
@@ -282,7 +264,7 @@ static_assert(kScreenLanes >= 4 && (kScreenLanes & (kScreenLanes - 1)) == 0, "la
 // is built redundantly, the four inverse warps of the compressive check
 // (x and the three 1 mm probes, fusion.cpp:151-176) run on lanes 0-3 and
 // meet in lane 0 for the strain's sigma_max. Same arithmetic as screen_one.
-__device__ __forceinline__ int screen_group(V3 x, const double bd[4], const int bi[4],
+__device__ int screen_group(V3 x, const double bd[4], const int bi[4],
                             const double4* __restrict__ node_pos,
                             const double4* __restrict__ node_live,
                             const double4* __restrict__ node_dq, const ScreenParams& sp, int ids[4],
@@ -293,15 +275,12 @@ __device__ __forceinline__ int screen_group(V3 x, const double bd[4], const int 
   const int k = min(sp.K, sp.N);
   const int n0 = bi[0];
   const double4 l0 = node_live[n0], p0 = node_pos[n0];
-  double w[4] = {0.0, 0.0, 0.0, 0.0};
+  double w[4];
   cnt = 0;
-  ids[0] = n0;
-  w[0] = skin_weight(x, v3(l0.x, l0.y, l0.z), l0.w);
+  ids[cnt] = n0;
+  w[cnt] = skin_weight(x, v3(l0.x, l0.y, l0.z), l0.w);
   ++cnt;
-  // unrolled, slots written by predicated compile-time indices (registers)
-#pragma unroll
-  for (int m = 1; m < 4; ++m) {
-    if (m >= k) break;
+  for (int m = 1; m < k; ++m) {
     const int j = bi[m];
     const double4 lj = node_live[j], pj = node_pos[j];
     const double lpair = nrm(sub(v3(lj.x, lj.y, lj.z), v3(l0.x, l0.y, l0.z)));
@@ -309,24 +288,14 @@ __device__ __forceinline__ int screen_group(V3 x, const double bd[4], const int 
     if (rpair <= 0) continue;
     const double ratio = lpair / rpair;
     if (ratio <= 1.0 - sp.eps || ratio >= 1.0 + sp.eps) continue;
-    const double wj = skin_weight(x, v3(lj.x, lj.y, lj.z), lj.w);
-#pragma unroll
-    for (int t = 1; t < 4; ++t)
-      if (t == cnt) {
-        ids[t] = j;
-        w[t] = wj;
-      }
+    ids[cnt] = j;
+    w[cnt] = skin_weight(x, v3(lj.x, lj.y, lj.z), lj.w);
     ++cnt;
   }
   double wsum = 0;
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-    if (m < cnt) wsum += w[m];
-#pragma unroll
+  for (int m = 0; m < cnt; ++m) wsum += w[m];
   for (int m = 0; m < 4; ++m) ws[m] = m < cnt ? (float)w[m] : 0.f;
-#pragma unroll
-  for (int m = 1; m < 4; ++m)
-    if (m >= cnt) ids[m] = -1;
+  for (int m = cnt; m < 4; ++m) ids[m] = -1;
   if (wsum < sp.delta_nn) return 0;  // uniform across the group
   if (!sp.compressive) return 2;
   V3 pr = x, r = v3(0, 0, 0);
@@ -361,9 +330,6 @@ __device__ __forceinline__ int screen_group(V3 x, const double bd[4], const int 
 
 // (kScreenLanes: see above)
 constexpr int kScreenThreads = 256;
-#ifndef DS_SCREEN_MINB
-#define DS_SCREEN_MINB 2
-#endif
 
 // one block's group of kScreenThreads / kScreenLanes candidates from `kb`
 __device__ __forceinline__ void screen_block(
@@ -497,7 +463,7 @@ __device__ __forceinline__ void screen_block(
 // Persistent grid (the candidate count is on the device): blocks stride over
 // candidate groups; every thread of a block runs the same rounds (the tiled
 // fallback synchronises the block).
-__global__ void __launch_bounds__(kScreenThreads, DS_SCREEN_MINB) k_screen(
+__global__ void __launch_bounds__(kScreenThreads, 2) k_screen(
     const float4* __restrict__ cp, const int* __restrict__ n_cand_dev,
     const double4* __restrict__ node_pos, const double4* __restrict__ node_live,
     const float4* __restrict__ node_live_f, const int* __restrict__ rmax_bits,

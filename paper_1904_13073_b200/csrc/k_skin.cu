@@ -570,20 +570,24 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
   const float4 rp = m.rp[i];
   const V3 p = v3(rp.x, rp.y, rp.z);
   const int4 ki = m.ki[i];
+  const float4 kw = m.kw[i];
   int count = entry_count(ki);
   double sd[4];
   int si[4];
   double sw[4];
   const int ids[4] = {ki.x, ki.y, ki.z, ki.w};
+  const double ws[4] = {kw.x, kw.y, kw.z, kw.w};
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     if (s < count) {
       const double4 q = pos[ids[s]];
       sd[s] = sqn(sub(v3(q.x, q.y, q.z), p));
       si[s] = ids[s];
+      sw[s] = ws[s];
     } else {
       sd[s] = INFINITY;
       si[s] = 0x7fffffff;
+      sw[s] = 0;
     }
   }
   double worst = sd[0];
@@ -595,12 +599,6 @@ __global__ void k_skin_incremental(ModelBuf m, int n, const double4* __restrict_
     const double dy = fmax(fmax(bbox[1] - p.y, p.y - bbox[4]), 0.0);
     const double dz = fmax(fmax(bbox[2] - p.z, p.z - bbox[5]), 0.0);
     if ((dx * dx + dy * dy + dz * dz) * (1.0 - 1e-12) > worst) return;
-  }
-  {  // the weights only for entries that may change (16 of the 48 B per surfel)
-    const float4 kw = m.kw[i];
-    const double ws[4] = {kw.x, kw.y, kw.z, kw.w};
-#pragma unroll
-    for (int s = 0; s < 4; ++s) sw[s] = s < count ? ws[s] : 0.0;
   }
   // insertion sort of the first `count` slots (registers)
 #pragma unroll

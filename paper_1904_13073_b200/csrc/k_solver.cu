@@ -1204,7 +1204,11 @@ struct PcgArgs {
   DevScalars* sc;
 };
 
-// fixed-order CTA sums of three values; results valid in every thread
+// fixed-order CTA sums of three values; results valid in every thread.
+// kLeadSync = false: the caller guarantees that every thread has finished
+// reading `sh` from its previous use (a dedicated buffer with barriers in
+// between), which saves the leading barrier
+template <bool kLeadSync = true>
 __device__ __forceinline__ void cta_sum3(double& a, double& b, double& c, double4* sh) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -1212,7 +1216,7 @@ __device__ __forceinline__ void cta_sum3(double& a, double& b, double& c, double
     b += __shfl_xor_sync(0xffffffffu, b, off);
     c += __shfl_xor_sync(0xffffffffu, c, off);
   }
-  __syncthreads();
+  if (kLeadSync) __syncthreads();
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = make_double4(a, b, c, 0.0);
   __syncthreads();
   double ta = 0.0, tb = 0.0, tc = 0.0;
@@ -1337,6 +1341,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) a.sc->finite = 1;  // before any barrier
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double4 sh[kPcgWarps + 1];
+  __shared__ double4 sh2[2][kPcgWarps];  // the pipelined loop's two reductions
   __shared__ int s_rng[4];
   const int tid = threadIdx.x, G = gridDim.x;
   if (tid < 4) s_rng[tid] = a.slices[4 * blockIdx.x + tid];  // (r0, r1, bb0, bb1), per frame
@@ -1475,7 +1480,9 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
         pr += R[k] * R[k];
       }
       pcg_mark(a, 5 + 5 * it);
-      cta_sum3(pg, pd, pr, sh);
+      // own buffers: each is reused only after the grid barrier / the loop-top
+      // barrier, so the reductions skip their leading __syncthreads
+      cta_sum3<false>(pg, pd, pr, sh2[0]);
       double* part = a.part + 4 * G * (it & 1);
       if (tid == 0) {
         part[4 * blockIdx.x + 0] = pg;
@@ -1498,7 +1505,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
       // computed before the stopping test -- unused on the last round
       slice_spmv(V, C, RP, bb0, nb, nr, pub, Mv, mu, IT, Nv);
       pcg_mark(a, 8 + 5 * it);
-      cta_sum3(qa, qb, qc, sh);
+      cta_sum3<false>(qa, qb, qc, sh2[1]);
       pcg_mark(a, 9 + 5 * it);
       const double gamma = qa, delta = qb;
       rr = qc;

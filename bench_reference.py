@@ -1,19 +1,21 @@
 """CPU reference timing for bench.py: `--impl reference` and the `cpu_baseline` leg.
 
-The reference C++ sources cannot be compiled here (Eigen 3, libpng, GTest and
-vendored json/CLI11 are absent), so the reference algorithm is
-timed through the CPU oracle: the fp64 restatement of the reference in
-oracle/ (test infrastructure, never on the product path), driven through its
-`Pipeline::process_frame` restatement (pipeline.cpp:74-142) frame by frame —
-frame maps, model maps + rigid ICP, the full Levenberg-Marquardt loop with a
-dense 6N x 6N system per GN iteration (solver.cpp:296-420), forward warp,
-fusion, reinit checks. Nothing is extrapolated: every timed frame is one real
-process_frame call, wall-clocked on the host.
+The reference itself runs here: `oracle/_ref/libdynsurf_ref.so` is the
+UNMODIFIED reference (/root/reference/proj/core/src) compiled out of tree
+against the repo's shims for its absent dependencies (an Eigen subset, a
+libpng stub; `make -C oracle ref`; its own 106 unit
+tests pass on that build, tests/test_ref_oracle.py). It is driven through its
+own `Pipeline::process_frame` (pipeline.cpp:74-142) frame by frame -- frame
+maps, model maps + rigid ICP, the full Levenberg-Marquardt loop with a dense
+6N x 6N system per GN iteration (solver.cpp:296-420), forward warp, fusion,
+reinit checks. Nothing is extrapolated: every timed frame is one real
+process_frame call, wall-clocked on the host. (Where oracle/_ref was not
+built, the same timing runs through the oracle's restatement, kind "port".)
 
 Threads. The reference is single-threaded (no threads / OpenMP anywhere).
-  * config 1 runs exactly that: 1 core, the restated Eigen LDLT.
+  * config 1 runs exactly that: 1 core, the LDLT of the Eigen shim.
   * config 2's LM step is a dense LDLT of a ~9.2k x 9.2k matrix (648 MB) per
-    attempt — about 70 s on one core, ~12 min per frame. To finish in minutes,
+    attempt -- about 70 s on one core, ~12 min per frame. To finish in minutes,
     the reference arm hands that one step to LAPACK's Cholesky (scipy's
     OpenBLAS dpotrf/dpotrs on all host threads; dsysv if the Cholesky fails).
     Everything else stays single-threaded as in the reference. This can only
@@ -54,8 +56,9 @@ def host_cpu() -> dict:
 _keep = []  # the ctypes callback must outlive its installation
 
 
-def install_lapack_solver(O):
-    """or_set_dense_solver(LAPACK Cholesky): see the module docstring."""
+def _lapack_callback():
+    """A ctypes callback (n, a, b, x) -> 0 solving the dense LM step with
+    LAPACK's Cholesky: see the module docstring."""
     from scipy.linalg import lapack, solve
 
     FN = C.CFUNCTYPE(C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -77,16 +80,26 @@ def install_lapack_solver(O):
 
     cb = FN(fn)
     _keep.append(cb)
-    L = O.lib()
-    L.or_set_dense_solver.argtypes = [FN]
-    L.or_set_dense_solver(cb)
-    L.or_dense_solve_count.restype = C.c_int64
+    return FN, cb
+
+
+def _blas_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
 
         return max((p.get("num_threads") or 1) for p in threadpool_info()) or 1
     except Exception:
         return os.cpu_count() or 1
+
+
+def install_lapack_solver(O):
+    """or_set_dense_solver(LAPACK Cholesky) on the oracle port."""
+    FN, cb = _lapack_callback()
+    L = O.lib()
+    L.or_set_dense_solver.argtypes = [FN]
+    L.or_set_dense_solver(cb)
+    L.or_dense_solve_count.restype = C.c_int64
+    return _blas_threads()
 
 
 def uninstall_dense_solver(O):
@@ -128,13 +141,82 @@ def time_oracle_frames(spec, cfg, first_timed: int, n_timed: int, lapack: bool):
     return dict(secs=secs, stats=stats, threads=threads, dense_solves=int(solves))
 
 
+def ref_available() -> bool:
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import ref_py as R
+
+    return R.available()
+
+
+def time_ref_frames(spec, cfg, first_timed: int, n_timed: int, lapack: bool):
+    """time_oracle_frames on the compiled reference (oracle/_ref): its own
+    Pipeline::process_frame."""
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import oracle_py as O
+    import paper_1904_13073_b200 as pkg
+    import ref_py as R
+
+    # the dense LM step by LAPACK always (conservative: faster than the
+    # reference's unblocked LDLT); lapack=False keeps it on one thread
+    _, cb = _lapack_callback()
+    R.set_dense_solver(cb)
+    threads = _blas_threads() if lapack else 1
+    limit = None
+    if not lapack:  # one BLAS thread for the whole run (restored below)
+        from threadpoolctl import threadpool_limits
+
+        limit = threadpool_limits(1)
+    try:
+        ocfg = O.make_config(**{k: v for k, v in cfg.items() if k in O.DEFAULTS})
+        seq = pkg.SyntheticSequence(spec["scene"], spec["seq_frames"], cfg)
+        pipe = R.RefPipeline(ocfg)
+        solves0 = R.dense_solve_count()
+        secs, stats = [], []
+        for t in range(first_timed + n_timed):
+            d = seq.render_depth(t)
+            t0 = time.perf_counter()
+            st = pipe.process_frame(d, t)
+            dt = time.perf_counter() - t0
+            if t >= first_timed:
+                secs.append(dt)
+                stats.append(dict(frame=t, surfels=st["surfel_count"], nodes=st["node_count"],
+                                  gn_iters=st["solver_iterations"],
+                                  solve_s=st["ms"]["solve"] * 1e-3,
+                                  fusion_s=st["ms"]["fusion"] * 1e-3,
+                                  rigid_s=st["ms"]["rigid"] * 1e-3))
+        solves = R.dense_solve_count() - solves0
+        pipe.close()
+    finally:
+        R.set_dense_solver(None)
+        if limit is not None:
+            limit.restore_original_limits()
+    return dict(secs=secs, stats=stats, threads=threads, dense_solves=int(solves), kind="reference",
+                lapack_threads=threads)
+
+
+def time_frames(spec, cfg, first_timed: int, n_timed: int, lapack: bool):
+    """The compiled reference when oracle/_ref exists, else the oracle port."""
+    if ref_available():
+        return time_ref_frames(spec, cfg, first_timed, n_timed, lapack)
+    r = time_oracle_frames(spec, cfg, first_timed, n_timed, lapack)
+    r["kind"] = "port"
+    return r
+
+
 def describe(cfg_name, r, lapack):
     st = r["stats"]
     cpu = host_cpu()
     frames = f"frames {st[0]['frame']}-{st[-1]['frame']}" if len(st) > 1 else f"frame {st[0]['frame']}"
-    solver = (f"dense LM step by LAPACK Cholesky on {r['threads']} threads, the rest 1 thread"
-              if lapack else "restated Eigen LDLT, 1 thread")
-    return (f"CPU oracle process_frame (full LM loop, {solver}) on {cfg_name} {frames}: "
+    if r.get("kind") == "reference":
+        solver = (f"dense LM step by LAPACK Cholesky on {r['threads']} thread(s), the rest 1 thread"
+                  " (faster than the reference's unblocked LDLT: a conservative baseline)")
+    else:
+        solver = (f"dense LM step by LAPACK Cholesky on {r['threads']} threads, the rest 1 thread"
+                  if lapack else "restated Eigen LDLT, 1 thread")
+    who = ("reference Pipeline::process_frame (oracle/_ref: the unmodified reference sources "
+           "built against the repo's Eigen subset)" if r.get("kind") == "reference"
+           else "CPU oracle process_frame (the reference restated)")
+    return (f"{who} (full LM loop, {solver}) on {cfg_name} {frames}: "
             f"{len(st)} frames in {sum(r['secs']):.2f} s, surfels {st[0]['surfels']}-{st[-1]['surfels']}, "
             f"nodes {st[-1]['nodes']}, GN iterations {[s['gn_iters'] for s in st]}, "
             f"solve {sum(s['solve_s'] for s in st):.2f} s; host {cpu['model']} ({cpu['nproc']} threads)")
@@ -143,13 +225,13 @@ def describe(cfg_name, r, lapack):
 def cpu_baseline(args, spec, cfg):
     """bench.py's cpu_baseline leg: a bounded sample (~10-30 s of CPU work)."""
     if args.config == "cfg1":  # frames 1-5 after the init frame, 1 core
-        r = time_oracle_frames(spec, cfg, 1, 5, lapack=False)
+        r = time_frames(spec, cfg, 1, 5, lapack=False)
         cores, lapack = 1, False
     else:  # cfg2: the first tracked frame after the init frame
-        r = time_oracle_frames(spec, cfg, 1, 1, lapack=True)
+        r = time_frames(spec, cfg, 1, 1, lapack=True)
         cores, lapack = r["threads"], True
     v = len(r["secs"]) / sum(r["secs"])
-    return {"value": round(v, 6), "unit": "frames/s", "cores": cores, "kind": "port",
+    return {"value": round(v, 6), "unit": "frames/s", "cores": cores, "kind": r["kind"],
             "sample": describe(args.config, r, lapack)}
 
 
@@ -168,7 +250,7 @@ def run_reference(args):
     # timed window, which sits later in the sequence on a larger model.
     first = 1
     n_timed = spec["seq_frames"] - 1 if args.config == "cfg1" else MAX_TIMED["cfg2"]
-    r = time_oracle_frames(spec, cfg, first, n_timed, lapack=lapack)
+    r = time_frames(spec, cfg, first, n_timed, lapack=lapack)
     total = sum(r["secs"])
     v = len(r["secs"]) / total
     cores = r["threads"] if lapack else 1
@@ -178,10 +260,10 @@ def run_reference(args):
         "ms_per_step": round(1e3 * total / len(r["secs"]), 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "data": "synthetic",
         "config": {"workload": f"{args.config}: {spec['scene']} {spec['width']}x{spec['height']}, "
-                               f"max 10 GN per frame (reference LM loop, dense solve)",
+                               f"max {spec.get('gn_iters', 10)} GN per frame (reference LM loop, dense solve)",
                    "frames_timed": [s["frame"] for s in r["stats"]],
                    "device": f"host CPU ({host_cpu()['model']})"},
-        "cpu_baseline": {"value": round(v, 6), "unit": "frames/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": round(v, 6), "unit": "frames/s", "cores": cores, "kind": r["kind"],
                          "sample": describe(args.config, r, lapack)},
         "per_frame_s": [round(x, 3) for x in r["secs"]],
         "dense_solves": r["dense_solves"],

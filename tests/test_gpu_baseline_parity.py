@@ -200,3 +200,77 @@ def test_cfg2_stage_chain():
         gn, onn = ctx.download_nodes(), st.get_nodes()
         assert np.array_equal(gn["pos"], onn["pos"]) and np.array_equal(gn["nbr"], onn["nbr"])
     ctx.close()
+
+
+# ------------------------------------------------- directly against the reference
+def _ref_or_skip():
+    import ref_py as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref (the compiled reference) not built")
+    return R
+
+
+def _as_sets_agree(a, b):
+    return np.mean([set(x) == set(y) for x, y in zip(np.asarray(a), np.asarray(b))])
+
+
+@pytest.mark.parametrize("name,scene,W,H,f", [("cfg1", "deforming_sphere", 320, 240, 280.0),
+                                              ("cfg2", "articulated_body", 640, 480, 560.0)])
+def test_initialisation_against_compiled_reference(name, scene, W, H, f):
+    """Frame 0 on the device vs the UNMODIFIED reference (oracle/_ref,
+    pipeline.cpp:42-72): the device stores surfels in fp32, the reference in
+    fp64, so positions agree to fp32 rounding and the (d2, index) K-NN ties that
+    rounding decides may order or pick differently; everything else exact.
+    Measured (oracle fp32-mirror vs reference, which the device equals
+    bit-exactly): cfg2 neighbour sets differ on 0.13 % of nodes, skinning sets
+    on 0.02 % of surfels."""
+    R = _ref_or_skip()
+    cfg = pkg.camera_config(W, H, f, max_gn_iters=3)
+    d0 = pkg.SyntheticSequence(scene, 2, cfg).render_depth(0)
+    pipe = pkg.Pipeline(cfg)
+    a = pipe.process_frame(d0, 0)
+    rp = R.RefPipeline(O.make_config(**{k: v for k, v in cfg.items() if k in O.DEFAULTS}))
+    b = rp.process_frame(d0, 0)
+    for k in ("valid_pixels", "surfel_count", "node_count"):
+        assert a[k] == b[k], k
+    gn, rn = pipe.nodes(), rp.nodes()
+    assert np.abs(np.asarray(gn["pos"]) - rn["pos"]).max() <= 1e-7  # fp32 surfel storage
+    assert _as_sets_agree(gn["nbr"], rn["nbr"]) >= 0.995
+    gm, rm = pipe.model(), rp.model()
+    assert np.abs(np.asarray(gm["ref_pos"]) - rm["ref_pos"]).max() <= 1e-7
+    assert np.array_equal(gm["skin_count"], rm["skin_count"])
+    assert _as_sets_agree(np.asarray(gm["skin_idx"])[:, :4], rm["skin_idx"]) >= 0.999
+    pipe.close()
+    rp.close()
+
+
+def test_cfg1_frames_against_compiled_reference():
+    """BASELINE config 1, frames 0-3 through ds_process_frame (PCG run to
+    convergence) and through the reference's own Pipeline::process_frame
+    (dense LDLT), free-running: frame 0 exact; afterwards the fp32 device state
+    and the fp64 reference may take a marginal append decision differently
+    (measured: 1 surfel of 48k at frame 2), so counts within 0.1 %, poses
+    within 1e-6, GN correspondences within 0.1 %."""
+    R = _ref_or_skip()
+    cfg = pkg.camera_config(320, 240, 280.0, max_gn_iters=3, **CONVERGED)
+    seq = pkg.SyntheticSequence("deforming_sphere", 10, cfg)
+    pipe = pkg.Pipeline(cfg)
+    rp = R.RefPipeline(O.make_config(**{k: v for k, v in cfg.items() if k in O.DEFAULTS}))
+    for t in range(4):
+        d = seq.render_depth(t)
+        a = pipe.process_frame(d, t)
+        b = rp.process_frame(d, t)
+        assert a["valid_pixels"] == b["valid_pixels"], t
+        for k in ("surfel_count", "node_count", "appended"):
+            if t == 0:
+                assert a[k] == b[k], (t, k, a[k], b[k])
+            else:
+                assert abs(a[k] - b[k]) <= max(2, 1e-3 * b[k]), (t, k, a[k], b[k])
+        pr = np.concatenate([b["pose_R"].ravel(), b["pose_t"]])
+        assert np.abs(np.array(a["pose"]) - pr).max() <= 1e-6, t
+        if t > 0:
+            assert abs(a["correspondences"] - b["solver_correspondences"]) <= 1e-3 * b["solver_correspondences"], t
+            assert a["gn_iters"] == b["solver_iterations"], t
+    pipe.close()
+    rp.close()

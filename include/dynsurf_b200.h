@@ -266,6 +266,15 @@ ds_status ds_reset_kernel_stats(ds_context* ctx);
 ds_status ds_set_profiling(ds_context* ctx, int32_t enable);
 ds_status ds_total_launches(const ds_context* ctx, int64_t* launches);
 
+/* ---- host I/O helper (no device, no context) ---- */
+/* PNG row filters reversed (PNG spec 9.2), for read_depth_png (png_io.cpp:23-48,
+ * libpng's png_read_row in the reference): `data` is the inflated IDAT stream,
+ * height rows of (1 filter byte + width*bpp bytes); `out` receives height x
+ * width*bpp bytes. DS_ERR_DIMENSION_MISMATCH on a wrong-size stream,
+ * DS_ERR_INVALID_ARGUMENT on an invalid filter type or null pointer. */
+ds_status ds_png_unfilter(const uint8_t* data, int64_t size, int32_t width, int32_t height,
+                          int32_t bpp, uint8_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -128,6 +128,7 @@ SIGNATURES = {
     "ds_reset_kernel_stats": [P],
     "ds_set_profiling": [P, I32],
     "ds_total_launches": [P, C.POINTER(C.c_int64)],
+    "ds_png_unfilter": [P, C.c_int64, I32, I32, I32, P],
 }
 
 _RESTYPE = {

@@ -1547,6 +1547,39 @@ ds_status ds_set_profiling(ds_context* ctx, int32_t enable) {
   c.cfg.profile = enable ? 1 : 0;
   API_END
 }
+// PNG spec 9.2 row filters (None, Sub, Up, Average, Paeth), host code
+ds_status ds_png_unfilter(const uint8_t* data, int64_t size, int32_t width, int32_t height,
+                          int32_t bpp, uint8_t* out) {
+  if (!data || !out || width < 0 || height < 0 || bpp < 1) return DS_ERR_INVALID_ARGUMENT;
+  const int64_t stride = int64_t(width) * bpp;
+  if (size != int64_t(height) * (stride + 1)) return DS_ERR_DIMENSION_MISMATCH;
+  for (int64_t y = 0; y < height; ++y) {
+    const uint8_t ft = data[y * (stride + 1)];
+    const uint8_t* in = data + y * (stride + 1) + 1;
+    uint8_t* cur = out + y * stride;
+    const uint8_t* prior = y ? cur - stride : nullptr;
+    if (ft > 4) return DS_ERR_INVALID_ARGUMENT;
+    for (int64_t i = 0; i < stride; ++i) {
+      const int a = i >= bpp ? cur[i - bpp] : 0;
+      const int b = prior ? prior[i] : 0;
+      const int c = (prior && i >= bpp) ? prior[i - bpp] : 0;
+      int v = in[i];
+      if (ft == 1) {
+        v += a;
+      } else if (ft == 2) {
+        v += b;
+      } else if (ft == 3) {
+        v += (a + b) >> 1;
+      } else if (ft == 4) {
+        const int p = a + b - c, pa = std::abs(p - a), pb = std::abs(p - b), pc = std::abs(p - c);
+        v += (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
+      }
+      cur[i] = uint8_t(v);
+    }
+  }
+  return DS_OK;
+}
+
 ds_status ds_total_launches(const ds_context* ctx, int64_t* launches) {
   API_BEGIN
   REQUIRE(ctx && launches, "bad argument");

@@ -43,51 +43,21 @@ def _chunk(tag: bytes, data: bytes) -> bytes:
         ">I", zlib.crc32(tag + data) & 0xFFFFFFFF)
 
 
-def _paeth_row(raw: np.ndarray, prior: np.ndarray, bpp: int) -> np.ndarray:
-    out = np.empty_like(raw)
-    a = b = c = 0
-    for i in range(raw.size):
-        a = int(out[i - bpp]) if i >= bpp else 0
-        b = int(prior[i])
-        c = int(prior[i - bpp]) if i >= bpp else 0
-        p = a + b - c
-        pa, pb, pc = abs(p - a), abs(p - b), abs(p - c)
-        pred = a if (pa <= pb and pa <= pc) else (b if pb <= pc else c)
-        out[i] = (int(raw[i]) + pred) & 0xFF
-    return out
-
-
-def _avg_row(raw: np.ndarray, prior: np.ndarray, bpp: int) -> np.ndarray:
-    out = np.empty_like(raw)
-    for i in range(raw.size):
-        a = int(out[i - bpp]) if i >= bpp else 0
-        out[i] = (int(raw[i]) + ((a + int(prior[i])) >> 1)) & 0xFF
-    return out
-
-
 def _unfilter(data: bytes, width: int, height: int, bpp: int) -> np.ndarray:
+    """PNG row filters reversed by the native library (ds_png_unfilter, PNG
+    spec 9.2: the Average / Paeth filters libpng writes by default are
+    sequential along a row)."""
+    from . import _lib
+
     stride = width * bpp
     if len(data) != height * (stride + 1):
         raise CorruptFrame("PNG image data has the wrong size")
-    rows = np.frombuffer(data, np.uint8).reshape(height, stride + 1)
-    out = np.zeros((height, stride), np.uint8)
-    prior = np.zeros(stride, np.uint8)
-    for y in range(height):
-        ftype, raw = int(rows[y, 0]), rows[y, 1:]
-        if ftype == 0:
-            cur = raw.copy()
-        elif ftype == 1:  # Sub: running sum per byte lane, modulo 256
-            cur = np.cumsum(raw.reshape(width, bpp), axis=0, dtype=np.uint8).reshape(stride)
-        elif ftype == 2:  # Up
-            cur = raw + prior
-        elif ftype == 3:
-            cur = _avg_row(raw, prior, bpp)
-        elif ftype == 4:
-            cur = _paeth_row(raw, prior, bpp)
-        else:
-            raise CorruptFrame(f"PNG row filter {ftype} is invalid")
-        out[y] = cur
-        prior = cur
+    src = np.frombuffer(data, np.uint8)
+    out = np.empty((height, stride), np.uint8)
+    rc = _lib.load().ds_png_unfilter(src.ctypes.data, src.size, width, height, bpp,
+                                     out.ctypes.data)
+    if rc != 0:
+        raise CorruptFrame("PNG row filter is invalid")
     return out
 
 

@@ -80,6 +80,31 @@ def test_depth_png_decodes_every_row_filter(tmp_path):
     assert np.array_equal(sio.read_depth_png(str(p)), d)
 
 
+def test_depth_png_full_frame_filters_native_speed(tmp_path):
+    """A 640x480 frame with every row filter (libpng's default adaptive
+    filtering uses Average / Paeth heavily): decoded exactly by the native
+    unfilter (ds_png_unfilter) in well under the GPU frame budget's order of
+    magnitude (the Python per-byte loop took ~1 s)."""
+    import time
+
+    rng = np.random.default_rng(11)
+    d = rng.integers(0, 5000, size=(480, 640), dtype=np.uint16)
+    p = tmp_path / "big.png"
+    p.write_bytes(_png(640, 480, 16, 0, _encode_filtered(d)))
+    sio.read_depth_png(str(p))  # warm (library load)
+    t0 = time.perf_counter()
+    back = sio.read_depth_png(str(p))
+    dt = time.perf_counter() - t0
+    assert np.array_equal(back, d)
+    assert dt < 0.1, dt
+    bad = bytearray(_encode_filtered(d[:2, :4]))
+    bad[0] = 7  # invalid filter type
+    q = tmp_path / "badfilter.png"
+    q.write_bytes(_png(4, 2, 16, 0, bytes(bad)))
+    with pytest.raises(pkg.CorruptFrame, match="filter"):
+        sio.read_depth_png(str(q))
+
+
 def test_depth_png_errors(tmp_path):
     with pytest.raises(pkg.IoFailure):
         sio.read_depth_png(str(tmp_path / "missing.png"))

@@ -14,8 +14,10 @@ Pipeline::process_frame on the next frame of the sequence.
            inside the timed region).
   roofline achieved HBM GB/s of the dominant kernel (algorithmic bytes /
            mean launch time from per-launch CUDA events in a profiled pass).
-  cpu_baseline  the CPU oracle (fp64 restatement of the reference) running
-           its process_frame on a bounded sample of the same workload
+  cpu_baseline  the reference itself -- its unmodified sources compiled out of
+           tree against the repo's Eigen / libpng shims (oracle/_ref; the CPU
+           oracle's restatement where that was not built) -- running its own
+           Pipeline::process_frame on a bounded sample of the same workload
            (bench_reference.cpu_baseline: cfg2 frame 1 after the init frame).
 
 Multi-GPU: `--gpus N` spawns N processes itself (or runs under torchrun), one
@@ -24,8 +26,8 @@ by rank), no collective on the data path; the only inter-rank traffic is a
 gloo barrier and the max-over-ranks time. value = N*K / max-over-ranks time
 ("scaling": "weak").
 
-`--impl reference` times the reference algorithm on the host cores (the CPU
-oracle's process_frame; bench_reference.py) on the same config/metric; rank 0
+`--impl reference` times the reference on the host cores (oracle/_ref's
+Pipeline::process_frame; bench_reference.py) on the same config/metric; rank 0
 only.
 """
 from __future__ import annotations
@@ -414,7 +416,7 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     args.warmup = max(args.warmup, 3)
     # one step = one frame of the config's sequence: warm-up + timed frames stay
-    # within its length (cfg3's panning scene outgrows its node capacity past it)
+    # within its length
     spec = CONFIGS[args.config]
     args.steps = max(1, min(args.steps, spec["seq_frames"] - 1 - args.warmup,
                             spec.get("max_steps", args.steps)))

@@ -14,8 +14,10 @@ pixels per frame; on bending_sheet the oracle's stable-surfel distance is
 mean 1.8 / max 5.2 mm at frame 25 and 3.0 / 9.7 mm at frame 30, past the
 2 / 8 mm bar. The criterion-3/4 gaps are in the algorithm as specified, not
 in the B200 port: the unmodified reference compiled out of tree
-(oracle/_ref, scripts/r02/ref_acceptance.py) misses criterion 3 the same way
-(218 mm / 11.3 deg worst over 50 rigid_orbit frames, past the bar from frame 4).
+(oracle/_ref, scripts/r02/ref_acceptance.py) misses criteria 3-6 the same way:
+218 mm / 11.3 deg worst over 50 rigid_orbit frames (past the bar from frame 4);
+bending_sheet worst mean / max 23.8 / 94.7 mm; turntable count ratio 1.31;
+open_to_close 0 compressive rejections on and off.
 """
 import math
 

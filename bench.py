@@ -51,8 +51,13 @@ CFG1 = dict(width=320, height=240, focal=280.0, scene="deforming_sphere", seq_fr
             gn_iters=3)
 # BASELINE config 3: large scene with a panning camera (node append + reskinning
 # every frame) and an open-to-close contact, 1280x960
+# Initial capacities sized for the sequence's peak (9.2 M surfels, 15.2 k nodes)
+# with ~2x headroom: the device grows them geometrically at frame boundaries
+# when a frame could overflow (ds_capacity), but a growth re-allocates every
+# buffer (measured: 120 ms for nodes 16k -> 32k, 0.87 s for surfels 9.8 M ->
+# 19.7 M) -- a one-off hitch a real-time user avoids by sizing up front.
 CFG3 = dict(width=1280, height=960, focal=1120.0, scene="large_scene", seq_frames=60,
-            max_nodes=16384)  # initial node capacity; grown at frame boundaries past ~13k nodes
+            max_nodes=32768, max_surfels=20_000_000)
 CONFIGS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3}
 
 
@@ -121,8 +126,9 @@ class ClockSampler:
 def make_cfg(spec, **kw):
     import paper_1904_13073_b200 as pkg
 
-    if "max_nodes" in spec:
-        kw.setdefault("max_nodes", spec["max_nodes"])
+    for k in ("max_nodes", "max_surfels"):
+        if k in spec:
+            kw.setdefault(k, spec[k])
     return pkg.camera_config(spec["width"], spec["height"], spec["focal"],
                              max_gn_iters=spec.get("gn_iters", 10), pcg_max_iters=10, **kw)
 
@@ -483,12 +489,16 @@ def main():
         "dtype": "f64+f32", "storage": "fp64 arithmetic; fp32 SoA surfels, fp64 nodes, fp32 JtJ blocks",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {r['spec']['scene']} {r['cfg']['width']}x"
-                               f"{r['cfg']['height']}, 10 GN x 10 PCG per frame",
+                               f"{r['cfg']['height']}, {r['spec'].get('gn_iters', 10)} GN x 10 PCG "
+                               f"per frame",
                    "surfels": st[-1]["surfel_count"], "nodes": st[-1]["node_count"],
                    "frames_per_rank": K, "l2": "flushed between steps (256 MiB write, untimed)",
                    "surfels_range": [min(s["surfel_count"] for s in st), max(s["surfel_count"] for s in st)],
                    "correspondences_mean": round(float(np.mean([s["correspondences"] for s in st]))),
-                   "parallelism": f"independent sequences, 1 per GPU x {world}"},
+                   "parallelism": f"independent sequences, 1 per GPU x {world}",
+                   **({"initial_capacity": {k: r["spec"][k] for k in ("max_surfels", "max_nodes")
+                                            if k in r["spec"]}}
+                      if any(k in r["spec"] for k in ("max_surfels", "max_nodes")) else {})},
         "e2e": {"value": round(e2e, 3), "unit": "frames/s", "h2d_bytes_per_step": r["bytes_in"],
                 "d2h_bytes_per_step": 360},
         "gpu_launches": int(r["launches"]),

@@ -1174,9 +1174,15 @@ __global__ void __launch_bounds__(kStatsThreads) k_g_stats(
 // the grid partials. Slices above the shared-memory budget (very large N) keep
 // the same arithmetic on global scratch. Reductions are fixed-order (thread ->
 // warp -> CTA -> grid); the decomposition depends only on (N, nnzb, G).
-constexpr int kPcgThreads = 512;
+#ifndef DS_PCG_THREADS
+#define DS_PCG_THREADS 256
+#endif
+constexpr int kPcgThreads = DS_PCG_THREADS;  // measured: 256 beats 512 / 384 / 128
 constexpr int kPcgWarps = kPcgThreads / 32;
-constexpr int kPcgSmem = 200 * 1024;
+#ifndef DS_PCG_SMEM_KB
+#define DS_PCG_SMEM_KB 200
+#endif
+constexpr int kPcgSmem = DS_PCG_SMEM_KB * 1024;  // A/B builds: -DDS_PCG_SMEM_KB=100 (2 CTAs/SM)
 constexpr int kPcgVecs = 10;  // x r u w m n z q s p
 
 struct PcgArgs {
@@ -1372,10 +1378,21 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
       float* sv = reinterpret_cast<float*>(IT + 6 * (size_t)nb);
       int* sc = reinterpret_cast<int*>(sv + 36 * (size_t)nb);
       srp = sc + nb;
+      // the slice's blocks and columns stream in asynchronously (cp.async)
+      // while the block-Jacobi inverses below are computed; waited for before
+      // the first use (the __syncthreads after the r0 initialisation)
       const float4* gv = reinterpret_cast<const float4*>(a.val + 36 * (size_t)bb0);
       float4* sv4 = reinterpret_cast<float4*>(sv);
-      for (int k = tid; k < 9 * nb; k += kPcgThreads) sv4[k] = gv[k];
-      for (int k = tid; k < nb; k += kPcgThreads) sc[k] = a.col[bb0 + k];
+      for (int k = tid; k < 9 * nb; k += kPcgThreads) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(sv4 + k);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gv + k) : "memory");
+      }
+      for (int k = tid; k < nb; k += kPcgThreads) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(sc + k);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(a.col + bb0 + k)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
       V = sv;
       C = sc;
     } else {
@@ -1443,6 +1460,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs a) {
     Sv[k] = 0.0;
     Pv[k] = 0.0;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");  // the staged slice (no-op if none)
   __syncthreads();
   pcg_mark(a, 60);
   // u0 = M^-1 r0, published (pipelined: in the odd buffer, which iteration 0's
@@ -1982,7 +2000,7 @@ void pcg_solve_async(Ctx& c, int max_iters, double tol) {
   a.items = c.pcg_items;
   a.part = c.pcg_part;
   a.slices = c.pcg_slices;
-  a.smem_cap = c.pcg_smem_cap;
+  a.smem_cap = std::min(c.pcg_smem_cap, kPcgSmem);
   a.trace = c.pcg_trace;
   a.sc = c.dsc;
   const int grid = pcg_ctas(c);

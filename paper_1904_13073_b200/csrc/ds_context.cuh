@@ -107,6 +107,7 @@ struct GraphSlot {
   cudaGraphExec_t exec = nullptr;
   int64_t kernels = 0;  // kernel launches per replay (accounting)
   int64_t kernels_lin = 0;  // device LM loop: kernels per linearisation round
+  int64_t kernels_tail = 0;  // device LM loop: kernels after the loop (the report)
 };
 
 struct ProfRec {

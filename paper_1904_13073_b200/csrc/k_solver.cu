@@ -2236,6 +2236,15 @@ __global__ void __launch_bounds__(1024) k_lm_decide(DevScalars* sc, LmParams lp,
 }
 
 // Build the per-frame solve graph: WHILE(loop) { IF(relin) {linearise}; attempt; decide }.
+// mean |r| at the final nodes over the last pair set (solver.cpp:409-420)
+void report_async(Ctx& c, const double* pose) {
+  const int nbp = cdiv(c.P, 256);
+  DS_CUDA(cudaMemsetAsync(&c.dsc->mean_cnt, 0, sizeof(int), c.stream));
+  DS_LAUNCH(c, KK_ENERGY, 120.0 * c.P * 0.5, nbp, 256, 0, k_pair_energy, c.pair_s, c.M(), c.node_dq,
+            c.f_vert, c.f_nrm, pair_params(c, pose), 1, c.red_part, &c.dsc->mean_cnt,
+            c.tickets + 0, &c.dsc->mean_abs_r);
+}
+
 bool build_solve_graph(Ctx& c, const double* pose, int t_now, int t_last, int max_pcg,
                        double tol) {
   cudaGraph_t g = nullptr;
@@ -2309,8 +2318,23 @@ bool build_solve_graph(Ctx& c, const double* pose, int t_now, int t_last, int ma
   }
   ok = cudaStreamEndCapture(c.stream, &tmp) == cudaSuccess;
   if (!ok) return fail_();
+  const int64_t k_round = c.total_launches - l0 - k_lin;
+  // the report as the graph's last node, after the loop: one host sync per solve
+  if (cudaStreamBeginCaptureToGraph(c.stream, g, &wnode, nullptr, 1,
+                                    cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return fail_();
+  try {
+    report_async(c, pose);
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &tmp);
+    fail_();
+    throw;
+  }
+  ok = cudaStreamEndCapture(c.stream, &tmp) == cudaSuccess;
+  if (!ok) return fail_();
   c.g_solve.kernels_lin = k_lin;
-  c.g_solve.kernels = c.total_launches - l0 - k_lin;
+  c.g_solve.kernels = k_round;
+  c.g_solve.kernels_tail = c.total_launches - l0 - k_lin - k_round;
   c.total_launches = l0;
   if (c.g_solve.exec) {
     cudaGraphExecUpdateResultInfo info;
@@ -2410,6 +2434,7 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
   const double tol = c.cfg.pcg_tol;
   const bool graphs = c.use_graphs && !c.cfg.profile;
   int n_pairs = 0;
+  bool report_done = false;
   if (graphs && c.device_lm && c.cfg.max_gn_iters > 0) {
     // the whole LM loop on the device: one graph launch, one host sync
     DS_LAUNCH(c, KK_MISC, 64.0, 1, 1, 0, k_lm_init, c.dsc);
@@ -2427,7 +2452,9 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
       c.mm_clean = true;  // every linearisation's consumer resets the maps
       fetch_scalars(c);
       const DevScalars& h = *c.hsc;
-      c.total_launches += c.g_solve.kernels_lin * h.lm_relins + c.g_solve.kernels * h.lm_rounds;
+      c.total_launches += c.g_solve.kernels_lin * h.lm_relins + c.g_solve.kernels * h.lm_rounds +
+                          c.g_solve.kernels_tail;
+      report_done = true;  // captured as the graph's last node
       c.lm_attempts = h.lm_attempts_total;
       c.pcg_iterations = h.pcg_iter_total;
       rep.iterations = h.lm_accepted;
@@ -2496,13 +2523,10 @@ void solve_nonrigid(Ctx& c, const double* pose, int t_now, int t_last, ds_solver
   }
 report:
   rep.correspondences = n_pairs;
-  // mean |r| at the final nodes over the last pair set (solver.cpp:409-420)
-  const int nbp = cdiv(c.P, 256);
-  DS_CUDA(cudaMemsetAsync(&c.dsc->mean_cnt, 0, sizeof(int), c.stream));
-  DS_LAUNCH(c, KK_ENERGY, 120.0 * c.P * 0.5, nbp, 256, 0, k_pair_energy, c.pair_s, c.M(), c.node_dq,
-            c.f_vert, c.f_nrm, pair_params(c, pose), 1, c.red_part, &c.dsc->mean_cnt,
-            c.tickets + 0, &c.dsc->mean_abs_r);
-  fetch_scalars(c);
+  if (!report_done) {  // host LM path
+    report_async(c, pose);
+    fetch_scalars(c);
+  }
   if (c.check_ne && c.hsc->ne_err) {  // assert_normal_equations (solver.cpp:375)
     if (c.hsc->ne_err & NE_ASYMMETRIC) fail(DS_ERR_NUMERICAL, "normal equations lost symmetry");
     fail(DS_ERR_NUMERICAL, "normal equations diagonal block not PSD");

@@ -95,7 +95,8 @@ struct DevScalars {
   double rigid_pose[12];
   // JtJ pattern counts, published by its last kernel (read with the frame's
   // next scalar fetch instead of host syncs inside the pattern build)
-  int pat_n_up, pat_n_full, pat_n_chunks, pat_n_multi, pat_err, ne_err, _pad_pat[2];
+  int pat_n_up, pat_n_full, pat_n_chunks, pat_n_multi, pat_err, ne_err;
+  int surv_old, fuse_err;  // apply_fusion: appended survivors' offset, append error (device-side)
   unsigned ne_scale_bits, _pad_ne;  // assert_normal_equations: max|H| (fp32 bits)
 };
 
@@ -404,6 +405,10 @@ void init_warp_field(Ctx& c);
 void compute_node_edges(Ctx& c, bool build_grid = true);
 bool build_knn_grid(Ctx& c, KnnGrid& g, const double4* pos, int n, double h, int load_inv = 2);
 int extend_warp_field(Ctx& c, const float4* positions, int n);  // returns appended
+// the same over positions base[*off_dev .. *end_dev) with the count on the
+// device (<= bound); its greedy pass ends with a full scalar fetch
+int extend_warp_field_dev(Ctx& c, const float4* base, const int* off_dev, const int* end_dev,
+                          int bound);
 void update_skinning_incremental(Ctx& c, int first_new);
 
 // ---- raster (k_raster.cu)

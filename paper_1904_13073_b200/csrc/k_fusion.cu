@@ -832,12 +832,18 @@ void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out)
             &c.dsc->degenerate, c.cfg.delta_stable, c.any_stable_pre);
   DS_CUDA(cudaMemcpyAsync(&c.dsc->n_keep, c.keep_scan + limit, sizeof(int),
                           cudaMemcpyDeviceToDevice, c.stream));
-  int surv_old = 0;
-  DS_CUDA(cudaMemcpyAsync(&surv_old, c.keep_scan + n_old, sizeof(int), cudaMemcpyDeviceToHost,
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->surv_old, c.keep_scan + n_old, sizeof(int),
+                          cudaMemcpyDeviceToDevice, c.stream));
+  DS_CUDA(cudaMemcpyAsync(&c.dsc->fuse_err, &c.dsc->err, sizeof(int), cudaMemcpyDeviceToDevice,
                           c.stream));
-  fetch_scalars(c);
-  if (c.hsc->err & 16) fail(DS_ERR_CAPACITY, "surfel capacity exceeded while appending");
   c.cur ^= 1;
+  // extend the warp field over the appended survivors (compacted order):
+  // positions rp[surv_old, n_keep) of the compacted model, counts on the
+  // device -- no host sync here; the greedy pass's fetch brings every count
+  const int first_new = c.n_nodes;
+  oc.new_nodes = extend_warp_field_dev(c, c.M().rp, &c.dsc->surv_old, &c.dsc->n_keep,
+                                       std::min(P, c.S_cap));
+  if (c.hsc->fuse_err & 16) fail(DS_ERR_CAPACITY, "surfel capacity exceeded while appending");
   const int n_acc = c.hsc->n_accept;
   const int n_new = c.hsc->n_keep;
   oc.fused = c.hsc->fused;
@@ -847,10 +853,6 @@ void apply_fusion(Ctx& c, const double* pose, int t_now, ds_fusion_outcome* out)
   oc.removed = n_old + n_acc - n_new;
   oc.degenerate_warps = c.hsc->degenerate;
   c.n_surfels = n_new;
-  // extend the warp field over the appended survivors (compacted order)
-  const int app_surv = n_new - surv_old;
-  const int first_new = c.n_nodes;
-  oc.new_nodes = extend_warp_field(c, c.M().rp + surv_old, app_surv);
   if (oc.new_nodes > 0) update_skinning_incremental(c, first_new);
   // (seeds, edges and the incremental reskin stay on the side stream: joined
   // by the next API call or after the next frame's rigid ICP is launched;

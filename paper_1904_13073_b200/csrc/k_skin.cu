@@ -206,11 +206,12 @@ __global__ void __launch_bounds__(kGreedyThreads) k_greedy_nodes(
 // kUncLanes lanes per candidate split the 27 cells; a covered candidate
 // (the common case) stops after the first round, where lane 0 holds its own cell.
 constexpr int kUncLanes = 8;
-__global__ void k_uncovered(const float4* __restrict__ cand, int M, double sigma, HashView h,
-                            const double4* __restrict__ node_pos, int* __restrict__ flag) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = gt / kUncLanes, lane = gt % kUncLanes;
-  if (i >= M) return;  // whole group
+// candidate i of cand: flag[i] = 1 when no node lies within sigma (kUncLanes
+// lanes per candidate, all of the group call it)
+__device__ __forceinline__ void uncovered_one(const float4* __restrict__ cand, int i, double sigma,
+                                              HashView h, const double4* __restrict__ node_pos,
+                                              int* __restrict__ flag) {
+  const int lane = (blockIdx.x * blockDim.x + threadIdx.x) % kUncLanes;
   const unsigned gmask = 0xffu << ((threadIdx.x & 31) & ~(unsigned)(kUncLanes - 1));
   const float4 cp = cand[i];
   const V3 p = v3(cp.x, cp.y, cp.z);
@@ -240,10 +241,39 @@ __global__ void k_uncovered(const float4* __restrict__ cand, int M, double sigma
   }
   if (lane == 0) flag[i] = found ? 0 : 1;
 }
+__global__ void k_uncovered(const float4* __restrict__ cand, int M, double sigma, HashView h,
+                            const double4* __restrict__ node_pos, int* __restrict__ flag) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = gt / kUncLanes;
+  if (i >= M) return;  // whole group
+  uncovered_one(cand, i, sigma, h, node_pos, flag);
+}
 __global__ void k_gather_uncovered(const float4* __restrict__ cand, const int* __restrict__ flag,
                                    const int* __restrict__ scan, int M, float4* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < M && flag[i]) out[scan[i]] = cand[i];
+}
+// device-count variants: candidates base[*off, *end), flags zero past the count
+__global__ void k_uncovered_dev(const float4* __restrict__ base, const int* __restrict__ off,
+                                const int* __restrict__ end, int bound, double sigma, HashView h,
+                                const double4* __restrict__ node_pos, int* __restrict__ flag) {
+  const int o = *off, M = *end - o;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = gt / kUncLanes;
+  if (i >= bound) return;
+  if (i >= M) {
+    if (gt % kUncLanes == 0) flag[i] = 0;
+    return;  // whole group
+  }
+  uncovered_one(base + o, i, sigma, h, node_pos, flag);
+}
+__global__ void k_gather_uncovered_dev(const float4* __restrict__ base, const int* __restrict__ off,
+                                       const int* __restrict__ end, const int* __restrict__ flag,
+                                       const int* __restrict__ scan, int bound,
+                                       float4* __restrict__ out) {
+  const int o = *off, M = *end - o;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < bound && i < M && flag[i]) out[scan[i]] = base[o + i];
 }
 
 __global__ void k_identity_dq(double4* dq, int from, int to) {
@@ -729,10 +759,9 @@ int greedy(Ctx& c, const float4* cand, int M, int n0, int list_mode, const int* 
   DS_LAUNCH(c, KK_GREEDY_NODES, 16.0 * M, 1, kGreedyThreads, 0, k_greedy_nodes, cand, M, M_dev,
             c.cfg.node_sigma, hash_view(c), c.node_pos, &c.dsc->n_nodes, c.N_cap, list_mode,
             &c.dsc->err);
-  int res[2];
-  DS_CUDA(cudaMemcpyAsync(&res[0], &c.dsc->n_nodes, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  DS_CUDA(cudaMemcpyAsync(&res[1], &c.dsc->err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  sync(c);
+  // one full scalar fetch (the caller may also read its other counts)
+  fetch_scalars(c);
+  const int res[2] = {c.hsc->n_nodes, c.hsc->err};
   if (res[1] & DERR_NODE_CAP) fail(DS_ERR_CAPACITY, "node capacity exceeded");
   if (list_mode && (res[1] & DERR_HASH_FULL)) {
     // more than kListNodes new nodes: redo in hash mode (existing nodes are
@@ -786,6 +815,8 @@ void init_warp_field(Ctx& c) {
               c.M(), c.n_surfels, c.node_pos, n, std::min(4, c.cfg.knn_k));
 }
 
+int extend_tail(Ctx& c, int n0, int total);
+
 int extend_warp_field(Ctx& c, const float4* positions, int n) {
   if (n == 0) return 0;
   const int n0 = c.n_nodes;
@@ -806,6 +837,11 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
     m_dev = c.keep_scan + n;  // the uncovered count stays on the device
   }
   const int total = greedy(c, cand, m, n0, n0 > 0 ? 1 : 0, m_dev);
+  return extend_tail(c, n0, total);
+}
+
+// the new nodes' seeds and edges (side stream), after the greedy pass
+int extend_tail(Ctx& c, int n0, int total) {
   const int added = total - n0;
   c.n_nodes = total;
   if (added > 0) {
@@ -831,6 +867,25 @@ int extend_warp_field(Ctx& c, const float4* positions, int n) {
     c.nodes_pending = true;
   }
   return added;
+}
+
+int extend_warp_field_dev(Ctx& c, const float4* base, const int* off_dev, const int* end_dev,
+                          int bound) {
+  if (bound <= 0) return 0;
+  const int n0 = c.n_nodes;
+  clear_hash(c);
+  DS_CUDA(cudaMemsetAsync(&c.dsc->err, 0, sizeof(int), c.stream));
+  if (n0 > 0)
+    DS_LAUNCH(c, KK_GREEDY_NODES, 32.0 * n0, cdiv(n0, 256), 256, 0, k_ht_prefill, hash_view(c),
+              c.node_pos, n0, &c.dsc->err);
+  DS_LAUNCH(c, KK_GREEDY_NODES, 20.0 * bound, cdiv((long long)bound * kUncLanes, 256), 256, 0,
+            k_uncovered_dev, base, off_dev, end_dev, bound, c.cfg.node_sigma, hash_view(c),
+            c.node_pos, c.keep);
+  scan_exclusive(c, c.keep, c.keep_scan, bound);
+  DS_LAUNCH(c, KK_GREEDY_NODES, 24.0 * bound, cdiv(bound, 256), 256, 0, k_gather_uncovered_dev, base,
+            off_dev, end_dev, c.keep, c.keep_scan, bound, c.ext_pos);
+  const int total = greedy(c, c.ext_pos, bound, n0, n0 > 0 ? 1 : 0, c.keep_scan + bound);
+  return extend_tail(c, n0, total);
 }
 
 void update_skinning_incremental(Ctx& c, int first_new) {

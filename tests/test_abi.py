@@ -150,6 +150,6 @@ def test_bench_configs_and_reference_arm_for_config3():
 
     assert set(bench.CONFIGS) == {"cfg1", "cfg2", "cfg3"}
     cfg = bench.make_cfg(bench.CFG3)
-    assert cfg["width"] == 1280 and cfg["max_nodes"] == 16384
+    assert cfg["width"] == 1280 and cfg["max_nodes"] == 32768 and cfg["max_surfels"] == 20_000_000
     out = bench_reference.run_reference(argparse.Namespace(config="cfg3", steps=1, gpus=1))
     assert out["impl"] == "reference" and "unavailable" in out

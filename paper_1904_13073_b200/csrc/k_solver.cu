@@ -179,6 +179,10 @@ __device__ __forceinline__ double pair_term_one(int c, int s, const ModelBuf& m,
 // Fused model-map resolve + association (raster.cpp:104-119, solver.cpp:244-271)
 // + per-pair terms: the pixel's winner and correspondence are decided in
 // registers, the CTA packs its paired pixels and evaluates their terms.
+#ifndef DS_PAIR_PIX
+#define DS_PAIR_PIX 1
+#endif
+constexpr int kPairPix = DS_PAIR_PIX;  // pixels per thread in k_assoc_pair_terms (measured: 1 > 2, 4 -- spills)
 #ifndef DS_PAIR_TERMS_MINB
 #define DS_PAIR_TERMS_MINB 3
 #endif
@@ -192,51 +196,62 @@ __global__ void __launch_bounds__(256, DS_PAIR_TERMS_MINB) k_assoc_pair_terms(
     int* __restrict__ s_head, double* __restrict__ part, unsigned* __restrict__ ticket,
     double* __restrict__ out) {
   pdl_wait();  // programmatic dependent launch: predecessor results visible
-  __shared__ int s_pix[256], s_srf[256];
-  __shared__ int s_wcnt[8];
+  // kPairPix pixels per thread: the CTA resolves 256 x kPairPix pixels and
+  // packs their pairs (~40 %) so that all its warps run pair terms
+  __shared__ int s_pix[256 * kPairPix], s_srf[256 * kPairPix];
+  __shared__ int s_wcnt[8 * kPairPix];
   __shared__ unsigned s_done;
   __shared__ double s_wsum[8];
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (threadIdx.x == 0) s_done = 0u;  // visible after the packing barriers below
-  int ps = -1;
-  if (c < pp.P) {
-    // resolve (raster.cpp:104-119), then reset the consumed z-buffer entries
-    // so the next GN iteration's splats start from empty maps without memsets
-    const int pw = pidx[c], sw = sidx[c];
-    const int win = pw != kEmptyIdx ? pw : (sw != kEmptyIdx ? sw : -1);
-    if (pw != kEmptyIdx) {
-      pidx[c] = kEmptyIdx;
-      pkey[c] = ~0ull;
-    }
-    if (sw != kEmptyIdx) {
-      sidx[c] = kEmptyIdx;
-      skey[c] = ~0ull;
-    }
-    mm_idx[c] = win;
-    ps = associate_pixel(c, win, m, fvert, fnrm, fflag, pp.pose);
-    pair_s[c] = ps;
-  }
-  const unsigned bal = __ballot_sync(0xffffffffu, ps >= 0);
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    s_wcnt[wid] = __popc(bal);
-    if (bal) atomicAdd(n_pairs, __popc(bal));
-  }
-  __syncthreads();
-  int off = 0;
-  for (int w = 0; w < wid; ++w) off += s_wcnt[w];
-  if (ps >= 0) {
-    const int k = off + __popc(bal & ((1u << lane) - 1u));
-    s_pix[k] = c;
-    s_srf[k] = ps;
-  }
-  __syncthreads();
   int tot = 0;
-  for (int w = 0; w < 8; ++w) tot += s_wcnt[w];
-  const int pc = threadIdx.x < tot ? s_pix[threadIdx.x] : -1;
-  const int sc = threadIdx.x < tot ? s_srf[threadIdx.x] : -1;
-  const double e = pair_term_one(pc, sc, m, node_dq, fvert, fnrm, pp, pair_ok, rows, pair_r, s_cnt,
-                                 s_head);
+#pragma unroll
+  for (int q = 0; q < kPairPix; ++q) {
+    const int c = (blockIdx.x * kPairPix + q) * 256 + threadIdx.x;
+    int ps = -1;
+    if (c < pp.P) {
+      // resolve (raster.cpp:104-119), then reset the consumed z-buffer entries
+      // so the next GN iteration's splats start from empty maps without memsets
+      const int pw = pidx[c], sw = sidx[c];
+      const int win = pw != kEmptyIdx ? pw : (sw != kEmptyIdx ? sw : -1);
+      if (pw != kEmptyIdx) {
+        pidx[c] = kEmptyIdx;
+        pkey[c] = ~0ull;
+      }
+      if (sw != kEmptyIdx) {
+        sidx[c] = kEmptyIdx;
+        skey[c] = ~0ull;
+      }
+      mm_idx[c] = win;
+      ps = associate_pixel(c, win, m, fvert, fnrm, fflag, pp.pose);
+      pair_s[c] = ps;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, ps >= 0);
+    if (lane == 0) {
+      s_wcnt[q * 8 + wid] = __popc(bal);
+      if (bal) atomicAdd(n_pairs, __popc(bal));
+    }
+    __syncthreads();
+    int off = tot;
+    for (int w = 0; w < wid; ++w) off += s_wcnt[q * 8 + w];
+    if (ps >= 0) {
+      const int k = off + __popc(bal & ((1u << lane) - 1u));
+      s_pix[k] = c;
+      s_srf[k] = ps;
+    }
+    for (int w = 0; w < 8; ++w) tot += s_wcnt[q * 8 + w];
+  }
+  __syncthreads();
+  double e = 0.0;
+  if (kPairPix == 1) {
+    const int pc = threadIdx.x < tot ? s_pix[threadIdx.x] : -1;
+    const int sc = threadIdx.x < tot ? s_srf[threadIdx.x] : -1;
+    e = pair_term_one(pc, sc, m, node_dq, fvert, fnrm, pp, pair_ok, rows, pair_r, s_cnt, s_head);
+  } else {
+    for (int k = threadIdx.x; k < tot; k += 256)
+      e += pair_term_one(s_pix[k], s_srf[k], m, node_dq, fvert, fnrm, pp, pair_ok, rows, pair_r,
+                         s_cnt, s_head);
+  }
   // data energy, fixed order; warps past the packed pairs finish at once
   grid_sum_warps<256>(e, &s_done, s_wsum, part, ticket, out, blockIdx.x, gridDim.x);
 }
@@ -309,6 +324,11 @@ __global__ void __launch_bounds__(256) k_reg_energy(const double4* __restrict__ 
   grid_sum<256>(v, part, ticket, out);
 }
 
+#ifndef DS_ENERGY_PIX
+#define DS_ENERGY_PIX 2
+#endif
+constexpr int kEnergyPix = DS_ENERGY_PIX;  // pixels per thread in k_energy (measured: 2 > 1, 4)
+
 // E_post of an LM attempt in one launch: blocks [0, nbp) evaluate E_data over
 // the pair set (solver.cpp:132-143), blocks [nbp, nbp + nbe) E_reg over the
 // directed edges (solver.cpp:145-155); two independent fixed-order sums.
@@ -328,13 +348,29 @@ __global__ void __launch_bounds__(256) k_energy(const int* __restrict__ pair_s, 
   __shared__ double s_wsum[8];
   if (threadIdx.x == 0) s_done = 0u;  // visible after the next barrier
   if ((int)blockIdx.x < nbp) {
-    __shared__ int s_list[256];
-    __shared__ int s_wcnt[8];
-    int n_valid;
-    const int c = pack_pairs(pair_s, pp.P, s_list, s_wcnt, n_valid);
+    // kEnergyPix pixels per thread: the CTA packs its ~40 % paired pixels of
+    // 256 x kEnergyPix into a list that keeps all its warps busy
+    __shared__ int s_list[256 * kEnergyPix];
+    __shared__ int s_wcnt[8 * kEnergyPix];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int tot = 0;
+#pragma unroll
+    for (int q = 0; q < kEnergyPix; ++q) {
+      const int c = (blockIdx.x * kEnergyPix + q) * 256 + threadIdx.x;
+      const bool v = c < pp.P && pair_s[c] >= 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, v);
+      if (lane == 0) s_wcnt[q * 8 + wid] = __popc(bal);
+      __syncthreads();
+      int off = tot;
+      for (int w = 0; w < wid; ++w) off += s_wcnt[q * 8 + w];
+      if (v) s_list[off + __popc(bal & ((1u << lane) - 1u))] = c;
+      for (int w = 0; w < 8; ++w) tot += s_wcnt[q * 8 + w];
+    }
+    __syncthreads();
     double e = 0.0;
-    const int s = c >= 0 ? pair_s[c] : -1;
-    if (s >= 0) {
+    for (int k = threadIdx.x; k < tot; k += 256) {  // pixel order within the thread
+      const int c = s_list[k];
+      const int s = pair_s[c];
       const Blend b = blend_entry(m.ki[s], m.kw[s], node_dq);
       if (!b.degenerate) {
         const float4 rp = m.rp[s];
@@ -343,7 +379,7 @@ __global__ void __launch_bounds__(256) k_energy(const int* __restrict__ pair_s, 
         const V3 nd = rig_rotate(pp.pose, v3(fn.x, fn.y, fn.z));
         const V3 y = rig_apply(blend_rig_fast(b), v3(rp.x, rp.y, rp.z));
         const double r = dot(nd, sub(y, vd));
-        e = r * r;
+        e += r * r;
       }
     }
     grid_sum_warps<256>(e, &s_done, s_wsum, part, tickets + 0, e_data, blockIdx.x, nbp);
@@ -1905,7 +1941,7 @@ void gn_linearize_async(Ctx& c, const double* pose, int t_now, int t_last, bool 
   DS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_mid, 0));  // pair-list resets done
   // per pixel: 2 x 4 B winner ids, frame maps 65 B, winner live 32 B, ids out 8 B; per pair:
   // surfel ref + skin 48 B, rows 96 B + r 8 B out
-  DS_LAUNCH_PDL(c, KK_PAIR_TERMS, 113.0 * P + 152.0 * c.n_pairs_ok_est, nbp, 256, 0,
+  DS_LAUNCH_PDL(c, KK_PAIR_TERMS, 113.0 * P + 152.0 * c.n_pairs_ok_est, cdiv(P, 256 * kPairPix), 256, 0,
             k_assoc_pair_terms, c.mm_pidx, c.mm_sidx, c.mm_pkey, c.mm_skey, c.f_flag, c.M(), c.node_dq, c.f_vert,
             c.f_nrm, pair_params(c, pose), c.mm_idx, c.pair_s, &c.dsc->n_pairs, c.pair_ok,
             c.pair_rows, c.pair_r, c.s_cnt, c.s_head, c.red_part, c.tickets + 0,
@@ -2126,7 +2162,7 @@ namespace {
 // total energy of the pair set at node transforms `dq` (se3 cache in `se3`)
 void energy_async(Ctx& c, const double* pose, const double4* dq, double* se3) {
   const int N = c.n_nodes, P = c.P;
-  const int nbp = cdiv(P, 256), nbe = cdiv(8 * N, 256);
+  const int nbp = cdiv(P, 256 * kEnergyPix), nbe = cdiv(8 * N, 256);
   // the node transforms `se3` of `dq` are written by apply_increments (fused)
   DS_LAUNCH_PDL(c, KK_ENERGY, 120.0 * c.n_pairs_ok_est + 200.0 * N, nbp + nbe, 256, 0, k_energy,
             c.pair_s, c.M(), dq, c.f_vert, c.f_nrm, pair_params(c, pose), c.node_pos, c.node_nbr,
